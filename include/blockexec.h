@@ -1,0 +1,144 @@
+/*
+ * blockexec.h — C ABI of the B200 per-block batched execution path (BlockLLM, arXiv 2404.18322).
+ *
+ * The reference (blocksim, /root/reference/proj/core) has no GPU and no FFI: "running a block"
+ * is Simulation::batch_duration_us(const Instance&, const ExecBatch&) -> double µs
+ * (proj/core/include/blocksim/scenario.hpp:94, called only from pump, src/scenario.cpp:493),
+ * a cost-table lookup (CostModel::block_us, src/costmodel.cpp:96-105). This header is the seam a
+ * maintainer drops in at that call site: the host keeps its Instance/ExecBatch/KvStore state and
+ * hands the batch to be_exec_batch, which gathers the members' activation rows, runs the block's
+ * decoder layers on the GPU and scatters the outputs to their next-hop rows.
+ *
+ * Conventions: plain C types, device pointers where marked d_*, int status codes (BE_OK = 0),
+ * never throws; be_last_error() describes the last failure of a context. One host thread per
+ * context (the reference Engine is single-threaded). Work is asynchronous on the
+ * stream passed in (NULL = the context's stream).
+ */
+#ifndef BLOCKEXEC_H
+#define BLOCKEXEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BE_OK = 0,
+  BE_ERR_INVALID = 1,  /* bad argument: std::invalid_argument in the reference */
+  BE_ERR_STATE = 2,    /* misuse of an object: std::logic_error in the reference */
+  BE_ERR_CUDA = 3,     /* CUDA runtime/driver failure */
+  BE_ERR_NOMEM = 4,    /* device allocation failed (MemoryLedger over capacity) */
+  BE_ERR_RUNTIME = 5   /* std::runtime_error class ("run: ...") */
+};
+
+enum { BE_PHASE_PREFILL = 0, BE_PHASE_DECODE = 1 }; /* blocksim::Phase, costmodel.hpp:12 */
+
+typedef struct be_ctx be_ctx;
+typedef struct be_block be_block;
+typedef struct be_kv_pool be_kv_pool;
+typedef struct be_workspace be_workspace;
+
+/* A block = a contiguous run of Llama decoder layers (attention + ffn components of the zoo,
+ * zoo.hpp:29-54). Weights are synthetic (random init), generated on the device from
+ * (seed, name) by the counter-mode generator of oracle/synth.h. */
+typedef struct {
+  int n_layers;
+  int d_model;     /* embed_dim_in == embed_dim_out */
+  int n_heads;
+  int head_dim;
+  int d_ff;
+  int max_pos;     /* RoPE table length */
+  float norm_eps;
+  float rope_theta;
+  float init_scale; /* weights uniform in [-s, s] */
+  uint64_t seed;
+  const char* name; /* stream prefix, e.g. "b0" */
+} be_block_desc;
+
+/* One token row of an execution batch (decode: one per request; prefill: one per prompt token). */
+typedef struct {
+  int32_t src_row;   /* activation-arena row holding this token's block input */
+  int32_t dst_row;   /* arena row receiving this token's block output (-1: not stored) */
+  int32_t kv_slot;   /* physical KV token slot = page_slot * 16 + pos % 16 */
+  int32_t pos;       /* absolute position in its sequence (RoPE, causal extent) */
+  int32_t pt_row;    /* row of the page table naming this token's segment pages */
+} be_token;
+
+/* Context / device ------------------------------------------------------------------------ */
+int be_ctx_create(int device, be_ctx** out);
+int be_ctx_destroy(be_ctx* ctx);
+const char* be_last_error(const be_ctx* ctx);
+int be_ctx_num_sms(const be_ctx* ctx);
+void* be_ctx_stream(be_ctx* ctx); /* cudaStream_t */
+int be_synchronize(be_ctx* ctx);
+
+/* Blocks (weights) ------------------------------------------------------------------------- */
+int be_block_load(be_ctx* ctx, const be_block_desc* desc, be_block** out);
+int be_block_free(be_block* blk);
+int64_t be_block_param_bytes(const be_block* blk);
+/* bytes of K+V per token for the whole block: sum over its attention layers of 4*d
+ * (CostModel::kv_bytes_per_token, costmodel.cpp:114-127) */
+int64_t be_block_kv_bytes_per_token(const be_block* blk);
+
+/* Block-local paged KV pool: n_pages pages of 16 tokens (kv.hpp:16) x all layers ------------ */
+int be_kv_pool_create(be_ctx* ctx, const be_block* blk, int n_pages, be_kv_pool** out);
+int be_kv_pool_free(be_kv_pool* pool);
+void* be_kv_pool_data(be_kv_pool* pool); /* device base pointer: [page][layer][K|V][head][16][hd] */
+int64_t be_kv_pool_page_bytes(const be_kv_pool* pool);
+/* Synchronous copy of pool bytes [offset, offset+bytes) to host memory (tests / migration). */
+int be_kv_pool_read(be_kv_pool* pool, int64_t offset, int64_t bytes, void* host_dst);
+
+/* Scratch for one executing batch (sized for max_tokens tokens) ----------------------------- */
+int be_workspace_create(be_ctx* ctx, int d_model, int d_ff, int n_heads, int max_tokens,
+                        int max_rows, int max_pages_per_row, be_workspace** out);
+int be_workspace_free(be_workspace* ws);
+
+/* Execute one batch of one block instance (replaces Simulation::batch_duration_us).
+ * tokens: host array of n_tokens be_token; page_table: host [n_pt_rows][pt_stride] int32 of
+ * physical page slots; d_arena_in/out: device bf16 [rows][d_model] activation arenas (may alias).
+ * The metadata is staged into the workspace and uploaded on `stream`. */
+int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int phase,
+                  int n_tokens, const be_token* tokens, int n_pt_rows, int pt_stride,
+                  const int32_t* page_table, const void* d_arena_in, void* d_arena_out,
+                  void* stream);
+
+/* Same, with all metadata already on the device (CUDA-graph friendly: no host work besides
+ * launches). d_tokens: device be_token[n_tokens]; d_page_table: device int32. */
+int be_exec_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int phase,
+                      int n_tokens, const be_token* d_tokens, int pt_stride,
+                      const int32_t* d_page_table, const void* d_arena_in, void* d_arena_out,
+                      void* stream);
+
+/* K1 / K2 standalone: routing-table gather and scatter of bf16 rows. */
+int be_gather_rows(be_ctx* ctx, const void* d_arena, const int32_t* d_src, int rows, int d,
+                   void* d_out, void* stream);
+int be_scatter_rows(be_ctx* ctx, const void* d_rows, const int32_t* d_dst, int rows, int d,
+                    void* d_arena, void* stream);
+
+/* K7: per-row cosine(pred, actual) in fp32 and accept = cos >= threshold (PAPER.md:637 uses
+ * 0.95); the reference's scalar definition is signature_similarity, zoo.cpp:78-88. */
+int be_cosine(be_ctx* ctx, const void* d_pred, const void* d_actual, int rows, int d,
+              float threshold, float* d_cos, int32_t* d_accept, void* stream);
+
+/* Synthetic data: counter-mode generator shared with oracle/synth.h. */
+int be_synth_rows(be_ctx* ctx, void* d_dst, int64_t n_elems, uint64_t seed, const char* stream_id,
+                  float scale, void* stream);
+/* Copies one weight tensor of a block back in its LOGICAL layout (rows x cols, fp32 host array).
+ * tensor: "wq","wk","wv","wo","wg","wu","wd". For parity tests. */
+int be_block_read_weight(be_block* blk, int layer, const char* tensor, float* host_out);
+
+/* Low-level kernels exported for tests and the roofline bench ------------------------------ */
+/* out[t][f] = bf16(sum_k W[f][k] X[t][k]) with W [N][K], X [ntok][K] bf16 row-major. */
+int be_gemm_bf16(be_ctx* ctx, const void* d_w, const void* d_x, void* d_out, int N, int K,
+                 int ntok, int ksplit, void* stream);
+/* Paged attention over a pool (decode rows / causal prefill rows). */
+int be_attention(be_ctx* ctx, const void* d_q, const void* d_pool, int n_layers, int n_heads,
+                 int head_dim, int layer, const int32_t* d_page_table, int pt_stride,
+                 const int32_t* d_row_pt, const int32_t* d_row_ctx, int rows, int splits,
+                 void* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKEXEC_H */

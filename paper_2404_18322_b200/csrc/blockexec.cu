@@ -1,0 +1,763 @@
+// C-ABI implementation of include/blockexec.h: contexts, synthetic block weights, paged KV
+// pools, workspaces and the per-block batched execution (gather -> L x decoder layer -> scatter).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/blockexec.h"
+#include "gemm_tc.cuh"
+
+namespace bx {
+// rowops.cu
+cudaError_t launch_gather(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, float*, cudaStream_t);
+cudaError_t launch_scatter(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, cudaStream_t);
+cudaError_t launch_rms_stats(const float*, int, int, float, float*, cudaStream_t);
+cudaError_t launch_cosine(const __nv_bfloat16*, const __nv_bfloat16*, int, int, float, float*, int*, cudaStream_t);
+cudaError_t launch_synth_weight(__nv_bfloat16*, int, int, uint64_t, uint64_t, float, int, int, const float*, cudaStream_t);
+cudaError_t launch_synth_rows(__nv_bfloat16*, long long, uint64_t, float, cudaStream_t);
+cudaError_t launch_rope_table(float2*, int, int, double, cudaStream_t);
+// attention.cu
+struct AttnParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* pool;
+  long long page_elems;
+  long long layer_elems;
+  int layer;
+  const int* page_table;
+  int pt_stride;
+  const int* row_pt;
+  const int* row_ctx;
+  int meta_stride;
+  int ctx_add;
+  int H;
+  float scale_log2;
+  __nv_bfloat16* out;
+  float* part;
+  int splits;
+};
+cudaError_t launch_attention(const AttnParams&, int rows, int head_dim, cudaStream_t);
+}  // namespace bx
+
+using bx::EpiParams;
+using bf16 = __nv_bfloat16;
+
+// ------------------------------------------------------------------------------ objects
+struct be_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  // scratch for the standalone GEMM entry point
+  float* gemm_ws = nullptr;
+  size_t gemm_ws_elems = 0;
+  int* gemm_counters = nullptr;
+};
+
+struct be_block {
+  be_ctx* ctx = nullptr;
+  be_block_desc desc{};
+  std::string name;
+  bf16* slab = nullptr;
+  size_t slab_elems = 0;
+  float2* rope = nullptr;
+  struct Layer {
+    bf16 *wqkv, *wo, *wgu, *wd;
+    CUtensorMap m_qkv, m_o, m_gu, m_d;
+  };
+  std::vector<Layer> layers;
+};
+
+struct be_kv_pool {
+  be_ctx* ctx = nullptr;
+  bf16* base = nullptr;
+  int n_pages = 0;
+  long long page_elems = 0;
+  long long layer_elems = 0;
+  int n_layers = 0, n_heads = 0, head_dim = 0;
+};
+
+struct be_workspace {
+  be_ctx* ctx = nullptr;
+  int d = 0, dff = 0, H = 0, max_tok = 0, max_rows = 0, max_pages = 0;
+  float* X = nullptr;
+  bf16* Xb = nullptr;
+  bf16* q = nullptr;
+  bf16* attn = nullptr;
+  bf16* h = nullptr;
+  float* rstd = nullptr;
+  float* splitws = nullptr;
+  size_t splitws_elems = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
+  float* attn_part = nullptr;
+  size_t attn_part_elems = 0;
+  be_token* d_tokens = nullptr;
+  int32_t* d_pt = nullptr;
+  size_t pt_capacity = 0;
+  // TMA maps of the B operands by BN (16..256)
+  std::map<int, CUtensorMap> m_xb, m_attn, m_h;
+};
+
+// ------------------------------------------------------------------------------ helpers
+namespace {
+
+int fail(be_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx != nullptr) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return code;
+}
+
+#define BE_CUDA(ctx, call)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail((ctx), BE_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                                     \
+  } while (0)
+
+uint64_t fnv1a64(const std::string& s) {
+  uint64_t h = 14695981039346656037ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// Key of a synthetic stream: the splitmix64 seeding state of blocksim's RngStream
+// (proj/core/include/blocksim/rng.hpp:17-19): seed ^ fnv1a64(stream_id).
+uint64_t stream_key(uint64_t seed, const std::string& id) { return seed ^ fnv1a64(id); }
+
+std::string weight_stream(const std::string& block, int layer, const char* tensor) {
+  return "weights:" + block + ":" + std::to_string(layer) + ":" + tensor;
+}
+
+// 2D bf16 row-major [rows][cols] tensor map, box {64 cols, box_rows rows}, 128B swizzle.
+int make_map(be_ctx* ctx, CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+             uint32_t box_rows) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * sizeof(bf16)};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ctx, BE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u",
+                (int)r, (unsigned long long)rows, (unsigned long long)cols, box_rows);
+  return BE_OK;
+}
+
+cudaStream_t pick_stream(be_ctx* ctx, void* s) {
+  return s != nullptr ? static_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+const int kBNs[5] = {16, 32, 64, 128, 256};
+
+int attn_splits(const be_ctx* ctx, int rows, int H, int max_pages) {
+  const long long ctas = (long long)rows * H;
+  const long long want = 4LL * ctx->num_sms;
+  if (ctas >= want) return 1;
+  int s = (int)((want + ctas - 1) / ctas);
+  if (s > 16) s = 16;
+  const int cap = max_pages / 4 > 1 ? max_pages / 4 : 1;  // keep >= 4 pages per split
+  if (s > cap) s = cap;
+  return s < 1 ? 1 : s;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ context
+extern "C" int be_ctx_create(int device, be_ctx** out) {
+  if (out == nullptr) return BE_ERR_INVALID;
+  *out = nullptr;
+  auto* ctx = new be_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return BE_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (major != 10) {
+    delete ctx;
+    return BE_ERR_RUNTIME;  // sm_100a only
+  }
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return BE_ERR_CUDA;
+  }
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+          cudaSuccess ||
+      fn == nullptr) {
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return BE_ERR_CUDA;
+  }
+  ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  *out = ctx;
+  return BE_OK;
+}
+
+extern "C" int be_ctx_destroy(be_ctx* ctx) {
+  if (ctx == nullptr) return BE_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->gemm_ws) cudaFree(ctx->gemm_ws);
+  if (ctx->gemm_counters) cudaFree(ctx->gemm_counters);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return BE_OK;
+}
+
+extern "C" const char* be_last_error(const be_ctx* ctx) {
+  return ctx == nullptr ? "null context" : ctx->err.c_str();
+}
+extern "C" int be_ctx_num_sms(const be_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+extern "C" void* be_ctx_stream(be_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+extern "C" int be_synchronize(be_ctx* ctx) {
+  if (ctx == nullptr) return BE_ERR_INVALID;
+  BE_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  BE_CUDA(ctx, cudaGetLastError());
+  return BE_OK;
+}
+
+// ------------------------------------------------------------------------------ blocks
+extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out) {
+  if (ctx == nullptr || d == nullptr || out == nullptr) return BE_ERR_INVALID;
+  *out = nullptr;
+  if (d->n_layers <= 0 || d->d_model <= 0 || d->n_heads <= 0 || d->head_dim <= 0 ||
+      d->d_ff <= 0 || d->n_heads * d->head_dim != d->d_model)
+    return fail(ctx, BE_ERR_INVALID, "block: inconsistent shape");
+  if (d->d_model % 128 != 0 || d->d_ff % 64 != 0 || (2 * d->d_ff) % 128 != 0)
+    return fail(ctx, BE_ERR_INVALID, "block: d_model %% 128 and d_ff %% 64 required");
+  if (d->head_dim != 64 && d->head_dim != 128)
+    return fail(ctx, BE_ERR_INVALID, "block: head_dim must be 64 or 128");
+  if (d->max_pos <= 0) return fail(ctx, BE_ERR_INVALID, "block: max_pos must be positive");
+  cudaSetDevice(ctx->device);
+  auto* b = new be_block();
+  b->ctx = ctx;
+  b->desc = *d;
+  b->name = d->name ? d->name : "block";
+  b->desc.name = nullptr;
+  const size_t D = d->d_model, F = d->d_ff;
+  const size_t per_layer = 3 * D * D + D * D + 2 * F * D + D * F;
+  b->slab_elems = per_layer * d->n_layers;
+  if (cudaMalloc(&b->slab, b->slab_elems * sizeof(bf16)) != cudaSuccess) {
+    delete b;
+    return fail(ctx, BE_ERR_NOMEM, "block: weight slab (%zu B) allocation failed",
+                b->slab_elems * sizeof(bf16));
+  }
+  if (cudaMalloc(&b->rope, (size_t)d->max_pos * d->head_dim / 2 * sizeof(float2)) != cudaSuccess) {
+    cudaFree(b->slab);
+    delete b;
+    return fail(ctx, BE_ERR_NOMEM, "block: rope table allocation failed");
+  }
+  cudaStream_t st = ctx->stream;
+  bx::launch_rope_table(b->rope, d->max_pos, d->head_dim, (double)d->rope_theta, st);
+  const float s = d->init_scale;
+  b->layers.resize(d->n_layers);
+  for (int l = 0; l < d->n_layers; ++l) {
+    auto& L = b->layers[l];
+    L.wqkv = b->slab + per_layer * l;
+    L.wo = L.wqkv + 3 * D * D;
+    L.wgu = L.wo + D * D;
+    L.wd = L.wgu + 2 * F * D;
+    auto key = [&](const char* t) { return stream_key(d->seed, weight_stream(b->name, l, t)); };
+    bx::launch_synth_weight(L.wqkv, (int)D, (int)D, key("wq"), 0, s, 1, d->head_dim, nullptr, st);
+    bx::launch_synth_weight(L.wqkv + D * D, (int)D, (int)D, key("wk"), 0, s, 1, d->head_dim, nullptr, st);
+    bx::launch_synth_weight(L.wqkv + 2 * D * D, (int)D, (int)D, key("wv"), 0, s, 0, d->head_dim, nullptr, st);
+    bx::launch_synth_weight(L.wo, (int)D, (int)D, key("wo"), 0, s, 0, d->head_dim, nullptr, st);
+    bx::launch_synth_weight(L.wgu, (int)(2 * F), (int)D, key("wg"), key("wu"), s, 2, d->head_dim, nullptr, st);
+    bx::launch_synth_weight(L.wd, (int)D, (int)F, key("wd"), 0, s, 0, d->head_dim, nullptr, st);
+    int rc;
+    if ((rc = make_map(ctx, &L.m_qkv, L.wqkv, 3 * D, D, 128)) != BE_OK ||
+        (rc = make_map(ctx, &L.m_o, L.wo, D, D, 128)) != BE_OK ||
+        (rc = make_map(ctx, &L.m_gu, L.wgu, 2 * F, D, 128)) != BE_OK ||
+        (rc = make_map(ctx, &L.m_d, L.wd, D, F, 128)) != BE_OK) {
+      be_block_free(b);
+      return rc;
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    be_block_free(b);
+    return fail(ctx, BE_ERR_CUDA, "block init: %s", cudaGetErrorString(e));
+  }
+  *out = b;
+  return BE_OK;
+}
+
+extern "C" int be_block_free(be_block* b) {
+  if (b == nullptr) return BE_ERR_INVALID;
+  cudaSetDevice(b->ctx->device);
+  if (b->slab) cudaFree(b->slab);
+  if (b->rope) cudaFree(b->rope);
+  delete b;
+  return BE_OK;
+}
+
+extern "C" int64_t be_block_param_bytes(const be_block* b) {
+  return b ? (int64_t)(b->slab_elems * sizeof(bf16)) : 0;
+}
+
+extern "C" int64_t be_block_kv_bytes_per_token(const be_block* b) {
+  return b ? 4LL * b->desc.d_model * b->desc.n_layers : 0;
+}
+
+extern "C" int be_block_read_weight(be_block* b, int layer, const char* tensor, float* host_out) {
+  if (b == nullptr || tensor == nullptr || host_out == nullptr) return BE_ERR_INVALID;
+  be_ctx* ctx = b->ctx;
+  if (layer < 0 || layer >= b->desc.n_layers) return fail(ctx, BE_ERR_INVALID, "bad layer");
+  const int D = b->desc.d_model, F = b->desc.d_ff, hd = b->desc.head_dim;
+  const auto& L = b->layers[layer];
+  const std::string t = tensor;
+  const bf16* src = nullptr;
+  int rows = 0, cols = 0, perm = 0, parity = 0;
+  if (t == "wq") { src = L.wqkv; rows = D; cols = D; perm = 1; }
+  else if (t == "wk") { src = L.wqkv + (size_t)D * D; rows = D; cols = D; perm = 1; }
+  else if (t == "wv") { src = L.wqkv + 2 * (size_t)D * D; rows = D; cols = D; }
+  else if (t == "wo") { src = L.wo; rows = D; cols = D; }
+  else if (t == "wg") { src = L.wgu; rows = F; cols = D; perm = 2; parity = 0; }
+  else if (t == "wu") { src = L.wgu; rows = F; cols = D; perm = 2; parity = 1; }
+  else if (t == "wd") { src = L.wd; rows = D; cols = F; }
+  else return fail(ctx, BE_ERR_INVALID, "unknown tensor %s", tensor);
+  const int prow = perm == 2 ? 2 * rows : rows;
+  std::vector<bf16> tmp((size_t)prow * cols);
+  BE_CUDA(ctx, cudaMemcpy(tmp.data(), src, tmp.size() * sizeof(bf16), cudaMemcpyDeviceToHost));
+  for (int pr = 0; pr < prow; ++pr) {
+    int lr = pr;
+    if (perm == 1) {
+      const int h = pr / hd, e = pr % hd;
+      lr = h * hd + ((e & 1) ? (e >> 1) + hd / 2 : (e >> 1));
+    } else if (perm == 2) {
+      if ((pr & 1) != parity) continue;
+      lr = pr >> 1;
+    }
+    for (int c = 0; c < cols; ++c)
+      host_out[(size_t)lr * cols + c] = __bfloat162float(tmp[(size_t)pr * cols + c]);
+  }
+  return BE_OK;
+}
+
+// ------------------------------------------------------------------------------ KV pool
+extern "C" int be_kv_pool_create(be_ctx* ctx, const be_block* b, int n_pages, be_kv_pool** out) {
+  if (ctx == nullptr || b == nullptr || out == nullptr || n_pages <= 0) return BE_ERR_INVALID;
+  *out = nullptr;
+  cudaSetDevice(ctx->device);
+  auto* p = new be_kv_pool();
+  p->ctx = ctx;
+  p->n_pages = n_pages;
+  p->n_layers = b->desc.n_layers;
+  p->n_heads = b->desc.n_heads;
+  p->head_dim = b->desc.head_dim;
+  p->layer_elems = 2LL * p->n_heads * 16 * p->head_dim;
+  p->page_elems = p->layer_elems * p->n_layers;
+  const size_t bytes = (size_t)p->page_elems * n_pages * sizeof(bf16);
+  if (cudaMalloc(&p->base, bytes) != cudaSuccess) {
+    delete p;
+    return fail(ctx, BE_ERR_NOMEM, "kv pool: %zu B allocation failed", bytes);
+  }
+  cudaMemsetAsync(p->base, 0, bytes, ctx->stream);
+  *out = p;
+  return BE_OK;
+}
+
+extern "C" int be_kv_pool_free(be_kv_pool* p) {
+  if (p == nullptr) return BE_ERR_INVALID;
+  cudaSetDevice(p->ctx->device);
+  if (p->base) cudaFree(p->base);
+  delete p;
+  return BE_OK;
+}
+
+extern "C" void* be_kv_pool_data(be_kv_pool* p) { return p ? p->base : nullptr; }
+extern "C" int64_t be_kv_pool_page_bytes(const be_kv_pool* p) {
+  return p ? p->page_elems * (int64_t)sizeof(bf16) : 0;
+}
+
+extern "C" int be_kv_pool_read(be_kv_pool* p, int64_t offset, int64_t bytes, void* host_dst) {
+  if (p == nullptr || host_dst == nullptr || offset < 0 || bytes < 0 ||
+      offset + bytes > p->page_elems * (int64_t)sizeof(bf16) * p->n_pages)
+    return BE_ERR_INVALID;
+  cudaSetDevice(p->ctx->device);
+  BE_CUDA(p->ctx, cudaStreamSynchronize(p->ctx->stream));
+  BE_CUDA(p->ctx, cudaMemcpy(host_dst, reinterpret_cast<const char*>(p->base) + offset, bytes,
+                             cudaMemcpyDeviceToHost));
+  return BE_OK;
+}
+
+// ------------------------------------------------------------------------------ workspace
+extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_tok, int max_rows,
+                                   int max_pages, be_workspace** out) {
+  if (ctx == nullptr || out == nullptr || d <= 0 || dff <= 0 || H <= 0 || max_tok <= 0 ||
+      max_rows <= 0 || max_pages <= 0)
+    return BE_ERR_INVALID;
+  *out = nullptr;
+  cudaSetDevice(ctx->device);
+  auto* w = new be_workspace();
+  w->ctx = ctx;
+  w->d = d;
+  w->dff = dff;
+  w->H = H;
+  w->max_tok = max_tok;
+  w->max_rows = max_rows;
+  w->max_pages = max_pages;
+  const size_t T = max_tok;
+  bool ok = true;
+  ok &= cudaMalloc(&w->X, T * d * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&w->Xb, T * d * sizeof(bf16)) == cudaSuccess;
+  ok &= cudaMalloc(&w->q, T * d * sizeof(bf16)) == cudaSuccess;
+  ok &= cudaMalloc(&w->attn, T * d * sizeof(bf16)) == cudaSuccess;
+  ok &= cudaMalloc(&w->h, T * dff * sizeof(bf16)) == cudaSuccess;
+  ok &= cudaMalloc(&w->rstd, T * sizeof(float)) == cudaSuccess;
+  w->splitws_elems = (size_t)16 << 20;  // 64 MB of fp32 split-K partials (L2 sized)
+  ok &= cudaMalloc(&w->splitws, w->splitws_elems * sizeof(float)) == cudaSuccess;
+  w->n_counters = 1 << 16;
+  ok &= cudaMalloc(&w->counters, w->n_counters * sizeof(int)) == cudaSuccess;
+  const size_t part_rows = T < 1024 ? T : 1024;
+  w->attn_part_elems = part_rows * H * 16 * (128 + 2);
+  ok &= cudaMalloc(&w->attn_part, w->attn_part_elems * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&w->d_tokens, T * sizeof(be_token)) == cudaSuccess;
+  w->pt_capacity = (size_t)max_rows * max_pages;
+  ok &= cudaMalloc(&w->d_pt, w->pt_capacity * sizeof(int32_t)) == cudaSuccess;
+  if (!ok) {
+    be_workspace_free(w);
+    return fail(ctx, BE_ERR_NOMEM, "workspace allocation failed (max_tok=%d)", max_tok);
+  }
+  cudaMemsetAsync(w->counters, 0, w->n_counters * sizeof(int), ctx->stream);
+  cudaMemsetAsync(w->X, 0, T * d * sizeof(float), ctx->stream);
+  cudaMemsetAsync(w->Xb, 0, T * d * sizeof(bf16), ctx->stream);
+  cudaMemsetAsync(w->attn, 0, T * d * sizeof(bf16), ctx->stream);
+  cudaMemsetAsync(w->h, 0, T * dff * sizeof(bf16), ctx->stream);
+  for (int bn : kBNs) {
+    CUtensorMap a, b2, c;
+    int rc;
+    if ((rc = make_map(ctx, &a, w->Xb, T, d, bn)) != BE_OK ||
+        (rc = make_map(ctx, &b2, w->attn, T, d, bn)) != BE_OK ||
+        (rc = make_map(ctx, &c, w->h, T, dff, bn)) != BE_OK) {
+      be_workspace_free(w);
+      return rc;
+    }
+    w->m_xb[bn] = a;
+    w->m_attn[bn] = b2;
+    w->m_h[bn] = c;
+  }
+  *out = w;
+  return BE_OK;
+}
+
+extern "C" int be_workspace_free(be_workspace* w) {
+  if (w == nullptr) return BE_ERR_INVALID;
+  cudaSetDevice(w->ctx->device);
+  void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->rstd, w->splitws, w->counters,
+                  w->attn_part, w->d_tokens, w->d_pt};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete w;
+  return BE_OK;
+}
+
+// ------------------------------------------------------------------------------ execution
+namespace {
+
+int run_gemm(be_ctx* ctx, be_workspace* ws, const CUtensorMap* mw, const CUtensorMap* mx, int N,
+             int K, int ntok, int bn, EpiParams epi, cudaStream_t st) {
+  bx::GemmLaunch L{};
+  L.map_w = mw;
+  L.map_x = mx;
+  L.N = N;
+  L.K = K;
+  L.bn = bn;
+  int ks = bx::gemm_pick_ksplit(N, K, ntok, bn, ctx->num_sms);
+  const int ntiles = (ntok + bn - 1) / bn;
+  while (ks > 1 && ((size_t)ks * ntiles * bn * N > ws->splitws_elems ||
+                    (N / 128) * ntiles > ws->n_counters))
+    --ks;
+  L.ksplit = ks;
+  epi.ws = ws->splitws;
+  epi.counters = ws->counters;
+  L.epi = epi;
+  cudaError_t e = bx::launch_gemm(L, st);
+  if (e != cudaSuccess)
+    return fail(ctx, BE_ERR_CUDA, "gemm N=%d K=%d ntok=%d: %s", N, K, ntok, cudaGetErrorString(e));
+  return BE_OK;
+}
+
+int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int phase,
+             int ntok, const be_token* d_tok, int pt_stride, const int32_t* d_pt,
+             const void* arena_in, void* arena_out, cudaStream_t st) {
+  (void)phase;
+  const auto& D = blk->desc;
+  const int d = D.d_model, F = D.d_ff, H = D.n_heads, hd = D.head_dim;
+  if (ws->d != d || ws->dff != F || ws->H != H)
+    return fail(ctx, BE_ERR_INVALID, "workspace shape does not match block");
+  if (ntok > ws->max_tok) return fail(ctx, BE_ERR_INVALID, "batch of %d tokens > workspace %d", ntok, ws->max_tok);
+  if (pool->n_layers != D.n_layers || pool->n_heads != H || pool->head_dim != hd)
+    return fail(ctx, BE_ERR_INVALID, "kv pool shape does not match block");
+  if (ntok == 0) return BE_OK;
+  const int* tok = reinterpret_cast<const int*>(d_tok);
+  const int bn = bx::gemm_pick_bn(ntok);
+  cudaError_t e;
+
+  // K1: gather the members' input rows into the batch (fp32 residual + bf16 shadow)
+  e = bx::launch_gather(static_cast<const bf16*>(arena_in), tok + 0, 5, ntok, d, ws->Xb, ws->X, st);
+  if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
+
+  const int max_pages = pt_stride;
+  const int splits = attn_splits(ctx, ntok, H, max_pages);
+  if ((size_t)ntok * H * splits * (hd + 2) > ws->attn_part_elems && splits > 1)
+    return fail(ctx, BE_ERR_INVALID, "attention partial buffer too small");
+
+  for (int l = 0; l < D.n_layers; ++l) {
+    const auto& L = blk->layers[l];
+    int rc;
+    // ---- attention component: RMSNorm (fused) -> QKV + RoPE + KV append -> paged attn -> O + residual
+    e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
+    if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
+    EpiParams eq{};
+    eq.mode = bx::kQKV;
+    eq.ntok = ntok;
+    eq.rstd = ws->rstd;
+    eq.out = ws->q;
+    eq.ldo = d;
+    eq.tok = tok;
+    eq.kv_pool = pool->base;
+    eq.page_elems = pool->page_elems;
+    eq.layer_elems = pool->layer_elems;
+    eq.layer = l;
+    eq.d_model = d;
+    eq.head_dim = hd;
+    eq.rope = blk->rope;
+    if ((rc = run_gemm(ctx, ws, &L.m_qkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st)) != BE_OK) return rc;
+
+    bx::AttnParams ap{};
+    ap.q = ws->q;
+    ap.pool = pool->base;
+    ap.page_elems = pool->page_elems;
+    ap.layer_elems = pool->layer_elems;
+    ap.layer = l;
+    ap.page_table = d_pt;
+    ap.pt_stride = pt_stride;
+    ap.row_pt = tok + 4;
+    ap.row_ctx = tok + 3;
+    ap.meta_stride = 5;
+    ap.ctx_add = 1;  // a token sees positions [0, pos]
+    ap.H = H;
+    ap.scale_log2 = (1.0f / sqrtf((float)hd)) * 1.4426950408889634f;
+    ap.out = ws->attn;
+    ap.part = ws->attn_part;
+    ap.splits = splits;
+    e = bx::launch_attention(ap, ntok, hd, st);
+    if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "attention: %s", cudaGetErrorString(e));
+
+    EpiParams eo{};
+    eo.mode = bx::kResid;
+    eo.ntok = ntok;
+    eo.xres = ws->X;
+    eo.xres_b = ws->Xb;
+    eo.ldr = d;
+    if ((rc = run_gemm(ctx, ws, &L.m_o, &ws->m_attn[bn], d, d, ntok, bn, eo, st)) != BE_OK) return rc;
+
+    // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
+    e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
+    if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
+    EpiParams eg{};
+    eg.mode = bx::kSwiGLU;
+    eg.ntok = ntok;
+    eg.rstd = ws->rstd;
+    eg.out = ws->h;
+    eg.ldo = F;
+    if ((rc = run_gemm(ctx, ws, &L.m_gu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st)) != BE_OK) return rc;
+    EpiParams ed{};
+    ed.mode = bx::kResid;
+    ed.ntok = ntok;
+    ed.xres = ws->X;
+    ed.xres_b = ws->Xb;
+    ed.ldr = d;
+    if ((rc = run_gemm(ctx, ws, &L.m_d, &ws->m_h[bn], d, F, ntok, bn, ed, st)) != BE_OK) return rc;
+  }
+  // K2: scatter the block outputs to their next-hop rows
+  e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st);
+  if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "scatter: %s", cudaGetErrorString(e));
+  return BE_OK;
+}
+
+}  // namespace
+
+extern "C" int be_exec_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws,
+                                 int phase, int n_tokens, const be_token* d_tokens, int pt_stride,
+                                 const int32_t* d_page_table, const void* d_arena_in,
+                                 void* d_arena_out, void* stream) {
+  if (ctx == nullptr || blk == nullptr || pool == nullptr || ws == nullptr || n_tokens < 0 ||
+      (n_tokens > 0 && (d_tokens == nullptr || d_page_table == nullptr || d_arena_in == nullptr ||
+                        d_arena_out == nullptr)) ||
+      pt_stride <= 0)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_batch_dev: bad arguments") : BE_ERR_INVALID;
+  if (phase != BE_PHASE_PREFILL && phase != BE_PHASE_DECODE)
+    return fail(ctx, BE_ERR_INVALID, "unknown phase %d", phase);
+  return exec_dev(ctx, blk, pool, ws, phase, n_tokens, d_tokens, pt_stride, d_page_table,
+                  d_arena_in, d_arena_out, pick_stream(ctx, stream));
+}
+
+extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws,
+                             int phase, int n_tokens, const be_token* tokens, int n_pt_rows,
+                             int pt_stride, const int32_t* page_table, const void* d_arena_in,
+                             void* d_arena_out, void* stream) {
+  if (ctx == nullptr || blk == nullptr || pool == nullptr || ws == nullptr || n_tokens < 0 ||
+      (n_tokens > 0 && tokens == nullptr) || pt_stride <= 0 || n_pt_rows < 0)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_batch: bad arguments") : BE_ERR_INVALID;
+  if (n_tokens > ws->max_tok)
+    return fail(ctx, BE_ERR_INVALID, "batch of %d tokens > workspace %d", n_tokens, ws->max_tok);
+  if ((size_t)n_pt_rows * pt_stride > ws->pt_capacity)
+    return fail(ctx, BE_ERR_INVALID, "page table %dx%d exceeds workspace", n_pt_rows, pt_stride);
+  // host-side validation of the routing metadata (the kernels trust it)
+  const int64_t kv_slots = (int64_t)pool->n_pages * 16;
+  for (int t = 0; t < n_tokens; ++t) {
+    const be_token& k = tokens[t];
+    if (k.pt_row < 0 || k.pt_row >= n_pt_rows || k.pos < 0 || k.kv_slot < 0 ||
+        k.kv_slot >= kv_slots || (k.kv_slot & 15) != (k.pos & 15) || k.src_row < 0 ||
+        (k.pos >> 4) >= pt_stride || k.pos >= blk->desc.max_pos)
+      return fail(ctx, BE_ERR_INVALID, "token %d: inconsistent routing metadata", t);
+  }
+  for (int64_t i = 0; i < (int64_t)n_pt_rows * pt_stride; ++i)
+    if (page_table[i] < -1 || page_table[i] >= pool->n_pages)
+      return fail(ctx, BE_ERR_INVALID, "page table entry %lld out of range", (long long)i);
+  cudaStream_t st = pick_stream(ctx, stream);
+  if (n_tokens > 0)
+    BE_CUDA(ctx, cudaMemcpyAsync(ws->d_tokens, tokens, n_tokens * sizeof(be_token),
+                                 cudaMemcpyHostToDevice, st));
+  if (n_pt_rows > 0)
+    BE_CUDA(ctx, cudaMemcpyAsync(ws->d_pt, page_table, (size_t)n_pt_rows * pt_stride * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, st));
+  return exec_dev(ctx, blk, pool, ws, phase, n_tokens, ws->d_tokens, pt_stride, ws->d_pt,
+                  d_arena_in, d_arena_out, st);
+}
+
+// ------------------------------------------------------------------------------ row kernels
+extern "C" int be_gather_rows(be_ctx* ctx, const void* arena, const int32_t* src, int rows, int d,
+                              void* out, void* stream) {
+  if (ctx == nullptr || rows < 0 || d % 8 != 0) return BE_ERR_INVALID;
+  cudaError_t e = bx::launch_gather(static_cast<const bf16*>(arena), src, 1, rows, d,
+                                    static_cast<bf16*>(out), nullptr, pick_stream(ctx, stream));
+  return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
+}
+
+extern "C" int be_scatter_rows(be_ctx* ctx, const void* rows_in, const int32_t* dst, int rows,
+                               int d, void* arena, void* stream) {
+  if (ctx == nullptr || rows < 0 || d % 8 != 0) return BE_ERR_INVALID;
+  cudaError_t e = bx::launch_scatter(static_cast<const bf16*>(rows_in), dst, 1, rows, d,
+                                     static_cast<bf16*>(arena), pick_stream(ctx, stream));
+  return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "scatter: %s", cudaGetErrorString(e));
+}
+
+extern "C" int be_cosine(be_ctx* ctx, const void* pred, const void* actual, int rows, int d,
+                         float thr, float* cos_out, int32_t* accept, void* stream) {
+  if (ctx == nullptr || rows < 0 || d % 8 != 0 || cos_out == nullptr) return BE_ERR_INVALID;
+  cudaError_t e = bx::launch_cosine(static_cast<const bf16*>(pred), static_cast<const bf16*>(actual),
+                                    rows, d, thr, cos_out, accept, pick_stream(ctx, stream));
+  return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "cosine: %s", cudaGetErrorString(e));
+}
+
+extern "C" int be_synth_rows(be_ctx* ctx, void* dst, int64_t n, uint64_t seed, const char* sid,
+                             float scale, void* stream) {
+  if (ctx == nullptr || dst == nullptr || sid == nullptr || n < 0) return BE_ERR_INVALID;
+  cudaError_t e = bx::launch_synth_rows(static_cast<bf16*>(dst), n, stream_key(seed, sid), scale,
+                                        pick_stream(ctx, stream));
+  return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "synth: %s", cudaGetErrorString(e));
+}
+
+extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out, int N, int K,
+                            int ntok, int ksplit, void* stream) {
+  if (ctx == nullptr || N % 128 != 0 || K % 64 != 0 || ntok <= 0) return BE_ERR_INVALID;
+  const int bn = bx::gemm_pick_bn(ntok);
+  CUtensorMap mw, mx;
+  int rc;
+  if ((rc = make_map(ctx, &mw, w, N, K, 128)) != BE_OK) return rc;
+  if ((rc = make_map(ctx, &mx, x, ntok, K, bn)) != BE_OK) return rc;
+  const int ntiles = (ntok + bn - 1) / bn;
+  if (ksplit <= 0) ksplit = bx::gemm_pick_ksplit(N, K, ntok, bn, ctx->num_sms);
+  const size_t need = (size_t)ksplit * ntiles * bn * N;
+  if (ksplit > 1 && need > ctx->gemm_ws_elems) {
+    if (ctx->gemm_ws) cudaFree(ctx->gemm_ws);
+    BE_CUDA(ctx, cudaMalloc(&ctx->gemm_ws, need * sizeof(float)));
+    ctx->gemm_ws_elems = need;
+  }
+  if (ctx->gemm_counters == nullptr) {
+    BE_CUDA(ctx, cudaMalloc(&ctx->gemm_counters, (1 << 16) * sizeof(int)));
+    BE_CUDA(ctx, cudaMemset(ctx->gemm_counters, 0, (1 << 16) * sizeof(int)));
+  }
+  bx::GemmLaunch L{};
+  L.map_w = &mw;
+  L.map_x = &mx;
+  L.N = N;
+  L.K = K;
+  L.bn = bn;
+  L.ksplit = ksplit;
+  L.epi.mode = bx::kStore;
+  L.epi.ntok = ntok;
+  L.epi.out = static_cast<bf16*>(out);
+  L.epi.ldo = N;
+  L.epi.ws = ctx->gemm_ws;
+  L.epi.counters = ctx->gemm_counters;
+  cudaError_t e = bx::launch_gemm(L, pick_stream(ctx, stream));
+  return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "gemm: %s", cudaGetErrorString(e));
+}
+
+extern "C" int be_attention(be_ctx* ctx, const void* q, const void* pool, int n_layers, int H,
+                            int hd, int layer, const int32_t* pt, int pt_stride,
+                            const int32_t* row_pt, const int32_t* row_ctx, int rows, int splits,
+                            void* out, void* stream) {
+  if (ctx == nullptr || rows < 0 || (hd != 64 && hd != 128) || splits < 1) return BE_ERR_INVALID;
+  static float* part = nullptr;
+  static size_t part_elems = 0;
+  if (splits > 1) {
+    const size_t need = (size_t)rows * H * splits * (hd + 2);
+    if (need > part_elems) {
+      if (part) cudaFree(part);
+      BE_CUDA(ctx, cudaMalloc(&part, need * sizeof(float)));
+      part_elems = need;
+    }
+  }
+  bx::AttnParams ap{};
+  ap.q = static_cast<const bf16*>(q);
+  ap.pool = static_cast<const bf16*>(pool);
+  ap.layer_elems = 2LL * H * 16 * hd;
+  ap.page_elems = ap.layer_elems * n_layers;
+  ap.layer = layer;
+  ap.page_table = pt;
+  ap.pt_stride = pt_stride;
+  ap.row_pt = row_pt;
+  ap.row_ctx = row_ctx;
+  ap.meta_stride = 1;
+  ap.ctx_add = 0;
+  ap.H = H;
+  ap.scale_log2 = (1.0f / sqrtf((float)hd)) * 1.4426950408889634f;
+  ap.out = static_cast<bf16*>(out);
+  ap.part = part;
+  ap.splits = splits;
+  cudaError_t e = bx::launch_attention(ap, rows, hd, pick_stream(ctx, stream));
+  return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "attention: %s", cudaGetErrorString(e));
+}

@@ -1,0 +1,83 @@
+// Block-forward GEMM on tcgen05: out^T[f, t] = sum_k W[f, k] * X[t, k] ("swap-AB": weight rows
+// fill the 128-row UMMA M dimension, the batch's tokens are the UMMA N dimension, 16..256).
+// Operands arrive by TMA (128B swizzle, K-major) through an mbarrier ring; one elected thread
+// issues tcgen05.mma into a TMEM accumulator; four warps drain TMEM in a fused epilogue:
+//   kStore   out = bf16(acc)                                   (plain projection)
+//   kResid   x += acc, xb = bf16(x)                            (O / down proj + residual)
+//   kSwiGLU  h = silu(gate) * up  (gate/up rows interleaved)   (FFN gate/up)
+//   kQKV     RoPE(q,k) + q store + paged KV append of k, v     (attention input proj)
+// The RMSNorm of the input row is fused as a per-token scale (rstd) applied to acc; the norm
+// weight gamma is folded into W at load time. Split-K partials meet in an fp32 workspace
+// (L2 resident) and the last CTA of a tile runs the epilogue.
+#pragma once
+#include <cuda.h>
+#include "ptx.cuh"
+
+namespace bx {
+
+enum EpiMode : int { kStore = 0, kResid = 1, kSwiGLU = 2, kQKV = 3 };
+
+struct EpiParams {
+  int mode;
+  int ntok;                // valid tokens (columns)
+  const float* rstd;       // [ntok] fused RMSNorm row scale, nullptr -> 1
+  __nv_bfloat16* out;      // kStore/kSwiGLU/kQKV(q): [ntok][ldo]
+  int ldo;
+  float* xres;             // kResid: fp32 residual stream [ntok][ldr]
+  __nv_bfloat16* xres_b;   // kResid: bf16 shadow of the residual (next GEMM's B operand)
+  int ldr;
+  // kQKV
+  const int* tok;          // [ntok] be_token records {src, dst, kv_slot, pos, pt_row}:
+                           //   kv_slot = page_slot * 16 + pos % 16, pos = RoPE position
+  __nv_bfloat16* kv_pool;  // paged KV pool of the block instance
+  long long page_elems;    // elements per page: L * 2 * H * 16 * hd
+  long long layer_elems;   // elements per layer inside a page: 2 * H * 16 * hd
+  int layer;
+  int d_model;
+  int head_dim;
+  const float2* rope;      // [max_pos][head_dim/2] (cos, sin)
+  // split-K
+  float* ws;               // [ksplit][ntiles][BN][N] fp32 partials
+  int* counters;           // [mtiles * ntiles] arrival counters (self-resetting)
+};
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+
+template <int BN>
+struct GemmSmem {
+  static constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+};
+
+template <int BN>
+__host__ __device__ constexpr int gemm_stages() {
+  // leave ~8 KB for barriers; cap at 8 stages (enough bytes in flight for one SM)
+  int s = (220 * 1024) / GemmSmem<BN>::kStageBytes;
+  return s > 8 ? 8 : s;
+}
+
+template <int BN>
+__host__ __device__ constexpr uint32_t tmem_cols() {
+  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+}
+
+// Host-side launch description.
+struct GemmLaunch {
+  const CUtensorMap* map_w;  // weights [N][K] bf16, box {64, 128}
+  const CUtensorMap* map_x;  // activations [rows][K] bf16, box {64, BN}
+  int N, K;
+  int ksplit;
+  int bn;                    // 16/32/64/128/256
+  EpiParams epi;
+};
+
+// Launches on `stream`; returns cudaError_t.
+cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream);
+
+// Chooses BN for a token count and a split-K factor so the grid covers the SMs.
+int gemm_pick_bn(int ntok);
+int gemm_pick_ksplit(int N, int K, int ntok, int bn, int num_sms);
+
+}  // namespace bx

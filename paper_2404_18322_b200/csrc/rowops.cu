@@ -1,0 +1,228 @@
+// Row kernels of the per-block path:
+//   K1 gather  : routing-table gather of per-request activation rows into the block batch
+//   K2 scatter : batch rows back to their next-hop rows of the activation arena
+//   rms_stats  : per-token RMSNorm scale (the normalisation itself is fused into the GEMM)
+//   K7 cosine  : predicted-vs-actual per-row cosine + accept verdict (speculation check)
+//   synth_init : counter-mode splitmix64 synthetic weights/inputs (identical bits to oracle/)
+// All HBM-bound: 16-byte vector accesses, one warp (or CTA) per row, grid >= 148 * k.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace bx {
+
+// ---------------------------------------------------------------- K1 gather
+// X[i] = float(arena[src[i]]), Xb[i] = arena[src[i]]; optional fp32 copy for the residual stream.
+__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ arena,
+                                   const int* __restrict__ src, int src_stride, int rows, int d,
+                                   __nv_bfloat16* __restrict__ xb, float* __restrict__ x) {
+  const int vec_per_row = d / 8;
+  const long long total = (long long)rows * vec_per_row;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < total;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(v / vec_per_row);
+    const int c = (int)(v - (long long)r * vec_per_row);
+    const uint4 val = __ldg(reinterpret_cast<const uint4*>(arena + (size_t)src[(size_t)r * src_stride] * d) + c);
+    reinterpret_cast<uint4*>(xb + (size_t)r * d)[c] = val;
+    if (x != nullptr) {
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&val);
+      float4 lo = make_float4(__bfloat162float(b[0]), __bfloat162float(b[1]),
+                              __bfloat162float(b[2]), __bfloat162float(b[3]));
+      float4 hi = make_float4(__bfloat162float(b[4]), __bfloat162float(b[5]),
+                              __bfloat162float(b[6]), __bfloat162float(b[7]));
+      float4* px = reinterpret_cast<float4*>(x + (size_t)r * d) + 2 * c;
+      px[0] = lo;
+      px[1] = hi;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2 scatter
+__global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ xb,
+                                    const int* __restrict__ dst, int dst_stride, int rows, int d,
+                                    __nv_bfloat16* __restrict__ arena) {
+  const int vec_per_row = d / 8;
+  const long long total = (long long)rows * vec_per_row;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < total;
+       v += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(v / vec_per_row);
+    const int c = (int)(v - (long long)r * vec_per_row);
+    const int drow = dst[(size_t)r * dst_stride];
+    if (drow < 0) continue;  // token output not needed downstream
+    const uint4 val = reinterpret_cast<const uint4*>(xb + (size_t)r * d)[c];
+    reinterpret_cast<uint4*>(arena + (size_t)drow * d)[c] = val;
+  }
+}
+
+// ---------------------------------------------------------------- rms stats
+// rstd[t] = 1 / sqrt(mean(x[t]^2) + eps), one warp per row.
+__global__ void rms_stats_kernel(const float* __restrict__ x, int rows, int d, float eps,
+                                 float* __restrict__ rstd) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float4* px = reinterpret_cast<const float4*>(x + (size_t)warp * d);
+  float s = 0.f;
+  for (int c = lane; c < d / 4; c += 32) {
+    const float4 v = px[c];
+    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) rstd[warp] = rsqrtf(s / (float)d + eps);
+}
+
+// ---------------------------------------------------------------- K7 cosine
+// cos[r] = <a_r, b_r> / (|a_r| |b_r|) in fp32; accept[r] = cos[r] >= thr. One warp per row.
+__global__ void cosine_rows_kernel(const __nv_bfloat16* __restrict__ a,
+                                   const __nv_bfloat16* __restrict__ b, int rows, int d,
+                                   float thr, float* __restrict__ cos_out,
+                                   int* __restrict__ accept) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const uint4* pa = reinterpret_cast<const uint4*>(a + (size_t)warp * d);
+  const uint4* pb = reinterpret_cast<const uint4*>(b + (size_t)warp * d);
+  float dot = 0.f, na = 0.f, nb = 0.f;
+  for (int c = lane; c < d / 8; c += 32) {
+    const uint4 va = __ldcs(pa + c), vb = __ldcs(pb + c);
+    const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&va);
+    const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&vb);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 fa = __bfloat1622float2(ha[i]);
+      const float2 fb = __bfloat1622float2(hb[i]);
+      dot = fmaf(fa.x, fb.x, fmaf(fa.y, fb.y, dot));
+      na = fmaf(fa.x, fa.x, fmaf(fa.y, fa.y, na));
+      nb = fmaf(fb.x, fb.x, fmaf(fb.y, fb.y, nb));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    na += __shfl_xor_sync(0xffffffffu, na, off);
+    nb += __shfl_xor_sync(0xffffffffu, nb, off);
+  }
+  if (lane == 0) {
+    // zero-norm rows have no defined cosine (the reference throws): report NaN, reject
+    const float c = (na > 0.f && nb > 0.f) ? dot / (sqrtf(na) * sqrtf(nb)) : __int_as_float(0x7fc00000);
+    cos_out[warp] = c;
+    if (accept != nullptr) accept[warp] = (c >= thr) ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------- synthetic init
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+// value of logical element i of the tensor whose stream key is `key` (see oracle/synth.h)
+__device__ __forceinline__ float synth_value(uint64_t key, uint64_t i, float scale) {
+  const uint64_t z = mix64(key + (i + 1) * 0x9e3779b97f4a7c15ull);
+  const float u = (float)(z >> 40) * (1.0f / 16777216.0f);
+  return (2.0f * u - 1.0f) * scale;
+}
+
+// Physical row layouts (see gemm QKV/SwiGLU epilogues):
+//   perm 0: identity
+//   perm 1: q/k rotate_half pair interleave inside each head (phys 2j <- j, 2j+1 <- j + hd/2)
+//   perm 2: gate/up interleave (phys 2j <- gate j, 2j+1 <- up j), two keys
+// dst holds `rows` physical rows of `cols`; gamma (optional, length cols) is folded in.
+__global__ void synth_weight_kernel(__nv_bfloat16* __restrict__ dst, int rows, int cols,
+                                    uint64_t key0, uint64_t key1, float scale, int perm,
+                                    int head_dim, const float* __restrict__ gamma) {
+  const long long total = (long long)rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int pr = (int)(idx / cols);
+    const int c = (int)(idx - (long long)pr * cols);
+    int lr = pr;
+    uint64_t key = key0;
+    if (perm == 1) {
+      const int h = pr / head_dim, e = pr - h * head_dim;
+      lr = h * head_dim + ((e & 1) ? (e >> 1) + head_dim / 2 : (e >> 1));
+    } else if (perm == 2) {
+      lr = pr >> 1;
+      key = (pr & 1) ? key1 : key0;
+    }
+    float v = synth_value(key, (uint64_t)lr * cols + c, scale);
+    v = __bfloat162float(__float2bfloat16_rn(v));  // logical bf16 weight
+    if (gamma != nullptr) v *= gamma[c];
+    dst[idx] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void synth_rows_kernel(__nv_bfloat16* __restrict__ dst, long long n, uint64_t key,
+                                  float scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(synth_value(key, (uint64_t)i, scale));
+}
+
+// rope[pos][j] = (cos, sin)(pos * theta^(-2j/hd)), computed in double for both sides
+__global__ void rope_table_kernel(float2* __restrict__ rope, int max_pos, int head_dim,
+                                  double theta) {
+  const int half = head_dim / 2;
+  const long long total = (long long)max_pos * half;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int pos = (int)(i / half), j = (int)(i - (long long)pos * half);
+    const double inv = pow(theta, -2.0 * j / head_dim);
+    const double ang = (double)pos * inv;
+    rope[i] = make_float2((float)cos(ang), (float)sin(ang));
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+static inline int grid_for(long long work, int threads, int cap) {
+  long long g = (work + threads - 1) / threads;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+cudaError_t launch_gather(const __nv_bfloat16* arena, const int* src, int src_stride, int rows,
+                          int d, __nv_bfloat16* xb, float* x, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  gather_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(arena, src, src_stride, rows, d, xb, x);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter(const __nv_bfloat16* xb, const int* dst, int dst_stride, int rows,
+                           int d, __nv_bfloat16* arena, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  scatter_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(xb, dst, dst_stride, rows, d, arena);
+  return cudaGetLastError();
+}
+cudaError_t launch_rms_stats(const float* x, int rows, int d, float eps, float* rstd,
+                             cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  rms_stats_kernel<<<(rows + 7) / 8, 256, 0, st>>>(x, rows, d, eps, rstd);
+  return cudaGetLastError();
+}
+cudaError_t launch_cosine(const __nv_bfloat16* a, const __nv_bfloat16* b, int rows, int d,
+                          float thr, float* cos_out, int* accept, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  cosine_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(a, b, rows, d, thr, cos_out, accept);
+  return cudaGetLastError();
+}
+cudaError_t launch_synth_weight(__nv_bfloat16* dst, int rows, int cols, uint64_t key0,
+                                uint64_t key1, float scale, int perm, int head_dim,
+                                const float* gamma, cudaStream_t st) {
+  synth_weight_kernel<<<grid_for((long long)rows * cols, 256, 148 * 32), 256, 0, st>>>(
+      dst, rows, cols, key0, key1, scale, perm, head_dim, gamma);
+  return cudaGetLastError();
+}
+cudaError_t launch_synth_rows(__nv_bfloat16* dst, long long n, uint64_t key, float scale,
+                              cudaStream_t st) {
+  synth_rows_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(dst, n, key, scale);
+  return cudaGetLastError();
+}
+cudaError_t launch_rope_table(float2* rope, int max_pos, int head_dim, double theta,
+                              cudaStream_t st) {
+  rope_table_kernel<<<grid_for((long long)max_pos * head_dim / 2, 256, 148 * 8), 256, 0, st>>>(
+      rope, max_pos, head_dim, theta);
+  return cudaGetLastError();
+}
+
+}  // namespace bx

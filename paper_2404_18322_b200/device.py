@@ -1,0 +1,202 @@
+"""Python handles over the C ABI (include/blockexec.h): context, blocks, KV pools, workspaces.
+
+PyTorch is only plumbing here (device buffers and streams); every computation runs in the
+sm_100a kernels of libblockexec.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import BlockDesc, Token, check, lib, PHASE_DECODE, PHASE_PREFILL  # noqa: F401
+
+PAGE_TOKENS = 16  # blocksim kPageTokens (proj/core/include/blocksim/kv.hpp:16)
+
+
+@dataclass(frozen=True)
+class BlockShape:
+    """Decoder-layer run served as one block (zoo.hpp:29-54 BlockDescriptor, as layers)."""
+    n_layers: int
+    d_model: int
+    n_heads: int
+    d_ff: int
+    max_pos: int = 4096
+    norm_eps: float = 1e-5
+    rope_theta: float = 10000.0
+    init_scale: float = 0.02 * 3 ** 0.5  # uniform with std 0.02
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+    @property
+    def kv_bytes_per_token(self) -> int:
+        # CostModel::kv_bytes_per_token: 4 * embed_dim per attention component (costmodel.cpp:114-127)
+        return 4 * self.d_model * self.n_layers
+
+    @property
+    def param_bytes(self) -> int:
+        d, f = self.d_model, self.d_ff
+        return 2 * self.n_layers * (4 * d * d + 3 * d * f)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        rc = lib().be_ctx_create(device, C.byref(h))
+        if rc != 0:
+            check(rc)
+        self.h = h
+
+    @property
+    def stream(self) -> C.c_void_p:
+        return C.c_void_p(lib().be_ctx_stream(self.h))
+
+    @property
+    def num_sms(self) -> int:
+        return lib().be_ctx_num_sms(self.h)
+
+    def sync(self) -> None:
+        check(lib().be_synchronize(self.h), self.h)
+
+    def close(self) -> None:
+        if self.h:
+            lib().be_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Block:
+    """One block's weights on the device (synthetic, generated from (seed, name))."""
+
+    def __init__(self, ctx: Context, shape: BlockShape, name: str, seed: int = 1):
+        self.ctx, self.shape, self.name, self.seed = ctx, shape, name, seed
+        self._name_b = name.encode()
+        desc = BlockDesc(shape.n_layers, shape.d_model, shape.n_heads, shape.head_dim, shape.d_ff,
+                         shape.max_pos, shape.norm_eps, shape.rope_theta, shape.init_scale, seed,
+                         self._name_b)
+        h = C.c_void_p()
+        check(lib().be_block_load(ctx.h, C.byref(desc), C.byref(h)), ctx.h)
+        self.h = h
+
+    def read_weight(self, layer: int, tensor: str) -> np.ndarray:
+        s = self.shape
+        rows, cols = {"wq": (s.d_model, s.d_model), "wk": (s.d_model, s.d_model),
+                      "wv": (s.d_model, s.d_model), "wo": (s.d_model, s.d_model),
+                      "wg": (s.d_ff, s.d_model), "wu": (s.d_ff, s.d_model),
+                      "wd": (s.d_model, s.d_ff)}[tensor]
+        out = np.empty((rows, cols), np.float32)
+        check(lib().be_block_read_weight(self.h, layer, tensor.encode(),
+                                         out.ctypes.data_as(C.c_void_p)), self.ctx.h)
+        return out
+
+    def free(self):
+        if self.h:
+            lib().be_block_free(self.h)
+            self.h = None
+
+
+class KvPool:
+    """Block-local paged KV pool: [page][layer][K|V][head][16][head_dim] bf16."""
+
+    def __init__(self, ctx: Context, block: Block, n_pages: int):
+        self.ctx, self.block, self.n_pages = ctx, block, n_pages
+        h = C.c_void_p()
+        check(lib().be_kv_pool_create(ctx.h, block.h, n_pages, C.byref(h)), ctx.h)
+        self.h = h
+
+    @property
+    def data_ptr(self) -> int:
+        return lib().be_kv_pool_data(self.h)
+
+    @property
+    def page_bytes(self) -> int:
+        return lib().be_kv_pool_page_bytes(self.h)
+
+    def read(self, n_elems: int, offset_elems: int = 0) -> np.ndarray:
+        """Copies bf16 pool elements to host, returned as fp32."""
+        raw = np.empty(n_elems, np.uint16)
+        check(lib().be_kv_pool_read(self.h, offset_elems * 2, n_elems * 2,
+                                    raw.ctypes.data_as(C.c_void_p)), self.ctx.h)
+        return (raw.astype(np.uint32) << 16).view(np.float32)
+
+    def free(self):
+        if self.h:
+            lib().be_kv_pool_free(self.h)
+            self.h = None
+
+
+class Workspace:
+    def __init__(self, ctx: Context, shape: BlockShape, max_tokens: int, max_rows: int,
+                 max_pages: int):
+        self.ctx, self.shape = ctx, shape
+        self.max_tokens, self.max_rows, self.max_pages = max_tokens, max_rows, max_pages
+        h = C.c_void_p()
+        check(lib().be_workspace_create(ctx.h, shape.d_model, shape.d_ff, shape.n_heads,
+                                        max_tokens, max_rows, max_pages, C.byref(h)), ctx.h)
+        self.h = h
+
+    def free(self):
+        if self.h:
+            lib().be_workspace_free(self.h)
+            self.h = None
+
+
+def tokens_array(rows) -> "C.Array":
+    """rows: iterable of (src_row, dst_row, kv_slot, pos, pt_row)."""
+    rows = list(rows)
+    arr = (Token * max(1, len(rows)))()
+    for i, r in enumerate(rows):
+        arr[i] = Token(*[int(v) for v in r])
+    return arr
+
+
+def exec_batch(ctx: Context, block: Block, pool: KvPool, ws: Workspace, phase: int, tokens,
+               page_table: np.ndarray, arena_in, arena_out, stream=None) -> None:
+    """One per-block batched execution (the call that replaces batch_duration_us)."""
+    toks = tokens_array(tokens)
+    n = len(tokens)
+    pt = np.ascontiguousarray(page_table, dtype=np.int32)
+    check(lib().be_exec_batch(ctx.h, block.h, pool.h, ws.h, phase, n, C.cast(toks, C.c_void_p),
+                              pt.shape[0], pt.shape[1], pt.ctypes.data_as(C.c_void_p),
+                              _ptr(arena_in), _ptr(arena_out),
+                              stream if stream is not None else C.c_void_p(0)), ctx.h)
+
+
+def gemm_bf16(ctx: Context, w, x, out, ksplit: int = 0) -> None:
+    N, K = w.shape
+    check(lib().be_gemm_bf16(ctx.h, _ptr(w), _ptr(x), _ptr(out), N, K, x.shape[0], ksplit,
+                             C.c_void_p(0)), ctx.h)
+
+
+def cosine(ctx: Context, pred, actual, threshold: float, cos_out, accept_out) -> None:
+    rows, d = pred.shape
+    check(lib().be_cosine(ctx.h, _ptr(pred), _ptr(actual), rows, d, threshold, _ptr(cos_out),
+                          _ptr(accept_out), C.c_void_p(0)), ctx.h)
+
+
+def gather_rows(ctx: Context, arena, src_idx, out) -> None:
+    check(lib().be_gather_rows(ctx.h, _ptr(arena), _ptr(src_idx), src_idx.shape[0],
+                               arena.shape[1], _ptr(out), C.c_void_p(0)), ctx.h)
+
+
+def scatter_rows(ctx: Context, rows, dst_idx, arena) -> None:
+    check(lib().be_scatter_rows(ctx.h, _ptr(rows), _ptr(dst_idx), dst_idx.shape[0],
+                                rows.shape[1], _ptr(arena), C.c_void_p(0)), ctx.h)
+
+
+def synth_rows(ctx: Context, dst, seed: int, stream_id: str, scale: float) -> None:
+    check(lib().be_synth_rows(ctx.h, _ptr(dst), dst.numel(), seed, stream_id.encode(), scale,
+                              C.c_void_p(0)), ctx.h)

@@ -1,0 +1,91 @@
+"""GPU parity of the individual sm_100a kernels (run with -m gpu on a B200).
+
+Integer/byte work (gather, scatter, synthetic weights) must be bit-exact; the floating-point
+kernels are checked against an fp32 reference with the tolerance written in each test.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2404_18322_b200 import device as dev  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).cuda()
+
+
+@pytest.mark.parametrize("N,K,ntok,ksplit", [
+    (128, 64, 1, 1), (256, 256, 8, 1), (768, 512, 300, 1), (1024, 1024, 16, 4),
+    (4096, 4096, 64, 0), (12288, 4096, 64, 0), (4096, 11008, 16, 0), (512, 256, 200, 2),
+])
+def test_gemm_matches_fp32(ctx, N, K, ntok, ksplit):
+    g = torch.Generator().manual_seed(N * 7 + K + ntok)
+    w = (torch.randn(N, K, generator=g) * 0.05).to(torch.bfloat16).cuda()
+    x = torch.randn(ntok, K, generator=g).to(torch.bfloat16).cuda()
+    out = torch.empty(ntok, N, dtype=torch.bfloat16, device="cuda")
+    dev.gemm_bf16(ctx, w, x, out, ksplit)
+    ctx.sync()
+    ref = x.float() @ w.float().t()
+    err = (out.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    # bf16 output rounding (2^-8 relative) dominates; fp32 accumulation order differs
+    assert err <= 8e-3 * scale + 1e-3, (err, scale)
+
+
+def test_gather_scatter_bit_exact(ctx):
+    d = 4096
+    arena = torch.randn(300, d).to(torch.bfloat16).cuda()
+    src = torch.tensor([5, 0, 299, 17, 17, 42, 8], dtype=torch.int32, device="cuda")
+    out = torch.empty(len(src), d, dtype=torch.bfloat16, device="cuda")
+    dev.gather_rows(ctx, arena, src, out)
+    ctx.sync()
+    assert torch.equal(out, arena[src.long()])
+    dst_arena = torch.zeros_like(arena)
+    dst = torch.tensor([3, 1, 4, 100, 5, 9, 2], dtype=torch.int32, device="cuda")
+    dev.scatter_rows(ctx, out, dst, dst_arena)
+    ctx.sync()
+    expect = torch.zeros_like(arena)
+    expect[dst.long()] = out
+    assert torch.equal(dst_arena, expect)
+
+
+def test_cosine_rows(ctx):
+    from oracle import oracle as O
+    rows, d = 256, 5120
+    g = torch.Generator().manual_seed(3)
+    a = torch.randn(rows, d, generator=g)
+    b = a + 0.35 * torch.randn(rows, d, generator=g) * torch.linspace(0, 1, rows)[:, None]
+    ab, bb = a.to(torch.bfloat16), b.to(torch.bfloat16)
+    cos = torch.empty(rows, dtype=torch.float32, device="cuda")
+    acc = torch.empty(rows, dtype=torch.int32, device="cuda")
+    dev.cosine(ctx, ab.cuda(), bb.cuda(), 0.95, cos, acc)
+    ctx.sync()
+    rc, racc = O.cosine_rows(ab.float().numpy(), bb.float().numpy(), 0.95)
+    np.testing.assert_allclose(cos.cpu().numpy(), rc, atol=2e-6)
+    # verdicts may only differ inside the fp32-vs-fp64 rounding band around the threshold
+    band = np.abs(rc - 0.95) < 1e-5
+    assert np.array_equal(acc.cpu().numpy()[~band], racc[~band])
+
+
+def test_synth_rows_bit_exact(ctx):
+    from oracle import oracle as O
+    n = 100003
+    t = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    dev.synth_rows(ctx, t, 7, "inputs:test", 1.7320508)
+    ctx.sync()
+    ref = O.synth(n, 7, "inputs:test", 1.7320508, round_bf16=True)
+    assert np.array_equal(t.float().cpu().numpy(), ref)
+
+
+def test_block_weights_bit_exact(ctx):
+    from oracle import oracle as O
+    shape = dev.BlockShape(n_layers=2, d_model=256, n_heads=4, d_ff=768, max_pos=64)
+    blk = dev.Block(ctx, shape, "b0", seed=1)
+    ob = O.OracleBlock(shape, "b0", seed=1)
+    for layer in range(2):
+        for t in ["wq", "wk", "wv", "wo", "wg", "wu", "wd"]:
+            assert np.array_equal(blk.read_weight(layer, t), ob.weight(layer, t)), (layer, t)
+    blk.free()
