@@ -1,0 +1,422 @@
+#!/usr/bin/env python3
+"""Benchmark of the per-block batched execution path (BASELINE.json metric: block-chain decode
+tokens/s, per-kernel % of roofline).
+
+One step = one lockstep decode token for every request of the C2 workload (BASELINE.json
+configs[1]: Llama-2-7B-shaped synthetic, 32 layers in 4-layer blocks, 4 tenants sharing the first
+24 layers, mixed batch 64, prompt 512, decode 128): 6 shared blocks at 64 rows and 8 private
+blocks at 16 rows, each a gather -> 4 decoder layers (tcgen05 GEMMs, paged attention) -> scatter,
+replayed as one CUDA graph. Inputs (weights 22.7 GB, KV ~21 GB) are far larger than L2.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun each rank serves its own replica of the workload (one GPU each, no data-path
+collective: scaling "weak"); rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return dict(PEAKS_FALLBACK), "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=1)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------------ CPU leg
+_CPU_BLOCK = {}
+
+
+def cpu_block_sample(wl, threads: int, rows_list=(64, 16), ctx: int = 576, reps: int = 1):
+    """Times the oracle (fp32 C restatement, OpenMP) on one block of the workload at each row
+    count; returns {rows: seconds}. TEST-INFRASTRUCTURE use: the CPU baseline only."""
+    import numpy as np
+    from oracle import oracle as O
+    if wl.name not in _CPU_BLOCK:
+        _CPU_BLOCK[wl.name] = O.OracleBlock(wl.shape, "cpu-sample", seed=wl.seed)
+    ob = _CPU_BLOCK[wl.name]
+    ctx = min(ctx, wl.req_prompt[0] + wl.req_output[0] // 2, wl.shape.max_pos - reps - 2)
+    out = {}
+    for rows in rows_list:
+        seqs = [ob.new_seq(ctx + reps + 1) for _ in range(rows)]
+        for s in seqs:
+            s.fill(ctx)
+        x = np.random.default_rng(0).standard_normal((rows, wl.shape.d_model)).astype(np.float32)
+        best = None
+        for rep in range(reps):
+            t0 = time.perf_counter()
+            ob.forward(seqs, list(range(rows)), [ctx + rep] * rows, x, threads=threads)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        out[rows] = best
+        del seqs
+    return out
+
+
+def cpu_step_tokens_per_s(wl, times: dict) -> float:
+    rows = wl.rows_at_block()
+    step = 0.0
+    for r in rows:
+        key = min(times, key=lambda k: abs(k - r))
+        step += times[key] * (r / key if key else 1.0) if r > key else times[key]
+    return wl.n_requests / step
+
+
+# ------------------------------------------------------------------------------------ GPU leg
+def kernel_rooflines(ctx, wl, peaks):
+    """Dominant kernels timed alone with CUDA events on the launching stream (inputs > L2)."""
+    import numpy as np
+    import torch
+    from paper_2404_18322_b200 import device as dev
+    from paper_2404_18322_b200._lib import lib, check
+    import ctypes as C
+
+    s = wl.shape
+    stream = torch.cuda.ExternalStream(ctx.stream.value)
+    res = {}
+    # --- decode attention: 64 rows at ctx 640 over a 4-layer pool (671 MB of K/V per layer)
+    rows, ctxlen, H, hd, L = 64, 640, s.n_heads, s.head_dim, s.n_layers
+    pages_per_row = (ctxlen + 15) // 16
+    n_pages = rows * pages_per_row
+    blk_desc_shape = s
+    blk = dev.Block(ctx, blk_desc_shape, "roofline", seed=3)
+    pool = dev.KvPool(ctx, blk, n_pages)
+    rng = np.random.default_rng(0)
+    pt = rng.permutation(n_pages).astype(np.int32).reshape(rows, pages_per_row)
+    d_pt = torch.from_numpy(pt).cuda()
+    d_rowpt = torch.arange(rows, dtype=torch.int32, device="cuda")
+    d_ctx = torch.full((rows,), ctxlen, dtype=torch.int32, device="cuda")
+    q = torch.randn(rows, H * hd, device="cuda").to(torch.bfloat16)
+    o = torch.empty_like(q)
+    torch.cuda.synchronize()
+
+    def attn(layer):
+        check(lib().be_attention(ctx.h, C.c_void_p(q.data_ptr()), C.c_void_p(pool.data_ptr), L, H,
+                                 hd, layer, C.c_void_p(d_pt.data_ptr()), pages_per_row,
+                                 C.c_void_p(d_rowpt.data_ptr()), C.c_void_p(d_ctx.data_ptr()),
+                                 rows, 1, C.c_void_p(o.data_ptr()), C.c_void_p(0)), ctx.h)
+
+    for layer in range(L):
+        attn(layer)
+    ctx.sync()
+    reps = 8
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(reps):
+        attn(i % L)
+    e1.record(stream)
+    ctx.sync()
+    t = e0.elapsed_time(e1) / reps / 1e3
+    bytes_ = rows * ctxlen * 2 * H * hd * 2 + 2 * rows * H * hd * 2
+    res["attention"] = {"kernel": "attn_decode_kernel<128>", "shape": f"{rows} rows x ctx {ctxlen}, "
+                        f"{H} heads x {hd}", "bytes_per_launch": bytes_, "us": t * 1e6,
+                        "achieved_gbs": bytes_ / t / 1e9}
+    pool.free()
+    blk.free()
+
+    # --- decode GEMMs at 64 rows, cycling through distinct weight copies (> L2)
+    for name, N, K in [("gate_up", 2 * s.d_ff, s.d_model), ("qkv", 3 * s.d_model, s.d_model),
+                       ("down", s.d_model, s.d_ff), ("o", s.d_model, s.d_model)]:
+        copies = max(2, int(np.ceil(3 * 126e6 / (N * K * 2))))
+        w = torch.empty(copies, N, K, dtype=torch.bfloat16, device="cuda").uniform_(-0.03, 0.03)
+        x = torch.randn(64, K, device="cuda").to(torch.bfloat16)
+        out = torch.empty(64, N, device="cuda", dtype=torch.bfloat16)
+        for i in range(copies):
+            dev.gemm_bf16(ctx, w[i], x, out)
+        ctx.sync()
+        reps = 4 * copies
+        e0.record(stream)
+        for i in range(reps):
+            dev.gemm_bf16(ctx, w[i % copies], x, out)
+        e1.record(stream)
+        ctx.sync()
+        t = e0.elapsed_time(e1) / reps / 1e3
+        bytes_ = 2 * (N * K + 64 * K + 64 * N)
+        res[f"gemm_{name}"] = {"kernel": "gemm_tc_kernel<64>", "shape": f"[64x{K}]x[{K}x{N}]",
+                               "bytes_per_launch": bytes_, "us": t * 1e6,
+                               "achieved_gbs": bytes_ / t / 1e9,
+                               "tflops": 2 * 64 * N * K / t / 1e12}
+        del w
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+    from paper_2404_18322_b200.device import Context
+    from paper_2404_18322_b200.runner import Runner
+    from paper_2404_18322_b200.workloads import CONFIGS
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peaks_kind = load_peaks()
+    wl = CONFIGS[args.config](prompt=args.prompt, output=args.output) if args.config != "c1" \
+        else CONFIGS["c1"](output=args.output)
+    ctx = Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream.value)
+    run = Runner(ctx, wl, mode=1, use_graphs=True)
+    t0 = time.time()
+    run.run()  # prefill every prompt (untimed)
+    ctx.sync()
+    prefill_s = time.time() - t0
+    n_live = run.live
+    for _ in range(args.warmup):
+        run.decode_step()
+    ctx.sync()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- device-timed region: K decode steps, inputs resident in HBM
+    barrier()
+    torch.cuda.synchronize()
+    ctx.sync()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    nb = 0
+    for _ in range(args.steps):
+        nb = run.decode_step()
+    e1.record(stream)
+    ctx.sync()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    stats = run.step_stats()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    tokens_per_step = n_live * world
+    value = tokens_per_step * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API: pinned host rows in, results out, every step
+    e2e = None
+    if not args.no_e2e:
+        d = wl.shape.d_model
+        hin = torch.empty(n_live, d, dtype=torch.bfloat16).pin_memory()
+        hout = torch.empty(n_live, d, dtype=torch.bfloat16).pin_memory()
+        hin.copy_(torch.randn(n_live, d).to(torch.bfloat16))
+        run.decode_step(hin, hout)
+        barrier()
+        ctx.sync()
+        t_start = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            run.decode_step(hin, hout)
+            hin.copy_(hout)  # greedy feedback: the step's output is the next input
+        e1.record(stream)
+        ctx.sync()
+        wall = time.perf_counter() - t_start
+        e_ms = max(e0.elapsed_time(e1), wall * 1e3)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": tokens_per_step * args.steps / (e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(hin.numel() * 2), "d2h_bytes_per_step": int(hout.numel() * 2),
+               "ms_per_step": e_ms / args.steps}
+
+    # ---- roofline of the dominant kernels, and of the whole step
+    kr = kernel_rooflines(ctx, wl, peaks) if rank == 0 and not args.no_roofline else {}
+    hbm = peaks["hbm_gbs"]
+    step_bytes = stats["weight_bytes"] + stats["kv_bytes"] + stats["act_bytes"]
+    roofline = None
+    if "attention" in kr:
+        a = kr["attention"]
+        roofline = {"bound": "hbm", "kernel": a["kernel"], "shape": a["shape"],
+                    "achieved": round(a["achieved_gbs"], 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(a["achieved_gbs"] / hbm, 4), "peak_kind": peaks_kind,
+                    "traffic": None, "us_per_launch": round(a["us"], 2)}
+    step_roofline = {"bound": "hbm", "bytes_per_step": step_bytes,
+                     "achieved": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(step_bytes / (ms_per_step / 1e3) / 1e9 / hbm, 4),
+                     "roofline_tokens_per_s": round(n_live * hbm * 1e9 / step_bytes, 1)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        times = cpu_block_sample(wl, threads)
+        cpu = {"value": round(cpu_step_tokens_per_s(wl, times), 3), "unit": "tokens/s",
+               "cores": threads, "kind": "port",
+               "sample": "oracle fp32 C restatement (OpenMP): one 4-layer block decode at 64 and "
+                         "16 rows, ctx 576; step = sum over the 14 block runs of the workload "
+                         f"(t64={times[64]:.3f}s, t16={times[16]:.3f}s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "block-chain decode tokens/s", "value": round(value, 2), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, "
+            "synthetic prompt embeddings; greedy feedback of the last hidden state)",
+            "config": {"workload": wl.name, "model": "Llama-2-7B-shaped" if args.config in ("c2", "c3")
+                       else wl.name, "tenants": len(wl.chains), "global_batch": n_live * world,
+                       "prompt": wl.req_prompt[0], "decode": wl.req_output[0],
+                       "blocks": f"{len(wl.block_names)} blocks x {wl.shape.n_layers} layers",
+                       "rows_per_block": wl.rows_at_block(), "batches_per_step": nb,
+                       "l2": "inputs larger than L2 (weights+KV streamed per step)",
+                       "parallelism": f"replica per GPU x{world}" if world > 1 else "1 GPU"},
+            "roofline": roofline, "step_roofline": step_roofline, "kernels": kr,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(stats["launches"]) * args.steps,
+            "graph_replayed": bool(stats["graph_replayed"]), "clocks": clk,
+            "prefill_s": round(prefill_s, 2),
+        }
+        print(json.dumps(line), flush=True)
+    run.close()
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args, world, rank, local):
+    """The reference arm: the path's arithmetic on the host cores (the reference computes no
+    tensors — blocksim prices a block with CostModel::block_us — so the timed CPU implementation
+    is our fp32 oracle port of the block forward, with all host threads)."""
+    if rank != 0:
+        return
+    from paper_2404_18322_b200.workloads import CONFIGS
+    wl = CONFIGS[args.config](prompt=args.prompt, output=args.output) if args.config != "c1" \
+        else CONFIGS["c1"](output=args.output)
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        times = cpu_block_sample(wl, threads)
+        if i >= args.warmup:
+            vals.append(cpu_step_tokens_per_s(wl, times))
+    v = statistics.mean(vals)
+    line = {"impl": "reference", "metric": "block-chain decode tokens/s", "value": round(v, 3),
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(wl.n_requests / v * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl.name, "global_batch": wl.n_requests},
+            "cpu_baseline": {"value": round(v, 3), "unit": "tokens/s", "cores": threads,
+                             "kind": "port", "sample": "per step: one 4-layer block decode at 64 "
+                             "and at 16 rows (ctx 576), extrapolated to the 14 block runs of a "
+                             "decode step"},
+            "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--prompt", type=int, default=512)
+    ap.add_argument("--output", type=int, default=128)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup()
+    need = 1 + args.warmup + 2 * args.steps + 2
+    if args.output < need:
+        args.output = need
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

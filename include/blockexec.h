@@ -110,6 +110,9 @@ int be_exec_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace
                       const int32_t* d_page_table, const void* d_arena_in, void* d_arena_out,
                       void* stream);
 
+/* Kernel launches one be_exec_batch of n_tokens performs (for launch accounting). */
+int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_tokens, int pt_stride);
+
 /* K1 / K2 standalone: routing-table gather and scatter of bf16 rows. */
 int be_gather_rows(be_ctx* ctx, const void* d_arena, const int32_t* d_src, int rows, int d,
                    void* d_out, void* stream);

@@ -1,0 +1,144 @@
+/*
+ * blockhost.h — C ABI of the host control plane that forms per-block batches and drives
+ * be_exec_batch (include/blockexec.h).
+ *
+ * Two layers, both mirroring blocksim semantics bit-for-bit where the reference defines them:
+ *  - bh_pool_* : block instances and queues — enqueue with the kv-resident priority segment,
+ *                greedy prefix pop_batch under a token budget, earliest-head arbitration
+ *                (InstancePool, proj/core/src/agent.cpp:132-224).
+ *  - bh_kv_*   : block-local paged KV bookkeeping with global page ids and the physical page
+ *                slots the GPU page tables hold (KvStore, proj/core/src/kv.cpp:105-237).
+ *  - bh_runner_* : the executor loop on one device (Simulation::pump / on_batch_finish /
+ *                advance_from, proj/core/src/scenario.cpp:465-669) with the GPU block run in
+ *                place of batch_duration_us (scenario.cpp:493).
+ * Status codes as in blockexec.h (0 ok, 1 invalid_argument, 2 logic_error, 5 runtime_error).
+ */
+#ifndef BLOCKHOST_H
+#define BLOCKHOST_H
+
+#include <stdint.h>
+
+#include "blockexec.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bh_pool bh_pool;
+typedef struct bh_kv bh_kv;
+typedef struct bh_runner bh_runner;
+
+/* QueueEntry (proj/core/include/blocksim/agent.hpp:20-30) */
+typedef struct {
+  int32_t request_id;
+  int32_t chain_step;
+  int32_t phase; /* BE_PHASE_* */
+  int32_t tokens;
+  int32_t context_tokens;
+  int32_t kv_resident;
+  double est_cost_us;
+  uint64_t enqueue_seq; /* assigned by enqueue */
+} bh_entry;
+
+/* ---- pool ---- */
+bh_pool* bh_pool_new(void);
+void bh_pool_free(bh_pool* p);
+const char* bh_pool_last_error(const bh_pool* p);
+int bh_pool_create_instance(bh_pool* p, const char* block_id, int device, int64_t now,
+                            int64_t ready_at, char* id_out, int id_cap);
+int bh_pool_mark_ready(bh_pool* p, const char* inst, int64_t now);
+int bh_pool_enqueue(bh_pool* p, const char* inst, const bh_entry* e);
+int bh_pool_pop_batch(bh_pool* p, const char* inst, int max_batch_tokens, int64_t now,
+                      bh_entry* out, int cap, int* n_out, int* phase_out);
+int bh_pool_finish_batch(bh_pool* p, const char* inst, int64_t now);
+/* 1 = found (id written), 0 = none */
+int bh_pool_next_runnable(bh_pool* p, int device, int64_t now, char* id_out, int id_cap);
+int bh_pool_remove_queued(bh_pool* p, const char* inst, int request_id, bh_entry* out, int cap,
+                          int* n_out);
+int bh_pool_take_tail(bh_pool* p, const char* inst, int count, bh_entry* out, int cap, int* n_out);
+int bh_pool_queue(bh_pool* p, const char* inst, bh_entry* out, int cap, int* n_out,
+                  double* queued_cost_us, int* executing);
+
+/* ---- kv ---- */
+bh_kv* bh_kv_new(void);
+void bh_kv_free(bh_kv* k);
+const char* bh_kv_last_error(const bh_kv* k);
+int bh_kv_attach_pool(bh_kv* k, const char* pool_key, int device, int n_pages);
+int bh_kv_set_capacity(bh_kv* k, int device, int64_t bytes);
+int bh_kv_create_segment(bh_kv* k, uint64_t request, const char* block, int device,
+                         int64_t bytes_per_token);
+int bh_kv_append_tokens(bh_kv* k, uint64_t request, const char* block, int n, int* added);
+int bh_kv_share_prefix(bh_kv* k, uint64_t request, uint64_t from, const char* block, int tokens,
+                       int* covered);
+int bh_kv_release(bh_kv* k, uint64_t request, const char* block);
+int bh_kv_release_request(bh_kv* k, uint64_t request);
+int bh_kv_move_segment(bh_kv* k, uint64_t request, const char* block, int dst_device);
+/* query: what = 0 device_of, 1 tokens, 2 pages, 3 shared_pages, 4 segment_bytes, 5 has_segment */
+int64_t bh_kv_query(const bh_kv* k, uint64_t request, const char* block, int what);
+int64_t bh_kv_bytes_saved(const bh_kv* k);
+int64_t bh_kv_used(const bh_kv* k, int device);
+int bh_kv_page_ids(const bh_kv* k, uint64_t request, const char* block, uint64_t* out, int cap,
+                   int* n_out);
+int bh_kv_page_slots(const bh_kv* k, uint64_t request, const char* block, int32_t* out, int cap,
+                     int* n_out);
+
+/* ---- runner: the multi-tenant block-chain workload on one device ---- */
+typedef struct {
+  int n_blocks;
+  const be_block_desc* blocks; /* distinct blocks of the zoo; all share d_model */
+  int n_tenants;
+  const int32_t* chain_ptr;    /* [n_tenants + 1] CSR offsets into chain_blocks */
+  const int32_t* chain_blocks; /* block indices, the tenant's chain in order */
+  int n_requests;
+  const int32_t* req_tenant;   /* [n_requests] */
+  const int32_t* req_prompt;   /* [n_requests] prompt tokens */
+  const int32_t* req_output;   /* [n_requests] tokens to generate (first token comes from prefill) */
+  int max_batch_tokens;        /* pop_batch budget (ScenarioConfig::max_batch_tokens) */
+  int mode;                    /* 0 = reference event order (arrivals at t=0, interleaved
+                                  prefill/decode); 1 = lockstep (all prefill, then decode) */
+  int use_graphs;              /* capture steady-state decode steps in CUDA graphs */
+  uint64_t seed;               /* synthetic prompt embeddings: stream "inputs:req<r>" */
+} bh_workload;
+
+typedef struct {
+  int32_t instance; /* instance index (creation order, "i<instance+1>") */
+  int32_t block;
+  int32_t phase;
+  int32_t n_members;
+  int32_t first_member; /* offset into the member arrays of bh_runner_trace */
+} bh_batch_rec;
+
+int bh_runner_create(be_ctx* ctx, const bh_workload* w, bh_runner** out);
+int bh_runner_free(bh_runner* r);
+const char* bh_runner_last_error(const bh_runner* r);
+/* Runs until every request finished prefill (lockstep) or `max_batches` batches ran (mode 0,
+ * <= 0 = until all requests complete). */
+int bh_runner_run(bh_runner* r, int max_batches);
+/* Lockstep decode: one token for every live request (one pass over all chains). host_in /
+ * host_out optional pinned or pageable [n_live][d] bf16 rows (request order) copied in before
+ * and out after the step; *n_batches receives the batches executed. */
+int bh_runner_decode_step(bh_runner* r, const void* host_in, void* host_out, int* n_batches);
+int bh_runner_live_requests(const bh_runner* r);
+int64_t bh_runner_tokens_generated(const bh_runner* r);
+/* Batch trace since creation. members: request ids, steps, context tokens (may be NULL). */
+int bh_runner_trace(const bh_runner* r, bh_batch_rec* recs, int cap, int* n_out,
+                    int32_t* member_req, int32_t* member_step, int32_t* member_ctx, int mcap,
+                    int* m_out);
+int bh_runner_clear_trace(bh_runner* r);
+/* Device pointer of the decode activation arena ([n_requests][d] bf16, row = request). */
+void* bh_runner_arena(bh_runner* r);
+/* Per-step accounting of the last decode step for roofline reporting. */
+typedef struct {
+  double weight_bytes;   /* bytes of block weights streamed */
+  double kv_bytes;       /* bytes of K/V read by attention */
+  double act_bytes;      /* gather + scatter bytes */
+  double flops;          /* 2*M*N*K over all GEMMs + 4*ctx*d attention */
+  int launches;          /* kernel launches of the step */
+  int graph_replayed;    /* 1 when the step ran as a CUDA graph replay */
+} bh_step_stats;
+int bh_runner_step_stats(const bh_runner* r, bh_step_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKHOST_H */

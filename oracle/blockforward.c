@@ -147,6 +147,18 @@ void or_seq_free(or_seq* s) {
   free(s);
 }
 int or_seq_len(const or_seq* s) { return s->len; }
+/* Fills positions [0, len) of every layer's K/V with synthetic values (CPU-baseline timing:
+ * stands in for a prefill the timed sample does not redo). */
+void or_seq_fill(or_seq* s, int len, uint64_t seed) {
+  if (len > s->max_tokens) len = s->max_tokens;
+  const uint64_t key = or_stream_key(seed, "oracle:kvfill");
+  const size_t per = (size_t)s->max_tokens * s->d;
+#pragma omp parallel for schedule(static)
+  for (long long lk = 0; lk < (long long)s->n_layers * 2; ++lk)
+    for (size_t i = 0; i < (size_t)len * s->d; ++i)
+      s->kv[lk * per + i] = or_synth_value(key, lk * per + i, 1.0f);
+  s->len = len;
+}
 const float* or_seq_kv(const or_seq* s, int layer, int kv) {
   return s->kv + ((size_t)layer * 2 + kv) * s->max_tokens * s->d;
 }

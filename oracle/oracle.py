@@ -43,6 +43,7 @@ def lib():
         L.or_seq_free.argtypes = [P]
         L.or_seq_len.restype = C.c_int
         L.or_seq_len.argtypes = [P]
+        L.or_seq_fill.argtypes = [P, C.c_int, C.c_uint64]
         L.or_seq_kv.restype = C.POINTER(C.c_float)
         L.or_seq_kv.argtypes = [P, C.c_int, C.c_int]
         L.or_block_forward.restype = C.c_int
@@ -107,6 +108,9 @@ class OracleSeq:
         self.block = block
         self.max_tokens = max_tokens
         self.h = lib().or_seq_create(block.h, max_tokens)
+
+    def fill(self, length: int, seed: int = 1) -> None:
+        lib().or_seq_fill(self.h, length, seed)
 
     def kv(self, layer: int, which: int) -> np.ndarray:
         d = self.block.shape.d_model

@@ -656,6 +656,13 @@ extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_wo
                   d_arena_in, d_arena_out, st);
 }
 
+extern "C" int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_tokens,
+                                      int pt_stride) {
+  if (ctx == nullptr || blk == nullptr || n_tokens <= 0) return 0;
+  const int splits = attn_splits(ctx, n_tokens, blk->desc.n_heads, pt_stride);
+  return 2 + blk->desc.n_layers * (7 + (splits > 1 ? 1 : 0));
+}
+
 // ------------------------------------------------------------------------------ row kernels
 extern "C" int be_gather_rows(be_ctx* ctx, const void* arena, const int32_t* src, int rows, int d,
                               void* out, void* stream) {

@@ -40,7 +40,8 @@ void KvStore::free_slot(const std::string& pool_key, int device, int slot) {
   if (it != pools_.end()) it->second.release(slot);
 }
 
-std::uint64_t KvStore::new_page(const Segment& s, int device) {
+std::uint64_t KvStore::new_page(std::uint64_t request, const std::string& block,
+                                const Segment& s, int device) {
   reserve(device, s.bytes_per_page);
   const std::uint64_t id = next_page_++;
   Page p;
@@ -48,15 +49,41 @@ std::uint64_t KvStore::new_page(const Segment& s, int device) {
   p.ref = 1;
   p.device = device;
   p.pool_key = s.pool_key;
-  try {
-    p.slot = alloc_slot(s.pool_key, device);
-  } catch (...) {
-    unreserve(device, s.bytes_per_page);
-    --next_page_;
-    throw;
+  auto rit = reserved_.find({request, block});
+  if (rit != reserved_.end() && !rit->second.slots.empty() && rit->second.device == device &&
+      rit->second.pool_key == s.pool_key) {
+    p.slot = rit->second.slots.front();
+    rit->second.slots.erase(rit->second.slots.begin());
+    if (rit->second.slots.empty()) reserved_.erase(rit);
+  } else {
+    try {
+      p.slot = alloc_slot(s.pool_key, device);
+    } catch (...) {
+      unreserve(device, s.bytes_per_page);
+      --next_page_;
+      throw;
+    }
   }
   pages_[id] = p;
   return id;
+}
+
+std::vector<int> KvStore::reserve_slots(std::uint64_t request, const std::string& block,
+                                        const std::string& pool_key, int device,
+                                        int total_pages) {
+  std::vector<int> row = page_slots(request, block);
+  auto& r = reserved_[{request, block}];
+  if (r.slots.empty()) {
+    r.pool_key = pool_key;
+    r.device = device;
+  } else if (r.pool_key != pool_key || r.device != device) {
+    throw KvError("slot reservation moved between pools");
+  }
+  while (static_cast<int>(row.size() + r.slots.size()) < total_pages)
+    r.slots.push_back(alloc_slot(pool_key, device));
+  row.insert(row.end(), r.slots.begin(), r.slots.end());
+  if (r.slots.empty()) reserved_.erase({request, block});
+  return row;
 }
 
 void KvStore::create_segment(std::uint64_t request, const std::string& block, int device,
@@ -81,7 +108,7 @@ int KvStore::append_tokens(std::uint64_t request, const std::string& block, int 
   const int need = pages_for(s.tokens);
   int added = 0;
   while (static_cast<int>(s.page_ids.size()) < need) {
-    s.page_ids.push_back(new_page(s, s.device));
+    s.page_ids.push_back(new_page(request, block, s, s.device));
     ++added;
   }
   return added;
@@ -117,6 +144,11 @@ void KvStore::deref(std::uint64_t id) {
 }
 
 void KvStore::release(std::uint64_t request, const std::string& block) {
+  auto rit = reserved_.find({request, block});
+  if (rit != reserved_.end()) {
+    for (int s : rit->second.slots) free_slot(rit->second.pool_key, rit->second.device, s);
+    reserved_.erase(rit);
+  }
   auto it = segments_.find({request, block});
   if (it == segments_.end()) return;
   for (std::uint64_t id : it->second.page_ids) deref(id);
@@ -124,6 +156,11 @@ void KvStore::release(std::uint64_t request, const std::string& block) {
 }
 
 void KvStore::release_request(std::uint64_t request) {
+  for (auto rit = reserved_.lower_bound({request, std::string()});
+       rit != reserved_.end() && rit->first.first == request;) {
+    for (int s : rit->second.slots) free_slot(rit->second.pool_key, rit->second.device, s);
+    rit = reserved_.erase(rit);
+  }
   auto it = segments_.lower_bound({request, std::string()});
   while (it != segments_.end() && it->first.first == request) {
     for (std::uint64_t id : it->second.page_ids) deref(id);

@@ -81,6 +81,14 @@ class KvStore {
   // Physical slots of the segment's pages, in token order (the GPU page-table row).
   std::vector<int> page_slots(std::uint64_t request, const std::string& block) const;
 
+  // The GPU writes a token's K/V while the block runs, but the reference creates the page that
+  // holds it later: prompt pages after the prefill step (scenario.cpp:671-695), decode pages at
+  // chain end (append_decode_kv, scenario.cpp:697-719). To keep page ids bit-identical, physical
+  // slots are reserved ahead of the bookkeeping and bound when the page id is created.
+  // Returns the page-table row covering `total_pages` pages (existing, then reserved).
+  std::vector<int> reserve_slots(std::uint64_t request, const std::string& block,
+                                 const std::string& pool_key, int device, int total_pages);
+
  private:
   struct Page {
     std::int64_t bytes = 0;
@@ -100,11 +108,17 @@ class KvStore {
   const Segment* find(std::uint64_t request, const std::string& block) const;
   void reserve(int device, std::int64_t bytes);
   void unreserve(int device, std::int64_t bytes);
-  std::uint64_t new_page(const Segment& s, int device);
+  std::uint64_t new_page(std::uint64_t request, const std::string& block, const Segment& s, int device);
   void deref(std::uint64_t id);
   int alloc_slot(const std::string& pool_key, int device);
   void free_slot(const std::string& pool_key, int device, int slot);
 
+  struct Reserved {
+    std::string pool_key;
+    int device = -1;
+    std::vector<int> slots;
+  };
+  std::map<std::pair<std::uint64_t, std::string>, Reserved> reserved_;
   std::map<std::pair<std::uint64_t, std::string>, Segment> segments_;
   std::map<std::uint64_t, Page> pages_;
   std::map<std::pair<std::string, int>, SlotPool> pools_;

@@ -1,0 +1,650 @@
+// The executor loop on one device: requests walk their block chains; at every block instance
+// queued (request, step) rows are gathered into a batch (Pool::pop_batch), the batch runs on the
+// GPU (be_exec_batch: gather -> decoder layers -> scatter), and each member advances to its next
+// chain step, its first decode token, or its next token.
+//
+// Reference mapping (proj/core/src/scenario.cpp): on_arrival :194-208, dispatch_step :210-242
+// (instances created lazily at first use, ids "i<N>"), enqueue_step :310-334 (decode entries
+// whose cache sits on the instance's device are kv-resident), pump :465-557 (one lane per
+// device: next_runnable -> pop_batch -> run), on_batch_finish :559-578 (members advance with
+// pumps deferred until all advanced), advance_after_step / advance_from :595-669,
+// create_kv_for_step :671-695 (prompt pages after the prefill step), append_decode_kv :697-719
+// (one token on every chain segment at chain end). The cost-table duration of pump is replaced by
+// the real block run; speculation, scale-out, migration and reviews are outside this loop.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/blockhost.h"
+#include "kv.hpp"
+#include "pool.hpp"
+
+namespace bh {
+
+namespace {
+int pages_for(int tokens) { return (tokens + kPageTokens - 1) / kPageTokens; }
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+struct BeError : std::runtime_error {
+  int code;
+  BeError(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+}  // namespace
+
+struct Request {
+  int idx = 0;       // 0-based
+  int id = 0;        // reference request id (1-based, workload.cpp:89-96)
+  int tenant = 0;
+  int prompt = 0;
+  int output = 0;
+  int step = 0;
+  Phase phase = Phase::kPrefill;
+  int generated = 0;
+  int ctx = 0;       // context tokens (QueueEntry::context_tokens)
+  bool done = false;
+  int poff = 0;      // first row of its prompt in the prefill arena
+};
+
+struct PlannedBatch {
+  int inst = 0;
+  int block = 0;
+  Phase phase = Phase::kDecode;
+  std::vector<be_token> toks;
+  std::vector<int32_t> pt;  // [n_rows][stride]
+  int n_rows = 0;
+  int stride = 1;
+};
+
+class Runner {
+ public:
+  Runner(be_ctx* ctx, const bh_workload& w);
+  ~Runner();
+  void run(int max_batches);
+  void decode_step(const void* host_in, void* host_out, int* n_batches);
+  int live() const;
+  std::int64_t generated() const { return tokens_generated_; }
+  void* arena() { return arena_; }
+
+  std::vector<bh_batch_rec> recs;
+  std::vector<int32_t> m_req, m_step, m_ctx;
+  bh_step_stats stats{};
+
+ private:
+  // --- executor loop pieces (scenario.cpp)
+  void dispatch(Request& r);
+  void pump();
+  void finish_running();
+  void advance_after_step(Request& r, int step);
+  void advance_from(Request& r, int step);
+  std::string instance_for(int block);
+  PlannedBatch plan(const std::string& inst_id, const Batch& b);
+  void launch(const PlannedBatch& pb, const be_token* d_tok, const int32_t* d_pt);
+  void execute_direct(const PlannedBatch& pb);
+  void record(const PlannedBatch& pb, const Batch& b);
+  void account(const PlannedBatch& pb);
+  int chain_len(const Request& r) const { return chain_ptr_[r.tenant + 1] - chain_ptr_[r.tenant]; }
+  int chain_block(const Request& r, int step) const { return chain_blocks_[chain_ptr_[r.tenant] + step]; }
+
+  be_ctx* ctx_;
+  cudaStream_t st_;
+  int mode_ = 0;
+  bool use_graphs_ = false;
+  int max_batch_tokens_ = 4096;
+  int d_ = 0;
+  int max_ctx_ = 0;
+  std::vector<be_block_desc> descs_;
+  std::vector<std::string> names_;
+  std::vector<be_block*> blocks_;
+  std::vector<be_kv_pool*> pools_;
+  std::vector<int> chain_ptr_, chain_blocks_;
+  std::vector<Request> reqs_;
+  std::vector<std::string> inst_of_block_;
+  std::vector<int> inst_index_;  // block -> instance creation index
+  Pool pool_;
+  KvStore kv_;
+  be_workspace* ws_ = nullptr;
+  void* arena_ = nullptr;   // decode rows [n_req][d]
+  void* parena_ = nullptr;  // prefill rows [sum prompt][d]
+  bool has_running_ = false;
+  std::string running_inst_;
+  Batch running_;
+  PlannedBatch running_plan_;
+  std::vector<int> step_done_order_;  // lockstep: completion order of the last step
+  bool in_lockstep_step_ = false;
+  std::int64_t tokens_generated_ = 0;
+  int batches_run_ = 0;
+  // graph replay of a steady-state lockstep decode step
+  std::vector<std::tuple<int, int, int>> graph_sig_;  // (block, n_tokens, stride) per batch
+  cudaGraphExec_t graph_exec_ = nullptr;
+  cudaGraph_t graph_ = nullptr;
+  char* meta_host_ = nullptr;  // pinned staging
+  char* meta_dev_ = nullptr;
+  size_t meta_cap_ = 0;
+};
+
+Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
+  if (w.n_blocks <= 0 || w.n_tenants <= 0 || w.n_requests <= 0 || !w.blocks || !w.chain_ptr ||
+      !w.chain_blocks || !w.req_tenant || !w.req_prompt || !w.req_output)
+    throw BeError(BE_ERR_INVALID, "runner: incomplete workload");
+  st_ = static_cast<cudaStream_t>(be_ctx_stream(ctx));
+  mode_ = w.mode;
+  use_graphs_ = w.use_graphs != 0;
+  max_batch_tokens_ = w.max_batch_tokens > 0 ? w.max_batch_tokens : 4096;
+  d_ = w.blocks[0].d_model;
+  for (int b = 0; b < w.n_blocks; ++b) {
+    if (w.blocks[b].d_model != d_) throw BeError(BE_ERR_INVALID, "runner: blocks differ in d_model");
+    descs_.push_back(w.blocks[b]);
+    names_.push_back(w.blocks[b].name ? w.blocks[b].name : ("b" + std::to_string(b)));
+    descs_.back().name = nullptr;
+  }
+  chain_ptr_.assign(w.chain_ptr, w.chain_ptr + w.n_tenants + 1);
+  chain_blocks_.assign(w.chain_blocks, w.chain_blocks + chain_ptr_.back());
+  for (int t = 0; t < w.n_tenants; ++t) {
+    if (chain_ptr_[t + 1] <= chain_ptr_[t]) throw BeError(BE_ERR_INVALID, "runner: empty chain");
+    for (int s = chain_ptr_[t]; s < chain_ptr_[t + 1]; ++s)
+      if (chain_blocks_[s] < 0 || chain_blocks_[s] >= w.n_blocks)
+        throw BeError(BE_ERR_INVALID, "runner: chain names an unknown block");
+  }
+  // requests; per-block KV page demand
+  std::vector<long long> pages_needed(w.n_blocks, 0);
+  int poff = 0, max_prompt = 0;
+  for (int i = 0; i < w.n_requests; ++i) {
+    Request r;
+    r.idx = i;
+    r.id = i + 1;
+    r.tenant = w.req_tenant[i];
+    r.prompt = w.req_prompt[i];
+    r.output = w.req_output[i];
+    if (r.tenant < 0 || r.tenant >= w.n_tenants || r.prompt <= 0 || r.output <= 0)
+      throw BeError(BE_ERR_INVALID, "runner: bad request");
+    r.ctx = r.prompt;
+    r.poff = poff;
+    poff += r.prompt;
+    max_prompt = std::max(max_prompt, r.prompt);
+    const int total = r.prompt + r.output;
+    max_ctx_ = std::max(max_ctx_, total);
+    for (int s = chain_ptr_[r.tenant]; s < chain_ptr_[r.tenant + 1]; ++s)
+      pages_needed[chain_blocks_[s]] += pages_for(total) + 1;
+    reqs_.push_back(r);
+  }
+  int dff = 0, H = 0;
+  for (int b = 0; b < w.n_blocks; ++b) {
+    if (descs_[b].max_pos < max_ctx_) descs_[b].max_pos = max_ctx_ + 16;
+    be_block_desc d = descs_[b];
+    d.name = names_[b].c_str();
+    be_block* blk = nullptr;
+    int rc = be_block_load(ctx, &d, &blk);
+    if (rc != BE_OK) throw BeError(rc, std::string("block load: ") + be_last_error(ctx));
+    blocks_.push_back(blk);
+    be_kv_pool* kp = nullptr;
+    const int np = static_cast<int>(std::max<long long>(1, pages_needed[b]));
+    rc = be_kv_pool_create(ctx, blk, np, &kp);
+    if (rc != BE_OK) throw BeError(rc, std::string("kv pool: ") + be_last_error(ctx));
+    pools_.push_back(kp);
+    kv_.attach_pool(names_[b], 0, np);
+    if (dff == 0) {
+      dff = descs_[b].d_ff;
+      H = descs_[b].n_heads;
+    } else if (dff != descs_[b].d_ff || H != descs_[b].n_heads) {
+      throw BeError(BE_ERR_INVALID, "runner: blocks differ in d_ff / heads");
+    }
+  }
+  inst_of_block_.assign(w.n_blocks, "");
+  inst_index_.assign(w.n_blocks, -1);
+  const int max_tok = std::max(std::min(poff, std::max(max_batch_tokens_, max_prompt)), w.n_requests);
+  int rc = be_workspace_create(ctx, d_, dff, H, max_tok, w.n_requests, pages_for(max_ctx_) + 1, &ws_);
+  if (rc != BE_OK) throw BeError(rc, std::string("workspace: ") + be_last_error(ctx));
+  ck(cudaMalloc(&arena_, (size_t)w.n_requests * d_ * 2), "arena");
+  ck(cudaMalloc(&parena_, (size_t)poff * d_ * 2), "prefill arena");
+  for (const auto& r : reqs_) {
+    const std::string sid = "inputs:req" + std::to_string(r.id);
+    rc = be_synth_rows(ctx, static_cast<char*>(parena_) + (size_t)r.poff * d_ * 2,
+                       (int64_t)r.prompt * d_, w.seed, sid.c_str(), 1.7320508f, st_);
+    if (rc != BE_OK) throw BeError(rc, "synthetic prompts");
+  }
+  ck(cudaStreamSynchronize(st_), "init");
+}
+
+Runner::~Runner() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  if (meta_host_) cudaFreeHost(meta_host_);
+  if (meta_dev_) cudaFree(meta_dev_);
+  if (arena_) cudaFree(arena_);
+  if (parena_) cudaFree(parena_);
+  if (ws_) be_workspace_free(ws_);
+  for (auto* p : pools_) be_kv_pool_free(p);
+  for (auto* b : blocks_) be_block_free(b);
+}
+
+int Runner::live() const {
+  int n = 0;
+  for (const auto& r : reqs_) n += r.done ? 0 : 1;
+  return n;
+}
+
+std::string Runner::instance_for(int block) {
+  if (inst_of_block_[block].empty()) {
+    // created on first dispatch, ready at once (parameters resident: no load time here)
+    Instance& in = pool_.create(names_[block], 0, 0, 0);
+    inst_of_block_[block] = in.id;
+    int created = 0;
+    for (int b : inst_index_) created += b >= 0 ? 1 : 0;
+    inst_index_[block] = created;
+  }
+  return inst_of_block_[block];
+}
+
+void Runner::dispatch(Request& r) {
+  const int block = chain_block(r, r.step);
+  const std::string inst = instance_for(block);
+  Entry e;
+  e.request_id = r.id;
+  e.chain_step = r.step;
+  e.phase = r.phase;
+  e.tokens = r.phase == Phase::kPrefill ? r.prompt : 1;
+  e.context_tokens = r.ctx;
+  e.kv_resident = r.phase == Phase::kDecode && kv_.device_of(r.id, names_[block]) == 0;
+  pool_.enqueue(inst, e);
+}
+
+PlannedBatch Runner::plan(const std::string& inst_id, const Batch& b) {
+  PlannedBatch pb;
+  const Instance& in = pool_.get(inst_id);
+  int block = 0;
+  while (names_[block] != in.block_id) ++block;
+  pb.block = block;
+  pb.inst = inst_index_[block];
+  pb.phase = b.phase;
+  pb.n_rows = static_cast<int>(b.members.size());
+  pb.stride = pages_for(max_ctx_) + 1;
+  pb.pt.assign((size_t)pb.n_rows * pb.stride, -1);
+  for (int m = 0; m < pb.n_rows; ++m) {
+    const Entry& e = b.members[m];
+    Request& r = reqs_[e.request_id - 1];
+    const std::string& bn = names_[block];
+    const int have = kv_.tokens(r.id, bn);
+    const int first = b.phase == Phase::kPrefill ? 0 : have;
+    const int count = b.phase == Phase::kPrefill ? r.prompt : 1;
+    const std::vector<int> row = kv_.reserve_slots(r.id, bn, bn, 0, pages_for(first + count));
+    std::copy(row.begin(), row.end(), pb.pt.begin() + (size_t)m * pb.stride);
+    for (int i = 0; i < count; ++i) {
+      const int pos = first + i;
+      be_token t;
+      if (b.phase == Phase::kPrefill) {
+        t.src_row = r.poff + i;
+        t.dst_row = r.poff + i;
+      } else {
+        t.src_row = r.idx;
+        t.dst_row = r.idx;
+      }
+      t.kv_slot = row[pos / kPageTokens] * kPageTokens + pos % kPageTokens;
+      t.pos = pos;
+      t.pt_row = m;
+      pb.toks.push_back(t);
+    }
+  }
+  return pb;
+}
+
+void Runner::launch(const PlannedBatch& pb, const be_token* d_tok, const int32_t* d_pt) {
+  void* arena = pb.phase == Phase::kPrefill ? parena_ : arena_;
+  const int rc = be_exec_batch_dev(ctx_, blocks_[pb.block], pools_[pb.block], ws_,
+                                   pb.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE,
+                                   static_cast<int>(pb.toks.size()), d_tok, pb.stride, d_pt, arena,
+                                   arena, st_);
+  if (rc != BE_OK) throw BeError(rc, std::string("exec: ") + be_last_error(ctx_));
+}
+
+void Runner::execute_direct(const PlannedBatch& pb) {
+  void* arena = pb.phase == Phase::kPrefill ? parena_ : arena_;
+  const int rc = be_exec_batch(ctx_, blocks_[pb.block], pools_[pb.block], ws_,
+                               pb.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE,
+                               static_cast<int>(pb.toks.size()), pb.toks.data(), pb.n_rows,
+                               pb.stride, pb.pt.data(), arena, arena, st_);
+  if (rc != BE_OK) throw BeError(rc, std::string("exec: ") + be_last_error(ctx_));
+  // be_exec_batch stages metadata from pageable memory: keep the host side in step
+  ck(cudaStreamSynchronize(st_), "batch");
+}
+
+void Runner::record(const PlannedBatch& pb, const Batch& b) {
+  bh_batch_rec rec;
+  rec.instance = pb.inst;
+  rec.block = pb.block;
+  rec.phase = b.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE;
+  rec.n_members = static_cast<int32_t>(b.members.size());
+  rec.first_member = static_cast<int32_t>(m_req.size());
+  for (const auto& e : b.members) {
+    m_req.push_back(e.request_id);
+    m_step.push_back(e.chain_step);
+    m_ctx.push_back(e.context_tokens);
+  }
+  recs.push_back(rec);
+}
+
+void Runner::account(const PlannedBatch& pb) {
+  const be_block_desc& D = descs_[pb.block];
+  const double d = D.d_model, F = D.d_ff, L = D.n_layers;
+  const double n = static_cast<double>(pb.toks.size());
+  stats.weight_bytes += (double)be_block_param_bytes(blocks_[pb.block]);
+  double ctx_sum = 0.0;
+  for (const auto& t : pb.toks) ctx_sum += t.pos + 1;
+  stats.kv_bytes += ctx_sum * L * 2.0 * d * 2.0;
+  stats.act_bytes += 2.0 * n * d * 2.0;
+  stats.flops += 2.0 * n * L * (4.0 * d * d + 3.0 * d * F) + 4.0 * ctx_sum * d * L;
+  stats.launches += be_exec_batch_launches(ctx_, blocks_[pb.block], static_cast<int>(pb.toks.size()), pb.stride);
+}
+
+void Runner::pump() {
+  if (has_running_) return;  // decode joins only happen on multi-lane timelines
+  Instance* in = pool_.next_runnable(0, 0);
+  if (in == nullptr) return;
+  running_inst_ = in->id;
+  running_ = pool_.pop_batch(in->id, max_batch_tokens_, 0);
+  running_plan_ = plan(running_inst_, running_);
+  record(running_plan_, running_);
+  has_running_ = true;
+}
+
+void Runner::finish_running() {
+  // the block run (replaces the cost-table duration of pump)
+  execute_direct(running_plan_);
+  account(running_plan_);
+  ++batches_run_;
+  has_running_ = false;
+  pool_.finish_batch(running_inst_, 0);
+  const Batch b = running_;
+  for (const auto& m : b.members) advance_after_step(reqs_[m.request_id - 1], m.chain_step);
+  pump();
+}
+
+void Runner::advance_after_step(Request& r, int step) {
+  if (r.phase == Phase::kPrefill) {
+    const std::string& bn = names_[chain_block(r, step)];
+    if (!kv_.has_segment(r.id, bn)) {
+      kv_.create_segment(r.id, bn, 0, be_block_kv_bytes_per_token(blocks_[chain_block(r, step)]));
+      kv_.append_tokens(r.id, bn, r.prompt);
+    }
+  }
+  advance_from(r, step);
+}
+
+void Runner::advance_from(Request& r, int step) {
+  if (step + 1 < chain_len(r)) {
+    r.step = step + 1;
+    dispatch(r);
+    return;
+  }
+  if (r.phase == Phase::kPrefill) {
+    // first token: the last prompt row's output becomes the first decode input
+    ck(cudaMemcpyAsync(static_cast<char*>(arena_) + (size_t)r.idx * d_ * 2,
+                       static_cast<char*>(parena_) + (size_t)(r.poff + r.prompt - 1) * d_ * 2,
+                       (size_t)d_ * 2, cudaMemcpyDeviceToDevice, st_),
+       "first token row");
+    r.generated = 1;
+    ++tokens_generated_;
+    r.ctx = r.prompt + 1;
+    if (r.generated >= r.output) {
+      r.done = true;
+      kv_.release_request(r.id);
+      return;
+    }
+    r.phase = Phase::kDecode;
+    r.step = 0;
+    if (mode_ == 0) dispatch(r);
+    return;
+  }
+  // decode token done: one more token on every segment of the chain
+  for (int s = 0; s < chain_len(r); ++s) {
+    const std::string& bn = names_[chain_block(r, s)];
+    if (kv_.has_segment(r.id, bn)) kv_.append_tokens(r.id, bn, 1);
+  }
+  r.generated += 1;
+  ++tokens_generated_;
+  r.ctx += 1;
+  if (r.generated >= r.output) {
+    r.done = true;
+    kv_.release_request(r.id);
+    return;
+  }
+  r.step = 0;
+  if (mode_ == 0) {
+    dispatch(r);
+  } else {
+    step_done_order_.push_back(r.idx);
+  }
+}
+
+void Runner::run(int max_batches) {
+  if (batches_run_ == 0 && !has_running_) {
+    // arrivals at t = 0 in request order; the first one starts the lane at once
+    for (auto& r : reqs_) {
+      dispatch(r);
+      pump();
+    }
+  }
+  int n = 0;
+  while (has_running_ && (max_batches <= 0 || n < max_batches)) {
+    finish_running();
+    ++n;
+  }
+  ck(cudaStreamSynchronize(st_), "run");
+  if (mode_ == 1 && !has_running_) {
+    // lockstep: decode starts for everyone together, in request order
+    step_done_order_.clear();
+    for (const auto& r : reqs_)
+      if (!r.done && r.phase == Phase::kDecode) step_done_order_.push_back(r.idx);
+  }
+}
+
+void Runner::decode_step(const void* host_in, void* host_out, int* n_batches) {
+  if (mode_ != 1) throw BeError(BE_ERR_STATE, "decode_step needs lockstep mode");
+  if (has_running_) throw BeError(BE_ERR_STATE, "prefill still running");
+  std::vector<int> order = step_done_order_;
+  step_done_order_.clear();
+  // host rows are the live requests in request order; contiguous runs move in one copy
+  std::vector<int> rows = order;
+  std::sort(rows.begin(), rows.end());
+  const size_t row_bytes = (size_t)d_ * 2;
+  auto copy_rows = [&](bool to_dev, void* host) {
+    size_t i = 0;
+    while (i < rows.size()) {
+      size_t j = i + 1;
+      while (j < rows.size() && rows[j] == rows[j - 1] + 1) ++j;
+      char* dev = static_cast<char*>(arena_) + (size_t)rows[i] * row_bytes;
+      char* hp = static_cast<char*>(host) + i * row_bytes;
+      ck(cudaMemcpyAsync(to_dev ? (void*)dev : (void*)hp, to_dev ? (void*)hp : (void*)dev,
+                         (j - i) * row_bytes,
+                         to_dev ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st_),
+         "host rows");
+      i = j;
+    }
+  };
+  if (host_in != nullptr) copy_rows(true, const_cast<void*>(host_in));
+  for (int idx : order) dispatch(reqs_[idx]);
+  // plan the whole step on the host (bookkeeping does not depend on GPU results)
+  std::vector<PlannedBatch> plans;
+  std::vector<Batch> batches;
+  stats = bh_step_stats{};
+  for (;;) {
+    pump();
+    if (!has_running_) break;
+    plans.push_back(running_plan_);
+    batches.push_back(running_);
+    has_running_ = false;
+    pool_.finish_batch(running_inst_, 0);
+    account(running_plan_);
+    ++batches_run_;
+    for (const auto& m : running_.members) advance_after_step(reqs_[m.request_id - 1], m.chain_step);
+  }
+  if (n_batches) *n_batches = static_cast<int>(plans.size());
+  // metadata layout: per batch [tokens][page table], 256-byte aligned
+  std::vector<size_t> off_tok(plans.size()), off_pt(plans.size());
+  size_t total = 0;
+  std::vector<std::tuple<int, int, int>> sig;
+  for (size_t i = 0; i < plans.size(); ++i) {
+    off_tok[i] = total;
+    total += (plans[i].toks.size() * sizeof(be_token) + 255) & ~size_t(255);
+    off_pt[i] = total;
+    total += (plans[i].pt.size() * sizeof(int32_t) + 255) & ~size_t(255);
+    sig.emplace_back(plans[i].block, static_cast<int>(plans[i].toks.size()), plans[i].stride);
+  }
+  if (total > meta_cap_) {
+    if (meta_host_) cudaFreeHost(meta_host_);
+    if (meta_dev_) cudaFree(meta_dev_);
+    meta_cap_ = total * 2;
+    ck(cudaMallocHost(&meta_host_, meta_cap_), "meta host");
+    ck(cudaMalloc(&meta_dev_, meta_cap_), "meta dev");
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+    graph_sig_.clear();
+  }
+  ck(cudaStreamSynchronize(st_), "meta reuse");  // previous step may still read the staging
+  for (size_t i = 0; i < plans.size(); ++i) {
+    std::memcpy(meta_host_ + off_tok[i], plans[i].toks.data(), plans[i].toks.size() * sizeof(be_token));
+    std::memcpy(meta_host_ + off_pt[i], plans[i].pt.data(), plans[i].pt.size() * sizeof(int32_t));
+  }
+  ck(cudaMemcpyAsync(meta_dev_, meta_host_, total, cudaMemcpyHostToDevice, st_), "meta h2d");
+  auto launch_all = [&]() {
+    for (size_t i = 0; i < plans.size(); ++i)
+      launch(plans[i], reinterpret_cast<const be_token*>(meta_dev_ + off_tok[i]),
+             reinterpret_cast<const int32_t*>(meta_dev_ + off_pt[i]));
+  };
+  stats.graph_replayed = 0;
+  if (use_graphs_ && sig == graph_sig_ && graph_exec_ != nullptr) {
+    ck(cudaGraphLaunch(graph_exec_, st_), "graph launch");
+    stats.graph_replayed = 1;
+  } else if (use_graphs_ && sig == graph_sig_) {
+    // second step with this structure: capture it
+    ck(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "capture begin");
+    try {
+      launch_all();
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(st_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    if (graph_) cudaGraphDestroy(graph_);
+    ck(cudaStreamEndCapture(st_, &graph_), "capture end");
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    ck(cudaGraphInstantiate(&graph_exec_, graph_, 0), "graph instantiate");
+    ck(cudaGraphLaunch(graph_exec_, st_), "graph launch");
+    stats.graph_replayed = 1;
+  } else {
+    launch_all();
+    graph_sig_ = sig;
+    if (graph_exec_) {
+      cudaGraphExecDestroy(graph_exec_);
+      graph_exec_ = nullptr;
+    }
+  }
+  for (size_t i = 0; i < plans.size(); ++i) record(plans[i], batches[i]);
+  if (host_out != nullptr) {
+    copy_rows(false, host_out);
+    ck(cudaStreamSynchronize(st_), "d2h sync");
+  }
+}
+
+}  // namespace bh
+
+// ------------------------------------------------------------------------------ C ABI
+struct bh_runner {
+  std::unique_ptr<bh::Runner> r;
+  std::string err;
+};
+
+namespace {
+template <class F>
+int guard(bh_runner* h, F&& f) {
+  try {
+    f();
+    return BE_OK;
+  } catch (const bh::BeError& e) {
+    if (h) h->err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    if (h) h->err = e.what();
+    return BE_ERR_INVALID;
+  } catch (const std::logic_error& e) {
+    if (h) h->err = e.what();
+    return BE_ERR_STATE;
+  } catch (const std::exception& e) {
+    if (h) h->err = e.what();
+    return BE_ERR_RUNTIME;
+  }
+}
+}  // namespace
+
+extern "C" int bh_runner_create(be_ctx* ctx, const bh_workload* w, bh_runner** out) {
+  if (ctx == nullptr || w == nullptr || out == nullptr) return BE_ERR_INVALID;
+  *out = nullptr;
+  auto* h = new bh_runner();
+  const int rc = guard(h, [&] { h->r = std::make_unique<bh::Runner>(ctx, *w); });
+  if (rc != BE_OK) {
+    std::fprintf(stderr, "bh_runner_create: %s\n", h->err.c_str());
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return BE_OK;
+}
+extern "C" int bh_runner_free(bh_runner* h) {
+  if (h == nullptr) return BE_ERR_INVALID;
+  delete h;
+  return BE_OK;
+}
+extern "C" const char* bh_runner_last_error(const bh_runner* h) { return h ? h->err.c_str() : "null"; }
+extern "C" int bh_runner_run(bh_runner* h, int max_batches) {
+  if (h == nullptr) return BE_ERR_INVALID;
+  return guard(h, [&] { h->r->run(max_batches); });
+}
+extern "C" int bh_runner_decode_step(bh_runner* h, const void* in, void* out, int* n_batches) {
+  if (h == nullptr) return BE_ERR_INVALID;
+  return guard(h, [&] { h->r->decode_step(in, out, n_batches); });
+}
+extern "C" int bh_runner_live_requests(const bh_runner* h) { return h ? h->r->live() : 0; }
+extern "C" int64_t bh_runner_tokens_generated(const bh_runner* h) { return h ? h->r->generated() : 0; }
+extern "C" void* bh_runner_arena(bh_runner* h) { return h ? h->r->arena() : nullptr; }
+extern "C" int bh_runner_trace(const bh_runner* h, bh_batch_rec* recs, int cap, int* n_out,
+                               int32_t* mreq, int32_t* mstep, int32_t* mctx, int mcap, int* m_out) {
+  if (h == nullptr || n_out == nullptr) return BE_ERR_INVALID;
+  const auto& R = *h->r;
+  *n_out = static_cast<int>(R.recs.size());
+  if (m_out) *m_out = static_cast<int>(R.m_req.size());
+  if (recs != nullptr)
+    for (int i = 0; i < std::min(cap, *n_out); ++i) recs[i] = R.recs[i];
+  const int nm = std::min<int>(mcap, static_cast<int>(R.m_req.size()));
+  for (int i = 0; i < nm; ++i) {
+    if (mreq) mreq[i] = R.m_req[i];
+    if (mstep) mstep[i] = R.m_step[i];
+    if (mctx) mctx[i] = R.m_ctx[i];
+  }
+  return BE_OK;
+}
+extern "C" int bh_runner_clear_trace(bh_runner* h) {
+  if (h == nullptr) return BE_ERR_INVALID;
+  h->r->recs.clear();
+  h->r->m_req.clear();
+  h->r->m_step.clear();
+  h->r->m_ctx.clear();
+  return BE_OK;
+}
+extern "C" int bh_runner_step_stats(const bh_runner* h, bh_step_stats* out) {
+  if (h == nullptr || out == nullptr) return BE_ERR_INVALID;
+  *out = h->r->stats;
+  return BE_OK;
+}

@@ -1,0 +1,161 @@
+"""Python handle over the C++ executor loop (include/blockhost.h bh_runner_*)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import check, lib, BlockDesc, BlockExecError
+from .device import Context
+from .workloads import Workload
+
+
+class BatchRec(C.Structure):
+    _fields_ = [("instance", C.c_int32), ("block", C.c_int32), ("phase", C.c_int32),
+                ("n_members", C.c_int32), ("first_member", C.c_int32)]
+
+
+class StepStats(C.Structure):
+    _fields_ = [("weight_bytes", C.c_double), ("kv_bytes", C.c_double),
+                ("act_bytes", C.c_double), ("flops", C.c_double), ("launches", C.c_int),
+                ("graph_replayed", C.c_int)]
+
+
+class WorkloadC(C.Structure):
+    _fields_ = [("n_blocks", C.c_int), ("blocks", C.c_void_p), ("n_tenants", C.c_int),
+                ("chain_ptr", C.c_void_p), ("chain_blocks", C.c_void_p),
+                ("n_requests", C.c_int), ("req_tenant", C.c_void_p),
+                ("req_prompt", C.c_void_p), ("req_output", C.c_void_p),
+                ("max_batch_tokens", C.c_int), ("mode", C.c_int), ("use_graphs", C.c_int),
+                ("seed", C.c_uint64)]
+
+
+_bound = False
+
+
+def _bind():
+    global _bound
+    if _bound:
+        return
+    L = lib()
+    P, I = C.c_void_p, C.c_int
+    for name, res, args in [
+        ("bh_runner_create", I, [P, P, C.POINTER(C.c_void_p)]),
+        ("bh_runner_free", I, [P]),
+        ("bh_runner_last_error", C.c_char_p, [P]),
+        ("bh_runner_run", I, [P, I]),
+        ("bh_runner_decode_step", I, [P, P, P, P]),
+        ("bh_runner_live_requests", I, [P]),
+        ("bh_runner_tokens_generated", C.c_int64, [P]),
+        ("bh_runner_trace", I, [P, P, I, P, P, P, P, I, P]),
+        ("bh_runner_clear_trace", I, [P]),
+        ("bh_runner_arena", P, [P]),
+        ("bh_runner_step_stats", I, [P, P]),
+    ]:
+        fn = getattr(L, name)
+        fn.restype, fn.argtypes = res, args
+    _bound = True
+
+
+class Runner:
+    """Multi-tenant block-chain execution on one GPU.
+
+    mode 0: the reference's event order (arrivals at t=0, interleaved prefill/decode);
+    mode 1: lockstep (all prompts prefilled, then decode one token for everyone per step).
+    """
+
+    def __init__(self, ctx: Context, wl: Workload, mode: int = 1, use_graphs: bool = True):
+        _bind()
+        self.ctx, self.wl = ctx, wl
+        s = wl.shape
+        self._names = [n.encode() for n in wl.block_names]
+        descs = (BlockDesc * len(wl.block_names))()
+        for i, nm in enumerate(self._names):
+            descs[i] = BlockDesc(s.n_layers, s.d_model, s.n_heads, s.head_dim, s.d_ff, s.max_pos,
+                                 s.norm_eps, s.rope_theta, s.init_scale, wl.seed, nm)
+        ptr = np.zeros(len(wl.chains) + 1, np.int32)
+        flat = []
+        for t, ch in enumerate(wl.chains):
+            flat += ch
+            ptr[t + 1] = len(flat)
+        self._keep = [descs, ptr, np.array(flat, np.int32),
+                      np.array(wl.req_tenant, np.int32), np.array(wl.req_prompt, np.int32),
+                      np.array(wl.req_output, np.int32)]
+        k = self._keep
+        w = WorkloadC(len(wl.block_names), C.cast(descs, C.c_void_p), len(wl.chains),
+                      k[1].ctypes.data, k[2].ctypes.data, wl.n_requests, k[3].ctypes.data,
+                      k[4].ctypes.data, k[5].ctypes.data, wl.max_batch_tokens, mode,
+                      1 if use_graphs else 0, wl.seed)
+        h = C.c_void_p()
+        rc = lib().bh_runner_create(ctx.h, C.byref(w), C.byref(h))
+        if rc != 0:
+            raise BlockExecError(rc, "bh_runner_create failed (see stderr): "
+                                 + lib().be_last_error(ctx.h).decode())
+        self.h = h
+
+    def _check(self, rc):
+        if rc != 0:
+            raise BlockExecError(rc, lib().bh_runner_last_error(self.h).decode())
+
+    def run(self, max_batches: int = 0) -> None:
+        self._check(lib().bh_runner_run(self.h, max_batches))
+
+    def decode_step(self, host_in=None, host_out=None) -> int:
+        n = C.c_int(0)
+        pin = C.c_void_p(host_in.data_ptr() if hasattr(host_in, "data_ptr") else
+                         (host_in.ctypes.data if host_in is not None else 0))
+        pout = C.c_void_p(host_out.data_ptr() if hasattr(host_out, "data_ptr") else
+                          (host_out.ctypes.data if host_out is not None else 0))
+        self._check(lib().bh_runner_decode_step(self.h, pin, pout, C.byref(n)))
+        return n.value
+
+    @property
+    def live(self) -> int:
+        return lib().bh_runner_live_requests(self.h)
+
+    @property
+    def tokens_generated(self) -> int:
+        return lib().bh_runner_tokens_generated(self.h)
+
+    @property
+    def arena_ptr(self) -> int:
+        return lib().bh_runner_arena(self.h)
+
+    def step_stats(self) -> dict:
+        s = StepStats()
+        self._check(lib().bh_runner_step_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in StepStats._fields_}
+
+    def trace(self):
+        """[(instance_idx, block_idx, phase, [(req, step, ctx), ...]), ...]"""
+        n, m = C.c_int(0), C.c_int(0)
+        self._check(lib().bh_runner_trace(self.h, None, 0, C.byref(n), None, None, None, 0,
+                                          C.byref(m)))
+        recs = (BatchRec * max(1, n.value))()
+        req = np.zeros(max(1, m.value), np.int32)
+        step = np.zeros_like(req)
+        ctxs = np.zeros_like(req)
+        self._check(lib().bh_runner_trace(self.h, C.cast(recs, C.c_void_p), n.value, C.byref(n),
+                                          req.ctypes.data, step.ctypes.data, ctxs.ctypes.data,
+                                          m.value, C.byref(m)))
+        out = []
+        for i in range(n.value):
+            r = recs[i]
+            mem = [(int(req[j]), int(step[j]), int(ctxs[j]))
+                   for j in range(r.first_member, r.first_member + r.n_members)]
+            out.append((r.instance, r.block, r.phase, mem))
+        return out
+
+    def clear_trace(self):
+        self._check(lib().bh_runner_clear_trace(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().bh_runner_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
