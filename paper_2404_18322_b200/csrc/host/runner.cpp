@@ -552,7 +552,6 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches) {
       graph_exec_ = nullptr;
     }
   }
-  for (size_t i = 0; i < plans.size(); ++i) record(plans[i], batches[i]);
   if (host_out != nullptr) {
     copy_rows(false, host_out);
     ck(cudaStreamSynchronize(st_), "d2h sync");
