@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams P) {
     l = l * corr + psum;
     m = m_new;
   }
+  // the next (PDL-launched) GEMM may start streaming its weights under this kernel's tail
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // merge token groups inside the warp (lanes with equal `sub`)
 #pragma unroll
   for (int off = LPT; off < 32; off <<= 1) {

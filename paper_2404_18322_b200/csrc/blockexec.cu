@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -61,6 +62,8 @@ struct be_ctx {
   float* gemm_ws = nullptr;
   size_t gemm_ws_elems = 0;
   int* gemm_counters = nullptr;
+  int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
+  int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
 };
 
 struct be_block {
@@ -217,6 +220,8 @@ extern "C" int be_ctx_create(int device, be_ctx** out) {
     return BE_ERR_CUDA;
   }
   ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  if (const char* g = getenv("BE_GEMM_GRID")) ctx->gemm_grid_cap = atoi(g);
+  if (const char* p = getenv("BE_PDL")) ctx->use_pdl = atoi(p) != 0;
   *out = ctx;
   return BE_OK;
 }
@@ -491,12 +496,13 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const CUtensorMap* mw, const CUtenso
   L.N = N;
   L.K = K;
   L.bn = bn;
-  int ks = bx::gemm_pick_ksplit(N, K, ntok, bn, ctx->num_sms);
-  const int ntiles = (ntok + bn - 1) / bn;
-  while (ks > 1 && ((size_t)ks * ntiles * bn * N > ws->splitws_elems ||
-                    (N / 128) * ntiles > ws->n_counters))
-    --ks;
-  L.ksplit = ks;
+  const bx::GemmPlan p = bx::gemm_plan(N, K, ntok, bn, ctx->num_sms, ws->splitws_elems,
+                                       ws->n_counters, ctx->gemm_grid_cap);
+  if (p.ws_needed > ws->splitws_elems)
+    return fail(ctx, BE_ERR_INVALID, "gemm N=%d K=%d ntok=%d: stream-K workspace too small", N, K, ntok);
+  L.grid = p.grid;
+  L.max_contrib = p.max_contrib;
+  L.pdl = ctx->use_pdl;
   epi.ws = ws->splitws;
   epi.counters = ws->counters;
   L.epi = epi;
@@ -697,21 +703,24 @@ extern "C" int be_synth_rows(be_ctx* ctx, void* dst, int64_t n, uint64_t seed, c
 }
 
 extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out, int N, int K,
-                            int ntok, int ksplit, void* stream) {
-  if (ctx == nullptr || N % 128 != 0 || K % 64 != 0 || ntok <= 0) return BE_ERR_INVALID;
+                            int ntok, int grid_cap, void* stream) {
+  if (ctx == nullptr || N % 128 != 0 || K % 64 != 0 || ntok <= 0 || grid_cap < 0)
+    return BE_ERR_INVALID;
   const int bn = bx::gemm_pick_bn(ntok);
   CUtensorMap mw, mx;
   int rc;
   if ((rc = make_map(ctx, &mw, w, N, K, 128)) != BE_OK) return rc;
   if ((rc = make_map(ctx, &mx, x, ntok, K, bn)) != BE_OK) return rc;
-  const int ntiles = (ntok + bn - 1) / bn;
-  if (ksplit <= 0) ksplit = bx::gemm_pick_ksplit(N, K, ntok, bn, ctx->num_sms);
-  const size_t need = (size_t)ksplit * ntiles * bn * N;
-  if (ksplit > 1 && need > ctx->gemm_ws_elems) {
+  const bx::GemmPlan p =
+      bx::gemm_plan(N, K, ntok, bn, ctx->num_sms, (size_t)1 << 40, 1 << 16, grid_cap);
+  if (p.ws_needed > ctx->gemm_ws_elems) {
     if (ctx->gemm_ws) cudaFree(ctx->gemm_ws);
-    BE_CUDA(ctx, cudaMalloc(&ctx->gemm_ws, need * sizeof(float)));
-    ctx->gemm_ws_elems = need;
+    ctx->gemm_ws = nullptr;
+    BE_CUDA(ctx, cudaMalloc(&ctx->gemm_ws, p.ws_needed * sizeof(float)));
+    ctx->gemm_ws_elems = p.ws_needed;
   }
+  const int tiles = (N / 128) * ((ntok + bn - 1) / bn);
+  if (tiles > (1 << 16)) return fail(ctx, BE_ERR_INVALID, "gemm: too many tiles");
   if (ctx->gemm_counters == nullptr) {
     BE_CUDA(ctx, cudaMalloc(&ctx->gemm_counters, (1 << 16) * sizeof(int)));
     BE_CUDA(ctx, cudaMemset(ctx->gemm_counters, 0, (1 << 16) * sizeof(int)));
@@ -722,7 +731,9 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.N = N;
   L.K = K;
   L.bn = bn;
-  L.ksplit = ksplit;
+  L.grid = p.grid;
+  L.max_contrib = p.max_contrib;
+  L.pdl = ctx->use_pdl;
   L.epi.mode = bx::kStore;
   L.epi.ntok = ntok;
   L.epi.out = static_cast<bf16*>(out);

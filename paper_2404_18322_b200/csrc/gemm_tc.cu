@@ -1,12 +1,32 @@
 // tcgen05 / TMEM / TMA block-forward GEMM (see gemm_tc.cuh for the contract).
+//
+// Persistent stream-K schedule: the (tile, k-block) iteration space of the whole GEMM is cut
+// into gridDim.x equal contiguous ranges, one per CTA (grid <= #SMs, one CTA per SM), so every
+// SM streams the same number of weight bytes whatever the tile count (no wave quantisation:
+// 172 gate/up tiles or 32 O-proj tiles both spread over all 148 SMs). A CTA range may start or
+// end inside a tile; such partial tiles meet in an fp32 workspace (L2-resident) and the last
+// contributor to arrive runs the fused epilogue (no CTA ever waits on another).
+//
+// Warp roles (192 threads): warp 0 = TMA producer (one elected lane), warp 1 = MMA issuer (one
+// elected lane) + TMEM allocator, warps 2..5 = epilogue (warp w drains TMEM lanes 32*(w%4)..).
+// Two TMEM accumulators ping-pong so the MMA of the next tile overlaps the epilogue of this one.
+// Programmatic dependent launch: weight tiles (which no earlier kernel writes) are requested
+// before griddepcontrol.wait, so the weight stream starts under the previous kernel's tail.
 #include "gemm_tc.cuh"
 
 namespace bx {
 
-// Applies the fused epilogue to 16 consecutive token columns [c0, c0+16) of this thread's
-// feature row f. `t0` is the first token index of the chunk; all lanes of a warp share t0.
-template <int BN>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int N, int f, int t0,
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Applies the fused epilogue to 16 consecutive token columns starting at token t0 for this
+// thread's feature row f; all lanes of a warp share t0.
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0,
                                                const float (&acc)[16]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -59,169 +79,240 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int N, int f,
   }
 }
 
+struct SkRange {
+  long long total;  // iterations = tiles * nkb
+  int G;            // CTAs
+  __device__ __forceinline__ long long begin(int c) const { return (long long)c * total / G; }
+  // CTA whose range holds iteration it
+  __device__ __forceinline__ int cta_of(long long it) const {
+    return (int)(((it + 1) * G - 1) / total);
+  }
+};
+
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(128, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w,
-                   const __grid_constant__ CUtensorMap map_x, int N, int K, int ksplit,
-                   EpiParams E) {
+__global__ void __launch_bounds__(192, 1)
+    gemm_sk_kernel(const __grid_constant__ CUtensorMap map_w,
+                   const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
+                   int max_contrib, EpiParams E) {
   using S = GemmSmem<BN>;
-  constexpr uint32_t kTmemCols = tmem_cols<BN>();
+  constexpr uint32_t kTmemCols = tmem_cols<2 * BN>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment for the 128B swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * S::kABytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * S::kBBytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* accum_full = empty + STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accum_full + 1);
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   int* flag = reinterpret_cast<int*>(tmem_holder + 1);
 
   const int warp = threadIdx.x >> 5;
-  const int m_tile = blockIdx.x;
-  const int n_tile = blockIdx.y;
-  const int split = blockIdx.z;
-  const int m0 = m_tile * kBM;
-  const int n0 = n_tile * BN;
+  const int lane = threadIdx.x & 31;
+  const int nkb = K / kBK;
+  SkRange R{(long long)m_tiles * n_tiles * nkb, (int)gridDim.x};
+  const long long it_begin = R.begin(blockIdx.x);
+  const long long it_end = R.begin(blockIdx.x + 1);
 
-  const int num_kb = K / kBK;
-  const int kb_begin = (int)((long long)split * num_kb / ksplit);
-  const int kb_end = (int)((long long)(split + 1) * num_kb / ksplit);
-  const int nkb = kb_end - kb_begin;
-
-  if (warp == 0 && elect_one()) {
+  if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_w);
     tma_prefetch_desc(&map_x);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_holder);
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_launch_dependents();
 
   if (warp == 0) {
-    // ---------------- TMA producer
-    if (elect_one()) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
+    if (lane == 0) {
+      // ---------------- TMA producer
+      const long long n_it = it_end - it_begin;
+      const int pre = (int)(n_it < STAGES ? n_it : STAGES);
+      // weights first: nothing upstream writes them, so they stream under the previous kernel
+      for (int i = 0; i < pre; ++i) {
+        const long long it = it_begin + i;
+        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
+        mbar_arrive_expect_tx(&full[i], S::kStageBytes);
+        tma_load_2d(&map_w, &full[i], sA + i * S::kABytes, kb * kBK, (tile % m_tiles) * kBM,
+                    kEvictFirst);
+      }
+      pdl_wait();  // activations are produced by the previous kernel
+      for (int i = 0; i < pre; ++i) {
+        const long long it = it_begin + i;
+        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
+        tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
+                    kEvictLast);
+      }
+      for (long long i = pre; i < n_it; ++i) {
+        const int s = (int)(i % STAGES);
         const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
+        const long long it = it_begin + i;
+        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
         mbar_arrive_expect_tx(&full[s], S::kStageBytes);
-        const int kc = (kb_begin + i) * kBK;
-        tma_load_2d(&map_w, &full[s], sA + s * S::kABytes, kc, m0, kEvictFirst);
-        tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kc, n0, kEvictLast);
+        tma_load_2d(&map_w, &full[s], sA + s * S::kABytes, kb * kBK, (tile % m_tiles) * kBM,
+                    kEvictFirst);
+        tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
+                    kEvictLast);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc_bf16(kBM, BN);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-      mbar_wait(&full[s], ph);
+    long long i = 0;  // ring position
+    int seg = 0;
+    for (long long it = it_begin; it < it_end; ++seg) {
+      const int kb0 = (int)(it % nkb);
+      const long long left = it_end - it;
+      const int kb1 = (int)((nkb - kb0) < left ? nkb : kb0 + left);
+      const int a = seg & 1;
+      const uint32_t u = (uint32_t)(seg >> 1);
+      mbar_wait(&tempty[a], (u & 1u) ^ 1u);
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t a_addr = smem_u32(sA + s * S::kABytes);
-        const uint32_t b_addr = smem_u32(sB + s * S::kBBytes);
+      const uint32_t tacc = tmem_base + (uint32_t)(a * BN);
+      for (int kb = kb0; kb < kb1; ++kb, ++i) {
+        const int s = (int)(i % STAGES);
+        mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + s * S::kABytes);
+          const uint32_t b_addr = smem_u32(sB + s * S::kBBytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // advance 16 bf16 (32 B) along K inside the 128B swizzle atom
-          const uint64_t da = make_sdesc_k128(a_addr + k * 32);
-          const uint64_t db = make_sdesc_k128(b_addr + k * 32);
-          umma_bf16(tmem_base, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < kBK / 16; ++k) {
+            umma_bf16(tacc, make_sdesc_k128(a_addr + k * 32), make_sdesc_k128(b_addr + k * 32),
+                      idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+          if (kb == kb1 - 1) umma_commit(&tfull[a]);
         }
-        umma_commit(&empty[s]);
-        if (i == nkb - 1) umma_commit(accum_full);
+        __syncwarp();
       }
-      __syncwarp();
-    }
-  }
-
-  // ---------------- epilogue: all 4 warps, warp w owns TMEM lanes [32w, 32w+32)
-  mbar_wait(accum_full, 0);
-  tc_fence_after();
-  const int f = m0 + warp * 32 + (threadIdx.x & 31);
-  const uint32_t t_lane = tmem_base + ((uint32_t)(warp * 32) << 16);
-  const int n_tiles = gridDim.y;
-
-  if (ksplit == 1) {
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      if (n0 + c0 >= E.ntok) break;
-      float acc[16];
-      tmem_ld16(t_lane + c0, acc);
-      epilogue_chunk<BN>(E, N, f, n0 + c0, acc);
+      it += kb1 - kb0;
     }
   } else {
-    // publish this split's partial, last arriver reduces and runs the epilogue
-    float* my_ws = E.ws + ((size_t)(split * n_tiles + n_tile) * BN) * N;
+    // ---------------- epilogue warps 2..5
+    pdl_wait();
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int seg = 0;
+    for (long long it = it_begin; it < it_end; ++seg) {
+      const int tile = (int)(it / nkb);
+      const int kb0 = (int)(it % nkb);
+      const long long left = it_end - it;
+      const int kb1 = (int)((nkb - kb0) < left ? nkb : kb0 + left);
+      it += kb1 - kb0;
+      const int m_tile = tile % m_tiles, n_tile = tile / m_tiles;
+      const int m0 = m_tile * kBM, n0 = n_tile * BN;
+      const int f = m0 + q * 32 + lane;
+      const int a = seg & 1;
+      const uint32_t u = (uint32_t)(seg >> 1);
+      mbar_wait(&tfull[a], u & 1u);
+      tc_fence_after();
+      const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
+      if (kb0 == 0 && kb1 == nkb) {
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      if (n0 + c0 >= E.ntok) break;
-      float acc[16];
-      tmem_ld16(t_lane + c0, acc);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) __stcg(my_ws + (size_t)(c0 + i) * N + f, acc[i]);
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int* ctr = E.counters + m_tile * n_tiles + n_tile;
-      const int prev = atomicAdd(ctr, 1);
-      const int last = prev == ksplit - 1;
-      if (last) *ctr = 0;  // self-reset for the next launch / graph replay
-      *flag = last;
-    }
-    __syncthreads();
-    if (*flag) {
-      __threadfence();
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        if (n0 + c0 >= E.ntok) break;
-        float acc[16];
-        tmem_ld16(t_lane + c0, acc);
-        for (int s2 = 0; s2 < ksplit; ++s2) {
-          if (s2 == split) continue;
-          const float* ws = E.ws + ((size_t)(s2 * n_tiles + n_tile) * BN) * N;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) acc[i] += __ldcg(ws + (size_t)(c0 + i) * N + f);
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          if (n0 + c0 >= E.ntok) break;
+          float acc[16];
+          tmem_ld16(t_lane + c0, acc);
+          epilogue_chunk(E, f, n0 + c0, acc);
         }
-        epilogue_chunk<BN>(E, N, f, n0 + c0, acc);
+      } else {
+        // partial tile: publish, last contributor reduces and runs the epilogue
+        const long long tile_it0 = (long long)tile * nkb;
+        const int c_first = R.cta_of(tile_it0);
+        const int c_last = R.cta_of(tile_it0 + nkb - 1);
+        const int n_contrib = c_last - c_first + 1;
+        const int me = (int)blockIdx.x - c_first;
+        float* slot = E.ws + ((size_t)(tile * max_contrib + me) * BN) * kBM;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          if (n0 + c0 >= E.ntok) break;
+          float acc[16];
+          tmem_ld16(t_lane + c0, acc);
+#pragma unroll
+          for (int i2 = 0; i2 < 16; ++i2) __stcg(slot + (size_t)(c0 + i2) * kBM + q * 32 + lane, acc[i2]);
+        }
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) {
+          int* ctr = E.counters + tile;
+          const int prev = atomicAdd(ctr, 1);
+          const int last = prev == n_contrib - 1;
+          if (last) *ctr = 0;  // self-reset for the next launch / graph replay
+          *flag = last;
+        }
+        named_bar_sync(1, 128);
+        if (*flag) {
+          __threadfence();
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            if (n0 + c0 >= E.ntok) break;
+            float acc[16];
+            tmem_ld16(t_lane + c0, acc);
+            for (int o = 0; o < n_contrib; ++o) {
+              if (o == me) continue;
+              const float* ws = E.ws + ((size_t)(tile * max_contrib + o) * BN) * kBM;
+#pragma unroll
+              for (int i2 = 0; i2 < 16; ++i2)
+                acc[i2] += __ldcg(ws + (size_t)(c0 + i2) * kBM + q * 32 + lane);
+            }
+            epilogue_chunk(E, f, n0 + c0, acc);
+          }
+        }
+        named_bar_sync(1, 128);  // flag is reused by the next partial tile
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_free<kTmemCols>(tmem_base);
+  if (warp == 1) tmem_free<kTmemCols>(tmem_base);
 }
 
 template <int BN>
 static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   constexpr int STAGES = gemm_stages<BN>();
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  auto kern = gemm_tc_kernel<BN, STAGES>;
+  auto kern = gemm_sk_kernel<BN, STAGES>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(L.N / kBM, (L.epi.ntok + BN - 1) / BN, L.ksplit);
-  kern<<<grid, 128, smem, stream>>>(*L.map_w, *L.map_x, L.N, L.K, L.ksplit, L.epi);
-  return cudaGetLastError();
+  const int m_tiles = L.N / kBM;
+  const int n_tiles = (L.epi.ntok + BN - 1) / BN;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.grid, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = L.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, *L.map_w, *L.map_x, L.K, m_tiles, n_tiles,
+                            L.max_contrib, L.epi);
 }
 
 cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream) {
-  if (L.N % kBM != 0 || L.K % kBK != 0 || L.ksplit < 1 || L.ksplit > L.K / kBK)
-    return cudaErrorInvalidValue;
+  if (L.N % kBM != 0 || L.K % kBK != 0 || L.grid < 1) return cudaErrorInvalidValue;
   switch (L.bn) {
     case 16: return launch_bn<16>(L, stream);
     case 32: return launch_bn<32>(L, stream);
@@ -240,18 +331,31 @@ int gemm_pick_bn(int ntok) {
   return 256;
 }
 
-int gemm_pick_ksplit(int N, int K, int ntok, int bn, int num_sms) {
-  const int tiles = (N / kBM) * ((ntok + bn - 1) / bn);
+GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems, int n_counters,
+                   int grid_cap) {
+  GemmPlan p{};
+  const int m_tiles = N / kBM;
+  const int n_tiles = (ntok + bn - 1) / bn;
+  const long long tiles = (long long)m_tiles * n_tiles;
   const int nkb = K / kBK;
-  if (tiles >= num_sms) return 1;
-  // smallest split that fills the SMs, keeping >= 4 K-blocks per split
-  int best = 1;
-  for (int s = 1; s <= 16; ++s) {
-    if (nkb / s < 4) break;
-    best = s;
-    if (tiles * s >= num_sms) break;
+  const long long total = tiles * nkb;
+  // grid: one CTA per SM, at least 4 k-blocks per CTA
+  long long g = num_sms;
+  if (grid_cap > 0 && g > grid_cap) g = grid_cap;
+  if (g > total / 4) g = total / 4 > 0 ? total / 4 : 1;
+  for (;;) {
+    const long long per_cta = total / g;
+    const int max_contrib = per_cta >= nkb ? 2 : (int)((nkb + per_cta - 1) / per_cta) + 1;
+    const size_t need = (size_t)tiles * max_contrib * bn * kBM;
+    if ((need <= ws_elems && tiles <= n_counters) || g == 1) {
+      p.grid = (int)g;
+      p.max_contrib = max_contrib;
+      p.ws_needed = need;
+      break;
+    }
+    g = g / 2 > 0 ? g / 2 : 1;
   }
-  return best;
+  return p;
 }
 
 }  // namespace bx

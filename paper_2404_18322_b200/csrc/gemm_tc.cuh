@@ -36,9 +36,9 @@ struct EpiParams {
   int d_model;
   int head_dim;
   const float2* rope;      // [max_pos][head_dim/2] (cos, sin)
-  // split-K
-  float* ws;               // [ksplit][ntiles][BN][N] fp32 partials
-  int* counters;           // [mtiles * ntiles] arrival counters (self-resetting)
+  // stream-K partial tiles
+  float* ws;               // [tiles][max_contrib][BN][128] fp32 partials
+  int* counters;           // [tiles] arrival counters (self-resetting)
 };
 
 constexpr int kBM = 128;
@@ -60,7 +60,7 @@ __host__ __device__ constexpr int gemm_stages() {
 
 template <int BN>
 __host__ __device__ constexpr uint32_t tmem_cols() {
-  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : (BN <= 256 ? 256 : 512)));
 }
 
 // Host-side launch description.
@@ -68,16 +68,25 @@ struct GemmLaunch {
   const CUtensorMap* map_w;  // weights [N][K] bf16, box {64, 128}
   const CUtensorMap* map_x;  // activations [rows][K] bf16, box {64, BN}
   int N, K;
-  int ksplit;
   int bn;                    // 16/32/64/128/256
+  int grid;                  // persistent CTAs (stream-K ranges)
+  int max_contrib;           // workspace slots per tile
+  int pdl;                   // launch with programmatic stream serialization
   EpiParams epi;
+};
+
+struct GemmPlan {
+  int grid;
+  int max_contrib;
+  size_t ws_needed;  // fp32 elements of split-tile partials
 };
 
 // Launches on `stream`; returns cudaError_t.
 cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream);
 
-// Chooses BN for a token count and a split-K factor so the grid covers the SMs.
+// BN for a token count; persistent grid and workspace need for the stream-K schedule.
 int gemm_pick_bn(int ntok);
-int gemm_pick_ksplit(int N, int K, int ntok, int bn, int num_sms);
+GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems, int n_counters,
+                   int grid_cap);
 
 }  // namespace bx

@@ -58,6 +58,7 @@ __global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ xb,
 // rstd[t] = 1 / sqrt(mean(x[t]^2) + eps), one warp per row.
 __global__ void rms_stats_kernel(const float* __restrict__ x, int rows, int d, float eps,
                                  float* __restrict__ rstd) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
