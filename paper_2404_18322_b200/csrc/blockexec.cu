@@ -498,7 +498,7 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const CUtensorMap* mw, const CUtenso
   L.bn = bn;
   const bx::GemmPlan p = bx::gemm_plan(N, K, ntok, bn, ctx->num_sms, ws->splitws_elems,
                                        ws->n_counters, ctx->gemm_grid_cap);
-  if (p.ws_needed > ws->splitws_elems)
+  if (p.ws_needed > ws->splitws_elems || p.tiles > ws->n_counters)
     return fail(ctx, BE_ERR_INVALID, "gemm N=%d K=%d ntok=%d: stream-K workspace too small", N, K, ntok);
   L.grid = p.grid;
   L.max_contrib = p.max_contrib;

@@ -235,7 +235,13 @@ __global__ void __launch_bounds__(192, 1)
         const int c_last = R.cta_of(tile_it0 + nkb - 1);
         const int n_contrib = c_last - c_first + 1;
         const int me = (int)blockIdx.x - c_first;
-        float* slot = E.ws + ((size_t)(tile * max_contrib + me) * BN) * kBM;
+        // a CTA owns two partial slots: its first segment (range starts inside the tile) and
+        // its last one; a tile's contributors are the CTAs c_first..c_last
+        auto slot_of = [&](int c) {
+          const int which = R.begin(c) >= tile_it0 ? 0 : 1;
+          return E.ws + ((size_t)(c * 2 + which) * BN) * kBM;
+        };
+        float* slot = slot_of(blockIdx.x);
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           if (n0 + c0 >= E.ntok) break;
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(192, 1)
             tmem_ld16(t_lane + c0, acc);
             for (int o = 0; o < n_contrib; ++o) {
               if (o == me) continue;
-              const float* ws = E.ws + ((size_t)(tile * max_contrib + o) * BN) * kBM;
+              const float* ws = slot_of(c_first + o);
 #pragma unroll
               for (int i2 = 0; i2 < 16; ++i2)
                 acc[i2] += __ldcg(ws + (size_t)(c0 + i2) * kBM + q * 32 + lane);
@@ -343,18 +349,13 @@ GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems,
   long long g = num_sms;
   if (grid_cap > 0 && g > grid_cap) g = grid_cap;
   if (g > total / 4) g = total / 4 > 0 ? total / 4 : 1;
-  for (;;) {
-    const long long per_cta = total / g;
-    const int max_contrib = per_cta >= nkb ? 2 : (int)((nkb + per_cta - 1) / per_cta) + 1;
-    const size_t need = (size_t)tiles * max_contrib * bn * kBM;
-    if ((need <= ws_elems && tiles <= n_counters) || g == 1) {
-      p.grid = (int)g;
-      p.max_contrib = max_contrib;
-      p.ws_needed = need;
-      break;
-    }
-    g = g / 2 > 0 ? g / 2 : 1;
-  }
+  // partial-tile slots: two per CTA (its first and its last segment)
+  while (g > 1 && (size_t)g * 2 * bn * kBM > ws_elems) g /= 2;
+  (void)n_counters;
+  p.grid = (int)g;
+  p.max_contrib = 2;
+  p.ws_needed = (size_t)g * 2 * bn * kBM;
+  p.tiles = tiles;
   return p;
 }
 

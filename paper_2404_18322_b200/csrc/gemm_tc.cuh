@@ -37,7 +37,7 @@ struct EpiParams {
   int head_dim;
   const float2* rope;      // [max_pos][head_dim/2] (cos, sin)
   // stream-K partial tiles
-  float* ws;               // [tiles][max_contrib][BN][128] fp32 partials
+  float* ws;               // [grid][2][BN][128] fp32 partials (first/last segment per CTA)
   int* counters;           // [tiles] arrival counters (self-resetting)
 };
 
@@ -79,6 +79,7 @@ struct GemmPlan {
   int grid;
   int max_contrib;
   size_t ws_needed;  // fp32 elements of split-tile partials
+  long long tiles;   // arrival counters needed
 };
 
 // Launches on `stream`; returns cudaError_t.
