@@ -262,6 +262,8 @@ def run_ours(args, world, rank, local):
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    if args.profile:
+        torch.cuda.profiler.start()
     e0.record(stream)
     nb = 0
     for _ in range(args.steps):
@@ -269,6 +271,8 @@ def run_ours(args, world, rank, local):
     e1.record(stream)
     ctx.sync()
     torch.cuda.synchronize()
+    if args.profile:
+        torch.cuda.profiler.stop()
     clk = clocks.stop()
     barrier()
     ms = e0.elapsed_time(e1)
@@ -405,6 +409,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
