@@ -201,15 +201,17 @@ def kernel_rooflines(ctx, wl, peaks):
                        ("down", s.d_model, s.d_ff), ("o", s.d_model, s.d_model)]:
         copies = max(2, int(np.ceil(3 * 126e6 / (N * K * 2))))
         w = torch.empty(copies, N, K, dtype=torch.bfloat16, device="cuda").uniform_(-0.03, 0.03)
+        for i in range(copies):
+            w[i] = dev.pack_weight(ctx, w[i])
         x = torch.randn(64, K, device="cuda").to(torch.bfloat16)
         out = torch.empty(64, N, device="cuda", dtype=torch.bfloat16)
         for i in range(copies):
-            dev.gemm_bf16(ctx, w[i], x, out)
+            dev.gemm_bf16(ctx, w[i], x, out, packed=True)
         ctx.sync()
         reps = 4 * copies
         e0.record(stream)
         for i in range(reps):
-            dev.gemm_bf16(ctx, w[i % copies], x, out)
+            dev.gemm_bf16(ctx, w[i % copies], x, out, packed=True)
         e1.record(stream)
         ctx.sync()
         t = e0.elapsed_time(e1) / reps / 1e3

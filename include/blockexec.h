@@ -132,9 +132,14 @@ int be_synth_rows(be_ctx* ctx, void* d_dst, int64_t n_elems, uint64_t seed, cons
 int be_block_read_weight(be_block* blk, int layer, const char* tensor, float* host_out);
 
 /* Low-level kernels exported for tests and the roofline bench ------------------------------ */
-/* out[t][f] = bf16(sum_k W[f][k] X[t][k]) with W [N][K], X [ntok][K] bf16 row-major. */
-int be_gemm_bf16(be_ctx* ctx, const void* d_w, const void* d_x, void* d_out, int N, int K,
-                 int ntok, int ksplit, void* stream);
+/* Row-major [N][K] bf16 -> the packed GEMM weight layout (128x64 tiles, tile-major, each tile in
+ * its 128B-swizzled shared-memory image; see csrc/ptx.cuh packed_index). Block weights are
+ * generated directly in this layout. */
+int be_pack_weight(be_ctx* ctx, const void* d_src, void* d_dst, int N, int K, void* stream);
+/* out[t][f] = bf16(sum_k W[f][k] X[t][k]) with W packed (be_pack_weight), X [ntok][K] bf16
+ * row-major. grid_cap bounds the persistent CTAs (0 = one per SM). */
+int be_gemm_bf16(be_ctx* ctx, const void* d_w_packed, const void* d_x, void* d_out, int N, int K,
+                 int ntok, int grid_cap, void* stream);
 /* Paged attention over a pool (decode rows / causal prefill rows). */
 int be_attention(be_ctx* ctx, const void* d_q, const void* d_pool, int n_layers, int n_heads,
                  int head_dim, int layer, const int32_t* d_page_table, int pt_stride,

@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
         "be_cosine": (I, [P, P, P, I, I, F, P, P, P]),
         "be_synth_rows": (I, [P, P, I64, U64, C.c_char_p, F, P]),
         "be_gemm_bf16": (I, [P, P, P, P, I, I, I, I, P]),
+        "be_pack_weight": (I, [P, P, P, I, I, P]),
+        "be_exec_batch_launches": (I, [P, P, I, I]),
         "be_attention": (I, [P, P, P, I, I, I, I, P, I, P, P, I, I, P, P]),
     }
     for name, (res, args) in sig.items():

@@ -25,6 +25,7 @@ cudaError_t launch_rms_stats(const float*, int, int, float, float*, cudaStream_t
 cudaError_t launch_cosine(const __nv_bfloat16*, const __nv_bfloat16*, int, int, float, float*, int*, cudaStream_t);
 cudaError_t launch_synth_weight(__nv_bfloat16*, int, int, uint64_t, uint64_t, float, int, int, const float*, cudaStream_t);
 cudaError_t launch_synth_rows(__nv_bfloat16*, long long, uint64_t, float, cudaStream_t);
+cudaError_t launch_pack_weight(const __nv_bfloat16*, __nv_bfloat16*, int, int, cudaStream_t);
 cudaError_t launch_rope_table(float2*, int, int, double, cudaStream_t);
 // attention.cu
 struct AttnParams {
@@ -74,8 +75,7 @@ struct be_block {
   size_t slab_elems = 0;
   float2* rope = nullptr;
   struct Layer {
-    bf16 *wqkv, *wo, *wgu, *wd;
-    CUtensorMap m_qkv, m_o, m_gu, m_d;
+    bf16 *wqkv, *wo, *wgu, *wd;  // packed tile layout (ptx.cuh packed_index)
   };
   std::vector<Layer> layers;
 };
@@ -297,14 +297,6 @@ extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out
     bx::launch_synth_weight(L.wo, (int)D, (int)D, key("wo"), 0, s, 0, d->head_dim, nullptr, st);
     bx::launch_synth_weight(L.wgu, (int)(2 * F), (int)D, key("wg"), key("wu"), s, 2, d->head_dim, nullptr, st);
     bx::launch_synth_weight(L.wd, (int)D, (int)F, key("wd"), 0, s, 0, d->head_dim, nullptr, st);
-    int rc;
-    if ((rc = make_map(ctx, &L.m_qkv, L.wqkv, 3 * D, D, 128)) != BE_OK ||
-        (rc = make_map(ctx, &L.m_o, L.wo, D, D, 128)) != BE_OK ||
-        (rc = make_map(ctx, &L.m_gu, L.wgu, 2 * F, D, 128)) != BE_OK ||
-        (rc = make_map(ctx, &L.m_d, L.wd, D, F, 128)) != BE_OK) {
-      be_block_free(b);
-      return rc;
-    }
   }
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
@@ -362,7 +354,7 @@ extern "C" int be_block_read_weight(be_block* b, int layer, const char* tensor, 
       lr = pr >> 1;
     }
     for (int c = 0; c < cols; ++c)
-      host_out[(size_t)lr * cols + c] = __bfloat162float(tmp[(size_t)pr * cols + c]);
+      host_out[(size_t)lr * cols + c] = __bfloat162float(tmp[bx::packed_index(pr, c, cols)]);
   }
   return BE_OK;
 }
@@ -488,10 +480,10 @@ extern "C" int be_workspace_free(be_workspace* w) {
 // ------------------------------------------------------------------------------ execution
 namespace {
 
-int run_gemm(be_ctx* ctx, be_workspace* ws, const CUtensorMap* mw, const CUtensorMap* mx, int N,
+int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensorMap* mx, int N,
              int K, int ntok, int bn, EpiParams epi, cudaStream_t st) {
   bx::GemmLaunch L{};
-  L.map_w = mw;
+  L.w_packed = w_packed;
   L.map_x = mx;
   L.N = N;
   L.K = K;
@@ -557,7 +549,7 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eq.d_model = d;
     eq.head_dim = hd;
     eq.rope = blk->rope;
-    if ((rc = run_gemm(ctx, ws, &L.m_qkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st)) != BE_OK) return rc;
+    if ((rc = run_gemm(ctx, ws, L.wqkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st)) != BE_OK) return rc;
 
     bx::AttnParams ap{};
     ap.q = ws->q;
@@ -585,7 +577,7 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eo.xres = ws->X;
     eo.xres_b = ws->Xb;
     eo.ldr = d;
-    if ((rc = run_gemm(ctx, ws, &L.m_o, &ws->m_attn[bn], d, d, ntok, bn, eo, st)) != BE_OK) return rc;
+    if ((rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st)) != BE_OK) return rc;
 
     // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
     e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
@@ -596,14 +588,14 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eg.rstd = ws->rstd;
     eg.out = ws->h;
     eg.ldo = F;
-    if ((rc = run_gemm(ctx, ws, &L.m_gu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st)) != BE_OK) return rc;
+    if ((rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st)) != BE_OK) return rc;
     EpiParams ed{};
     ed.mode = bx::kResid;
     ed.ntok = ntok;
     ed.xres = ws->X;
     ed.xres_b = ws->Xb;
     ed.ldr = d;
-    if ((rc = run_gemm(ctx, ws, &L.m_d, &ws->m_h[bn], d, F, ntok, bn, ed, st)) != BE_OK) return rc;
+    if ((rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st)) != BE_OK) return rc;
   }
   // K2: scatter the block outputs to their next-hop rows
   e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st);
@@ -702,14 +694,22 @@ extern "C" int be_synth_rows(be_ctx* ctx, void* dst, int64_t n, uint64_t seed, c
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "synth: %s", cudaGetErrorString(e));
 }
 
+extern "C" int be_pack_weight(be_ctx* ctx, const void* src, void* dst, int N, int K,
+                              void* stream) {
+  if (ctx == nullptr || src == nullptr || dst == nullptr || N % 128 != 0 || K % 64 != 0)
+    return BE_ERR_INVALID;
+  cudaError_t e = bx::launch_pack_weight(static_cast<const bf16*>(src), static_cast<bf16*>(dst), N,
+                                         K, pick_stream(ctx, stream));
+  return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "pack: %s", cudaGetErrorString(e));
+}
+
 extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out, int N, int K,
                             int ntok, int grid_cap, void* stream) {
   if (ctx == nullptr || N % 128 != 0 || K % 64 != 0 || ntok <= 0 || grid_cap < 0)
     return BE_ERR_INVALID;
   const int bn = bx::gemm_pick_bn(ntok);
-  CUtensorMap mw, mx;
+  CUtensorMap mx;
   int rc;
-  if ((rc = make_map(ctx, &mw, w, N, K, 128)) != BE_OK) return rc;
   if ((rc = make_map(ctx, &mx, x, ntok, K, bn)) != BE_OK) return rc;
   const bx::GemmPlan p =
       bx::gemm_plan(N, K, ntok, bn, ctx->num_sms, (size_t)1 << 40, 1 << 16, grid_cap);
@@ -726,7 +726,7 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
     BE_CUDA(ctx, cudaMemset(ctx->gemm_counters, 0, (1 << 16) * sizeof(int)));
   }
   bx::GemmLaunch L{};
-  L.map_w = &mw;
+  L.w_packed = static_cast<const bf16*>(w);
   L.map_x = &mx;
   L.N = N;
   L.K = K;

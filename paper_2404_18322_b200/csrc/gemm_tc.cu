@@ -91,7 +91,7 @@ struct SkRange {
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
-    gemm_sk_kernel(const __grid_constant__ CUtensorMap map_w,
+    gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
                    int max_contrib, EpiParams E) {
   using S = GemmSmem<BN>;
@@ -116,7 +116,6 @@ __global__ void __launch_bounds__(192, 1)
   const long long it_end = R.begin(blockIdx.x + 1);
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&map_w);
     tma_prefetch_desc(&map_x);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -137,16 +136,17 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- producer: packed weight tiles by bulk copy, activations by TMA
       const long long n_it = it_end - it_begin;
       const int pre = (int)(n_it < STAGES ? n_it : STAGES);
+      auto wtile = [&](long long it) {
+        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
+        return wpk + ((size_t)(tile % m_tiles) * nkb + kb) * (kBM * kBK);
+      };
       // weights first: nothing upstream writes them, so they stream under the previous kernel
       for (int i = 0; i < pre; ++i) {
-        const long long it = it_begin + i;
-        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
         mbar_arrive_expect_tx(&full[i], S::kStageBytes);
-        tma_load_2d(&map_w, &full[i], sA + i * S::kABytes, kb * kBK, (tile % m_tiles) * kBM,
-                    kEvictFirst);
+        bulk_load(sA + i * S::kABytes, wtile(it_begin + i), S::kABytes, &full[i], kEvictFirst);
       }
       pdl_wait();  // activations are produced by the previous kernel
       for (int i = 0; i < pre; ++i) {
@@ -162,8 +162,7 @@ __global__ void __launch_bounds__(192, 1)
         const long long it = it_begin + i;
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
         mbar_arrive_expect_tx(&full[s], S::kStageBytes);
-        tma_load_2d(&map_w, &full[s], sA + s * S::kABytes, kb * kBK, (tile % m_tiles) * kBM,
-                    kEvictFirst);
+        bulk_load(sA + s * S::kABytes, wtile(it), S::kABytes, &full[s], kEvictFirst);
         tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
                     kEvictLast);
       }
@@ -313,7 +312,7 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = L.pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, *L.map_w, *L.map_x, L.K, m_tiles, n_tiles,
+  return cudaLaunchKernelEx(&cfg, kern, L.w_packed, *L.map_x, L.K, m_tiles, n_tiles,
                             L.max_contrib, L.epi);
 }
 

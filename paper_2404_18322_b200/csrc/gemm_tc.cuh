@@ -65,7 +65,7 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
 
 // Host-side launch description.
 struct GemmLaunch {
-  const CUtensorMap* map_w;  // weights [N][K] bf16, box {64, 128}
+  const __nv_bfloat16* w_packed;  // weights [N][K] in the packed tile layout (ptx.cuh)
   const CUtensorMap* map_x;  // activations [rows][K] bf16, box {64, BN}
   int N, K;
   int bn;                    // 16/32/64/128/256

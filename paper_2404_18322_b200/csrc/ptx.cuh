@@ -69,6 +69,30 @@ __device__ __forceinline__ void tma_load_2d(const void* desc, uint64_t* bar, voi
       "l"(cache_hint)
       : "memory");
 }
+// 1D bulk copy global -> shared of `bytes` (multiple of 16), completion counted on `bar`.
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes,
+                                          uint64_t* bar, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(gmem)), "r"(bytes), "r"(smem_u32(bar)), "l"(cache_hint)
+      : "memory");
+}
+
+// Packed weight layout (HBM): a [N][K] bf16 weight is stored as 128x64 tiles, tile-major in
+// (m_tile, k_block) order, each 16 KB tile already in the 128B-swizzled image TMA would have
+// produced in shared memory (row r at r*128 B, 16-byte chunk c at ((c ^ (r % 8)) * 16)). One
+// contiguous 16 KB bulk copy then lands a UMMA-ready tile, and a CTA's stream-K range of
+// (tile, k-block) iterations is one contiguous run of HBM.
+__host__ __device__ __forceinline__ size_t packed_index(int row, int col, int K) {
+  const int nkb = K >> 6;
+  const int m_tile = row >> 7, r = row & 127;
+  const int kb = col >> 6, c = col & 63;
+  const int chunk = c >> 3, within = c & 7;
+  const size_t tile = (size_t)m_tile * nkb + kb;
+  return tile * 8192 + (size_t)r * 64 + (size_t)((chunk ^ (r & 7)) * 8 + within);
+}
+
 // Fixed L2 cache-policy encodings (createpolicy.fractional.L2::evict_first / evict_last, 1.0).
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;

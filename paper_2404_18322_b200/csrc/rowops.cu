@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace bx {
 
 // ---------------------------------------------------------------- K1 gather
@@ -150,7 +152,18 @@ __global__ void synth_weight_kernel(__nv_bfloat16* __restrict__ dst, int rows, i
     float v = synth_value(key, (uint64_t)lr * cols + c, scale);
     v = __bfloat162float(__float2bfloat16_rn(v));  // logical bf16 weight
     if (gamma != nullptr) v *= gamma[c];
-    dst[idx] = __float2bfloat16_rn(v);
+    dst[packed_index(pr, c, cols)] = __float2bfloat16_rn(v);  // GEMM-ready tile layout
+  }
+}
+
+// row-major [rows][cols] -> packed tile layout (ptx.cuh packed_index)
+__global__ void pack_weight_kernel(const __nv_bfloat16* __restrict__ src,
+                                   __nv_bfloat16* __restrict__ dst, int rows, int cols) {
+  const long long total = (long long)rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / cols), c = (int)(idx - (long long)r * cols);
+    dst[packed_index(r, c, cols)] = src[idx];
   }
 }
 
@@ -212,6 +225,11 @@ cudaError_t launch_synth_weight(__nv_bfloat16* dst, int rows, int cols, uint64_t
                                 const float* gamma, cudaStream_t st) {
   synth_weight_kernel<<<grid_for((long long)rows * cols, 256, 148 * 32), 256, 0, st>>>(
       dst, rows, cols, key0, key1, scale, perm, head_dim, gamma);
+  return cudaGetLastError();
+}
+cudaError_t launch_pack_weight(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int cols,
+                               cudaStream_t st) {
+  pack_weight_kernel<<<grid_for((long long)rows * cols, 256, 148 * 32), 256, 0, st>>>(src, dst, rows, cols);
   return cudaGetLastError();
 }
 cudaError_t launch_synth_rows(__nv_bfloat16* dst, long long n, uint64_t key, float scale,

@@ -175,9 +175,19 @@ def exec_batch(ctx: Context, block: Block, pool: KvPool, ws: Workspace, phase: i
                               stream if stream is not None else C.c_void_p(0)), ctx.h)
 
 
-def gemm_bf16(ctx: Context, w, x, out, ksplit: int = 0) -> None:
+def pack_weight(ctx: Context, w):
+    """Row-major [N][K] bf16 -> packed GEMM tile layout (csrc/ptx.cuh packed_index)."""
+    out = w.new_empty(w.shape)
     N, K = w.shape
-    check(lib().be_gemm_bf16(ctx.h, _ptr(w), _ptr(x), _ptr(out), N, K, x.shape[0], ksplit,
+    check(lib().be_pack_weight(ctx.h, _ptr(w), _ptr(out), N, K, C.c_void_p(0)), ctx.h)
+    return out
+
+
+def gemm_bf16(ctx: Context, w, x, out, grid_cap: int = 0, packed: bool = False) -> None:
+    """out[t] = x[t] @ w^T (bf16 in/out, fp32 accumulate) on the tcgen05 stream-K kernel."""
+    N, K = w.shape
+    wp = w if packed else pack_weight(ctx, w)
+    check(lib().be_gemm_bf16(ctx.h, _ptr(wp), _ptr(x), _ptr(out), N, K, x.shape[0], grid_cap,
                              C.c_void_p(0)), ctx.h)
 
 
