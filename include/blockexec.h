@@ -140,6 +140,10 @@ int be_pack_weight(be_ctx* ctx, const void* d_src, void* d_dst, int N, int K, vo
  * row-major. grid_cap bounds the persistent CTAs (0 = one per SM). */
 int be_gemm_bf16(be_ctx* ctx, const void* d_w_packed, const void* d_x, void* d_out, int N, int K,
                  int ntok, int grid_cap, void* stream);
+/* Roofline timing: device microseconds per GEMM launch from one CUDA-graph replay of `reps`
+ * launches cycling over n_w packed weight copies. */
+int be_bench_gemm(be_ctx* ctx, const void* const* d_w_packed, int n_w, const void* d_x,
+                  void* d_out, int N, int K, int ntok, int reps, float* us_per_launch);
 /* Paged attention over a pool (decode rows / causal prefill rows). */
 int be_attention(be_ctx* ctx, const void* d_q, const void* d_pool, int n_layers, int n_heads,
                  int head_dim, int layer, const int32_t* d_page_table, int pt_stride,

@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
         "be_synth_rows": (I, [P, P, I64, U64, C.c_char_p, F, P]),
         "be_gemm_bf16": (I, [P, P, P, P, I, I, I, I, P]),
         "be_pack_weight": (I, [P, P, P, I, I, P]),
+        "be_bench_gemm": (I, [P, P, I, P, P, I, I, I, I, C.POINTER(C.c_float)]),
         "be_exec_batch_launches": (I, [P, P, I, I]),
         "be_attention": (I, [P, P, P, I, I, I, I, P, I, P, P, I, I, P, P]),
     }

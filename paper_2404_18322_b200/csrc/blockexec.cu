@@ -734,7 +734,7 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.grid = p.grid;
   L.max_contrib = p.max_contrib;
   L.pdl = ctx->use_pdl;
-  L.epi.mode = bx::kStore;
+  L.epi.mode = getenv("BE_GEMM_NOEPI") ? -1 : bx::kStore;
   L.epi.ntok = ntok;
   L.epi.out = static_cast<bf16*>(out);
   L.epi.ldo = N;
@@ -742,6 +742,45 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.epi.counters = ctx->gemm_counters;
   cudaError_t e = bx::launch_gemm(L, pick_stream(ctx, stream));
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "gemm: %s", cudaGetErrorString(e));
+}
+
+// Device time per launch of the GEMM, measured as one CUDA-graph replay of `reps` launches that
+// cycle through `n_w` packed weight copies (so the weights come from HBM, not L2).
+extern "C" int be_bench_gemm(be_ctx* ctx, const void* const* w_packed, int n_w, const void* x,
+                             void* out, int N, int K, int ntok, int reps, float* us_per_launch) {
+  if (ctx == nullptr || w_packed == nullptr || n_w <= 0 || reps <= 0 || us_per_launch == nullptr)
+    return BE_ERR_INVALID;
+  cudaStream_t st = ctx->stream;
+  int rc = be_gemm_bf16(ctx, w_packed[0], x, out, N, K, ntok, 0, st);  // configure + allocate
+  if (rc != BE_OK) return rc;
+  BE_CUDA(ctx, cudaStreamSynchronize(st));
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  BE_CUDA(ctx, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  for (int r = 0; r < reps && rc == BE_OK; ++r)
+    rc = be_gemm_bf16(ctx, w_packed[r % n_w], x, out, N, K, ntok, 0, st);
+  cudaStreamEndCapture(st, &g);
+  if (rc != BE_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  BE_CUDA(ctx, cudaGraphInstantiate(&ge, g, 0));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaGraphLaunch(ge, st);  // warm
+  cudaEventRecord(e0, st);
+  cudaGraphLaunch(ge, st);
+  cudaEventRecord(e1, st);
+  BE_CUDA(ctx, cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *us_per_launch = ms * 1e3f / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  return BE_OK;
 }
 
 extern "C" int be_attention(be_ctx* ctx, const void* q, const void* pool, int n_layers, int H,

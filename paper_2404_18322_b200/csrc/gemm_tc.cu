@@ -29,6 +29,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0,
                                                const float (&acc)[16]) {
   const int lane = threadIdx.x & 31;
+  if (E.mode < 0) return;  // diagnostics: accumulate only
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int t = t0 + i;
