@@ -241,14 +241,17 @@ __global__ void __launch_bounds__(192, 1)
           const int which = R.begin(c) >= tile_it0 ? 0 : 1;
           return E.ws + ((size_t)(c * 2 + which) * BN) * kBM;
         };
-        float* slot = slot_of(blockIdx.x);
+        // partial layout [feature][BN]: each thread moves its 16-column chunks as float4s
+        const size_t frow = (size_t)(q * 32 + lane) * BN;
+        float4* slot = reinterpret_cast<float4*>(slot_of(blockIdx.x) + frow);
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           if (n0 + c0 >= E.ntok) break;
           float acc[16];
           tmem_ld16(t_lane + c0, acc);
 #pragma unroll
-          for (int i2 = 0; i2 < 16; ++i2) __stcg(slot + (size_t)(c0 + i2) * kBM + q * 32 + lane, acc[i2]);
+          for (int j = 0; j < 4; ++j)
+            __stcg(slot + (c0 >> 2) + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
         }
         __threadfence();
         named_bar_sync(1, 128);
@@ -265,14 +268,44 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             if (n0 + c0 >= E.ntok) break;
-            float acc[16];
-            tmem_ld16(t_lane + c0, acc);
-            for (int o = 0; o < n_contrib; ++o) {
-              if (o == me) continue;
-              const float* ws = slot_of(c_first + o);
+            float own[16], acc[16];
+            tmem_ld16(t_lane + c0, own);
 #pragma unroll
-              for (int i2 = 0; i2 < 16; ++i2)
-                acc[i2] += __ldcg(ws + (size_t)(c0 + i2) * kBM + q * 32 + lane);
+            for (int i2 = 0; i2 < 16; ++i2) acc[i2] = 0.f;
+            // contributors summed in a fixed order (deterministic whoever arrives last); loads
+            // of four contributors are in flight together
+            for (int o0 = 0; o0 < n_contrib; o0 += 4) {
+              float4 v[4][4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int o = o0 + j;
+                if (o < n_contrib && o != me) {
+                  const float4* p =
+                      reinterpret_cast<const float4*>(slot_of(c_first + o) + frow) + (c0 >> 2);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) v[j][k] = __ldcg(p + k);
+                } else {
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) v[j][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int o = o0 + j;
+                if (o >= n_contrib) break;
+                if (o == me) {
+#pragma unroll
+                  for (int i2 = 0; i2 < 16; ++i2) acc[i2] += own[i2];
+                } else {
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    acc[4 * k] += v[j][k].x;
+                    acc[4 * k + 1] += v[j][k].y;
+                    acc[4 * k + 2] += v[j][k].z;
+                    acc[4 * k + 3] += v[j][k].w;
+                  }
+                }
+              }
             }
             epilogue_chunk(E, f, n0 + c0, acc);
           }
