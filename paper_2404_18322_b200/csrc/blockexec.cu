@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <algorithm>
 #include <map>
 #include <string>
 #include <vector>
@@ -740,7 +741,35 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.epi.ldo = N;
   L.epi.ws = ctx->gemm_ws;
   L.epi.counters = ctx->gemm_counters;
+  unsigned long long* trace = nullptr;
+  const bool tracing = getenv("BE_GEMM_TRACE") != nullptr;
+  if (tracing) {
+    BE_CUDA(ctx, cudaMalloc(&trace, (size_t)p.grid * 8 * sizeof(unsigned long long)));
+    BE_CUDA(ctx, cudaMemset(trace, 0, (size_t)p.grid * 8 * sizeof(unsigned long long)));
+    L.epi.trace = trace;
+  }
   cudaError_t e = bx::launch_gemm(L, pick_stream(ctx, stream));
+  if (tracing) {
+    // diagnostics: per-phase globaltimer stamps across CTAs, microseconds from the first entry
+    std::vector<unsigned long long> h((size_t)p.grid * 8);
+    cudaStreamSynchronize(pick_stream(ctx, stream));
+    cudaMemcpy(h.data(), trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(trace);
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < p.grid; ++c) t0 = h[c * 8] && h[c * 8] < t0 ? h[c * 8] : t0;
+    const char* names[8] = {"entry", "setup", "pdl_wait", "last_load", "first_full", "last_full",
+                            "first_tfull", "exit"};
+    fprintf(stderr, "gemm trace N=%d K=%d ntok=%d grid=%d\n", N, K, ntok, p.grid);
+    for (int k = 0; k < 8; ++k) {
+      std::vector<double> v;
+      for (int c = 0; c < p.grid; ++c)
+        if (h[c * 8 + k]) v.push_back((h[c * 8 + k] - t0) / 1e3);
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, "  %-12s min %8.2f  med %8.2f  max %8.2f us (n=%zu)\n", names[k], v.front(),
+              v[v.size() / 2], v.back(), v.size());
+    }
+  }
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "gemm: %s", cudaGetErrorString(e));
 }
 

@@ -20,6 +20,13 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+__device__ __forceinline__ void stamp(const EpiParams& E, int idx) {
+  if (E.trace != nullptr) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    E.trace[blockIdx.x * 8 + idx] = t;
+  }
+}
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -116,6 +123,7 @@ __global__ void __launch_bounds__(192, 1)
   const long long it_begin = R.begin(blockIdx.x);
   const long long it_end = R.begin(blockIdx.x + 1);
 
+  if (threadIdx.x == 0) stamp(E, 0);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_x);
     for (int s = 0; s < STAGES; ++s) {
@@ -134,6 +142,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   pdl_launch_dependents();
+  if (threadIdx.x == 0) stamp(E, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -150,6 +159,7 @@ __global__ void __launch_bounds__(192, 1)
         bulk_load(sA + i * S::kABytes, wtile(it_begin + i), S::kABytes, &full[i], kEvictFirst);
       }
       pdl_wait();  // activations are produced by the previous kernel
+      stamp(E, 2);
       for (int i = 0; i < pre; ++i) {
         const long long it = it_begin + i;
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
@@ -167,6 +177,7 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
                     kEvictLast);
       }
+      stamp(E, 3);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
@@ -187,6 +198,8 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
         tc_fence_after();
         if (lane == 0) {
+          if (i == 0) stamp(E, 4);
+          if (it + (kb - kb0) == it_end - 1) stamp(E, 5);
           const uint32_t a_addr = smem_u32(sA + s * S::kABytes);
           const uint32_t b_addr = smem_u32(sB + s * S::kBBytes);
 #pragma unroll
@@ -219,6 +232,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t u = (uint32_t)(seg >> 1);
       mbar_wait(&tfull[a], u & 1u);
       tc_fence_after();
+      if (seg == 0 && warp == 2 && lane == 0) stamp(E, 6);
       const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
       if (kb0 == 0 && kb1 == nkb) {
 #pragma unroll 1
@@ -320,6 +334,7 @@ __global__ void __launch_bounds__(192, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) stamp(E, 7);
   if (warp == 1) tmem_free<kTmemCols>(tmem_base);
 }
 

@@ -39,6 +39,7 @@ struct EpiParams {
   // stream-K partial tiles
   float* ws;               // [grid][2][BN][128] fp32 partials (first/last segment per CTA)
   int* counters;           // [tiles] arrival counters (self-resetting)
+  unsigned long long* trace;  // diagnostics: [grid][8] globaltimer stamps, nullptr = off
 };
 
 constexpr int kBM = 128;
