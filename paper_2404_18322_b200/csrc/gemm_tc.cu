@@ -153,14 +153,16 @@ __global__ void __launch_bounds__(192, 1)
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
         return wpk + ((size_t)(tile % m_tiles) * nkb + kb) * (kBM * kBK);
       };
+      const bool load_b = (E.dbg & 2) == 0;
+      const uint32_t stage_bytes = load_b ? S::kStageBytes : S::kABytes;
       // weights first: nothing upstream writes them, so they stream under the previous kernel
       for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], S::kStageBytes);
+        mbar_arrive_expect_tx(&full[i], stage_bytes);
         bulk_load(sA + i * S::kABytes, wtile(it_begin + i), S::kABytes, &full[i], kEvictFirst);
       }
       pdl_wait();  // activations are produced by the previous kernel
       stamp(E, 2);
-      for (int i = 0; i < pre; ++i) {
+      for (int i = 0; i < pre && load_b; ++i) {
         const long long it = it_begin + i;
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
         tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
@@ -172,10 +174,11 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&empty[s], ph ^ 1u);
         const long long it = it_begin + i;
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
-        mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+        mbar_arrive_expect_tx(&full[s], stage_bytes);
         bulk_load(sA + s * S::kABytes, wtile(it), S::kABytes, &full[s], kEvictFirst);
-        tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
-                    kEvictLast);
+        if (load_b)
+          tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
+                      kEvictLast);
       }
       stamp(E, 3);
     }
@@ -202,13 +205,18 @@ __global__ void __launch_bounds__(192, 1)
           if (it + (kb - kb0) == it_end - 1) stamp(E, 5);
           const uint32_t a_addr = smem_u32(sA + s * S::kABytes);
           const uint32_t b_addr = smem_u32(sB + s * S::kBBytes);
+          if (E.dbg & 1) {
+            mbar_arrive(&empty[s]);
+            if (kb == kb1 - 1) mbar_arrive(&tfull[a]);
+          } else {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            umma_bf16(tacc, make_sdesc_k128(a_addr + k * 32), make_sdesc_k128(b_addr + k * 32),
-                      idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k) {
+              umma_bf16(tacc, make_sdesc_k128(a_addr + k * 32), make_sdesc_k128(b_addr + k * 32),
+                        idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[s]);
+            if (kb == kb1 - 1) umma_commit(&tfull[a]);
           }
-          umma_commit(&empty[s]);
-          if (kb == kb1 - 1) umma_commit(&tfull[a]);
         }
         __syncwarp();
       }

@@ -40,6 +40,7 @@ struct EpiParams {
   float* ws;               // [grid][2][BN][128] fp32 partials (first/last segment per CTA)
   int* counters;           // [tiles] arrival counters (self-resetting)
   unsigned long long* trace;  // diagnostics: [grid][8] globaltimer stamps, nullptr = off
+  int dbg;                    // diagnostics: bit0 skip MMA, bit1 skip activation loads
 };
 
 constexpr int kBM = 128;
