@@ -98,7 +98,7 @@ struct SkRange {
 };
 
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, gemm_ctas_per_sm<BN>())
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
                    int max_contrib, EpiParams E) {

@@ -53,11 +53,20 @@ struct GemmSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
 };
 
+// Ring depth. Decode shapes (BN <= 128) keep ~100 KB of stages so two CTAs fit on an SM: the
+// next GEMM of the chain (programmatic dependent launch) becomes resident beside the current
+// one and streams its first weight tiles under the current GEMM's tail. ~100 KB in flight per
+// SM is well above HBM bandwidth x unloaded latency (~45 KB/SM). Prefill tiles (BN = 256) are
+// tensor-bound and take the deep ring instead.
 template <int BN>
 __host__ __device__ constexpr int gemm_stages() {
-  // leave ~8 KB for barriers; cap at 8 stages (enough bytes in flight for one SM)
-  int s = (220 * 1024) / GemmSmem<BN>::kStageBytes;
+  if (BN >= 256) return (200 * 1024) / GemmSmem<BN>::kStageBytes;
+  int s = (100 * 1024) / GemmSmem<BN>::kStageBytes;
   return s > 8 ? 8 : s;
+}
+template <int BN>
+__host__ __device__ constexpr int gemm_ctas_per_sm() {
+  return BN >= 256 ? 1 : 2;
 }
 
 template <int BN>
