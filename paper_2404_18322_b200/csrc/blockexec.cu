@@ -66,6 +66,7 @@ struct be_ctx {
   int* gemm_counters = nullptr;
   int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
   int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
+  int gemm_deep = 1;      // GEMM ring depth: 1 deep (one CTA/SM), 0 shallow (BE_GEMM_RING)
 };
 
 struct be_block {
@@ -223,6 +224,7 @@ extern "C" int be_ctx_create(int device, be_ctx** out) {
   ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   if (const char* g = getenv("BE_GEMM_GRID")) ctx->gemm_grid_cap = atoi(g);
   if (const char* p = getenv("BE_PDL")) ctx->use_pdl = atoi(p) != 0;
+  if (const char* r = getenv("BE_GEMM_RING")) ctx->gemm_deep = strcmp(r, "shallow") != 0;
   *out = ctx;
   return BE_OK;
 }
@@ -496,6 +498,7 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
   L.grid = p.grid;
   L.max_contrib = p.max_contrib;
   L.pdl = ctx->use_pdl;
+  L.deep = ctx->gemm_deep;
   epi.ws = ws->splitws;
   epi.counters = ws->counters;
   L.epi = epi;
@@ -735,6 +738,7 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.grid = p.grid;
   L.max_contrib = p.max_contrib;
   L.pdl = ctx->use_pdl;
+  L.deep = ctx->gemm_deep;
   L.epi.mode = getenv("BE_GEMM_NOEPI") ? -1 : bx::kStore;
   if (const char* v = getenv("BE_GEMM_DBG")) L.epi.dbg = atoi(v);
   L.epi.ntok = ntok;

@@ -97,8 +97,8 @@ struct SkRange {
   }
 };
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(192, gemm_ctas_per_sm<BN>())
+template <int BN, int STAGES, int CTAS>
+__global__ void __launch_bounds__(192, CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
                    int max_contrib, EpiParams E) {
@@ -346,11 +346,12 @@ __global__ void __launch_bounds__(192, gemm_ctas_per_sm<BN>())
   if (warp == 1) tmem_free<kTmemCols>(tmem_base);
 }
 
-template <int BN>
+template <int BN, bool kDeep>
 static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
-  constexpr int STAGES = gemm_stages<BN>();
+  constexpr int STAGES = kDeep ? gemm_stages_deep<BN>() : gemm_stages<BN>();
+  constexpr int CTAS = kDeep ? 1 : gemm_ctas_per_sm<BN>();
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  auto kern = gemm_sk_kernel<BN, STAGES>;
+  auto kern = gemm_sk_kernel<BN, STAGES, CTAS>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -375,12 +376,22 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
 
 cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream) {
   if (L.N % kBM != 0 || L.K % kBK != 0 || L.grid < 1) return cudaErrorInvalidValue;
+  if (L.deep) {
+    switch (L.bn) {
+      case 16: return launch_bn<16, true>(L, stream);
+      case 32: return launch_bn<32, true>(L, stream);
+      case 64: return launch_bn<64, true>(L, stream);
+      case 128: return launch_bn<128, true>(L, stream);
+      case 256: return launch_bn<256, true>(L, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (L.bn) {
-    case 16: return launch_bn<16>(L, stream);
-    case 32: return launch_bn<32>(L, stream);
-    case 64: return launch_bn<64>(L, stream);
-    case 128: return launch_bn<128>(L, stream);
-    case 256: return launch_bn<256>(L, stream);
+    case 16: return launch_bn<16, false>(L, stream);
+    case 32: return launch_bn<32, false>(L, stream);
+    case 64: return launch_bn<64, false>(L, stream);
+    case 128: return launch_bn<128, false>(L, stream);
+    case 256: return launch_bn<256, true>(L, stream);
     default: return cudaErrorInvalidValue;
   }
 }

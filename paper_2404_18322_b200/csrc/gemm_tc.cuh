@@ -65,6 +65,11 @@ __host__ __device__ constexpr int gemm_stages() {
   return s > 8 ? 8 : s;
 }
 template <int BN>
+__host__ __device__ constexpr int gemm_stages_deep() {
+  const int s = (200 * 1024) / GemmSmem<BN>::kStageBytes;
+  return s > 8 ? 8 : s;
+}
+template <int BN>
 __host__ __device__ constexpr int gemm_ctas_per_sm() {
   return BN >= 256 ? 1 : 2;
 }
@@ -83,6 +88,7 @@ struct GemmLaunch {
   int grid;                  // persistent CTAs (stream-K ranges)
   int max_contrib;           // workspace slots per tile
   int pdl;                   // launch with programmatic stream serialization
+  int deep;                  // 1: ~200 KB ring, one CTA/SM; 0: ~100 KB ring, two CTAs/SM
   EpiParams epi;
 };
 
