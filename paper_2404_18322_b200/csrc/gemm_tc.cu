@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(192, CTAS)
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
         return wpk + ((size_t)(tile % m_tiles) * nkb + kb) * (kBM * kBK);
       };
-      const bool load_b = (E.dbg & 2) == 0;
-      const uint32_t stage_bytes = load_b ? S::kStageBytes : S::kABytes;
+      constexpr bool load_b = true;
+      constexpr uint32_t stage_bytes = S::kStageBytes;
       // weights first: nothing upstream writes them, so they stream under the previous kernel
       for (int i = 0; i < pre; ++i) {
         mbar_arrive_expect_tx(&full[i], stage_bytes);
@@ -201,22 +201,15 @@ __global__ void __launch_bounds__(192, CTAS)
         mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
         tc_fence_after();
         if (lane == 0) {
-          if (i == 0) stamp(E, 4);
-          if (it + (kb - kb0) == it_end - 1) stamp(E, 5);
           const uint32_t a_addr = smem_u32(sA + s * S::kABytes);
           const uint32_t b_addr = smem_u32(sB + s * S::kBBytes);
-          if (E.dbg & 1) {
-            mbar_arrive(&empty[s]);
-            if (kb == kb1 - 1) mbar_arrive(&tfull[a]);
-          } else {
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              umma_bf16(tacc, make_sdesc_k128(a_addr + k * 32), make_sdesc_k128(b_addr + k * 32),
-                        idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            }
-            umma_commit(&empty[s]);
-            if (kb == kb1 - 1) umma_commit(&tfull[a]);
+          for (int k = 0; k < kBK / 16; ++k) {
+            umma_bf16(tacc, make_sdesc_k128(a_addr + k * 32), make_sdesc_k128(b_addr + k * 32),
+                      idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
+          umma_commit(&empty[s]);
+          if (kb == kb1 - 1) umma_commit(&tfull[a]);
         }
         __syncwarp();
       }
