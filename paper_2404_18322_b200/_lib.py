@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libblockexec.so")
+LIB_PATH = os.environ.get("BE_LIB_PATH") or os.path.join(_HERE, "libblockexec.so")
 
 BE_OK = 0
 BE_ERRORS = {1: "invalid argument", 2: "bad state", 3: "CUDA failure", 4: "out of device memory",
