@@ -739,7 +739,7 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.max_contrib = p.max_contrib;
   L.pdl = ctx->use_pdl;
   L.deep = ctx->gemm_deep;
-  L.epi.mode = getenv("BE_GEMM_NOEPI") ? -1 : bx::kStore;
+  L.epi.mode = bx::kStore;
   if (const char* v = getenv("BE_GEMM_DBG")) L.epi.dbg = atoi(v);
   L.epi.ntok = ntok;
   L.epi.out = static_cast<bf16*>(out);

@@ -31,57 +31,101 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// Applies the fused epilogue to 16 consecutive token columns starting at token t0 for this
-// thread's feature row f; all lanes of a warp share t0.
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0,
-                                               const float (&acc)[16]) {
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&p);
+}
+
+// Fused epilogue over 16 consecutive token columns [t0, t0+16) of this thread's feature row f
+// (all lanes of a warp share t0; lanes hold consecutive features). Stores are vectorised across
+// lane pairs: for token pair (2p, 2p+1) one shuffle gives the even lane features (f, f+1) of
+// token 2p and the odd lane features (f-1, f) of token 2p+1, so every store is a bf16x2 / float2.
+template <int MODE>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0, float (&v)[16]) {
   const int lane = threadIdx.x & 31;
-  if (E.mode < 0) return;  // diagnostics: accumulate only
+  const bool odd = (lane & 1) != 0;
+  const int nvalid = E.ntok - t0 < 16 ? E.ntok - t0 : 16;  // warp-uniform, >= 1
+  if (MODE != kQKV && E.rstd != nullptr) {
+    // fused RMSNorm row scale (gamma folded into the weights)
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int t = t0 + i;
-    const bool valid = t < E.ntok;  // warp-uniform
-    float v = acc[i];
-    if (E.rstd != nullptr && valid) v *= E.rstd[t];
-    if (E.mode == kResid) {
-      if (valid) {
-        float* px = E.xres + (size_t)t * E.ldr + f;
-        const float nv = *px + v;
-        *px = nv;
-        E.xres_b[(size_t)t * E.ldr + f] = __float2bfloat16_rn(nv);
-      }
-    } else if (E.mode == kStore) {
-      if (valid) E.out[(size_t)t * E.ldo + f] = __float2bfloat16_rn(v);
-    } else if (E.mode == kSwiGLU) {
-      const float other = __shfl_xor_sync(0xffffffffu, v, 1);
-      if (valid && (lane & 1) == 0) {
-        // even lane holds gate_j, odd lane holds up_j
-        E.out[(size_t)t * E.ldo + (f >> 1)] = __float2bfloat16_rn(silu(v) * other);
-      }
-    } else {  // kQKV
-      const int d = E.d_model;
-      const int sec = f / d;  // 0 q, 1 k, 2 v (warp-uniform: d % 32 == 0)
-      const int fi = f - sec * d;
-      const int head = fi / E.head_dim;
-      const int e = fi - head * E.head_dim;
-      const float other = __shfl_xor_sync(0xffffffffu, v, 1);
-      if (!valid) continue;
-      float o = v;
-      if (sec < 2) {
-        // rows are pair-interleaved per head: even = dim j, odd = dim j + hd/2 (rotate_half)
-        const float2 cs = E.rope[(size_t)E.tok[t * 5 + 3] * (E.head_dim >> 1) + (e >> 1)];
-        o = (lane & 1) == 0 ? v * cs.x - other * cs.y : v * cs.x + other * cs.y;
-      }
-      if (sec == 0) {
-        E.out[(size_t)t * E.ldo + fi] = __float2bfloat16_rn(o);
+    for (int i = 0; i < 16; ++i)
+      if (i < nvalid) v[i] *= __ldg(E.rstd + t0 + i);
+  }
+  if constexpr (MODE == kStore || MODE == kResid) {
+    const int fe = f & ~1;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[2 * p] : v[2 * p + 1], 1);
+      const float lo = odd ? recv : v[2 * p];
+      const float hi = odd ? v[2 * p + 1] : recv;
+      const int t = t0 + 2 * p + (odd ? 1 : 0);
+      if (2 * p + (odd ? 1 : 0) >= nvalid) continue;
+      if constexpr (MODE == kStore) {
+        *reinterpret_cast<uint32_t*>(E.out + (size_t)t * E.ldo + fe) = pack_bf16x2(lo, hi);
       } else {
-        const int slot = E.tok[t * 5 + 2];
+        float2* px = reinterpret_cast<float2*>(E.xres + (size_t)t * E.ldr + fe);
+        float2 x = *px;
+        x.x += lo;
+        x.y += hi;
+        *px = x;
+        *reinterpret_cast<uint32_t*>(E.xres_b + (size_t)t * E.ldr + fe) = pack_bf16x2(x.x, x.y);
+      }
+    }
+  } else if constexpr (MODE == kSwiGLU) {
+    // even lane holds gate_j, odd lane holds up_j (rows interleaved at load time)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[2 * p] : v[2 * p + 1], 1);
+      const float g = odd ? recv : v[2 * p];
+      const float u = odd ? v[2 * p + 1] : recv;
+      const int ti = 2 * p + (odd ? 1 : 0);
+      if (ti >= nvalid) continue;
+      E.out[(size_t)(t0 + ti) * E.ldo + (f >> 1)] = __float2bfloat16_rn(silu(g) * u);
+    }
+  } else {  // kQKV: rstd, RoPE on q/k, q to the q buffer, k/v to their paged KV slots
+    const int d = E.d_model;
+    const int sec = f / d;  // warp-uniform (d % 32 == 0)
+    const int fi = f - sec * d;
+    const int head = fi / E.head_dim;
+    const int e = fi - head * E.head_dim;
+    // token metadata of the chunk: lane i (< 16) fetches token t0+i, broadcast by shuffles
+    const int ti_l = lane & 15;
+    const bool have = ti_l < nvalid;
+    const int my_slot = have ? __ldg(E.tok + (size_t)(t0 + ti_l) * 5 + 2) : 0;
+    const int my_pos = have ? __ldg(E.tok + (size_t)(t0 + ti_l) * 5 + 3) : 0;
+    const float my_rs = (have && E.rstd != nullptr) ? __ldg(E.rstd + t0 + ti_l) : 1.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] *= __shfl_sync(0xffffffffu, my_rs, i);
+    if (sec < 2) {
+      // rows are pair-interleaved per head: even = dim j, odd = dim j + hd/2 (rotate_half)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float other = __shfl_xor_sync(0xffffffffu, v[i], 1);
+        const int pos = __shfl_sync(0xffffffffu, my_pos, i);
+        if (i < nvalid) {
+          const float2 cs = __ldg(E.rope + (size_t)pos * (E.head_dim >> 1) + (e >> 1));
+          v[i] = odd ? v[i] * cs.x + other * cs.y : v[i] * cs.x - other * cs.y;
+        }
+      }
+    }
+    const int ee = e & ~1;
+    const int H = d / E.head_dim;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[2 * p] : v[2 * p + 1], 1);
+      const float lo = odd ? recv : v[2 * p];
+      const float hi = odd ? v[2 * p + 1] : recv;
+      const int ti = 2 * p + (odd ? 1 : 0);
+      const int slot = __shfl_sync(0xffffffffu, my_slot, ti);
+      if (ti >= nvalid) continue;
+      if (sec == 0) {
+        *reinterpret_cast<uint32_t*>(E.out + (size_t)(t0 + ti) * E.ldo + (fi & ~1)) =
+            pack_bf16x2(lo, hi);
+      } else {
         const long long page = slot >> 4;
-        const int tok = slot & 15;
-        const int H = d / E.head_dim;
         const size_t idx = (size_t)(page * E.page_elems + (long long)E.layer * E.layer_elems) +
-                           ((size_t)((sec - 1) * H + head) * 16 + tok) * E.head_dim + e;
-        E.kv_pool[idx] = __float2bfloat16_rn(o);
+                           ((size_t)((sec - 1) * H + head) * 16 + (slot & 15)) * E.head_dim + ee;
+        *reinterpret_cast<uint32_t*>(E.kv_pool + idx) = pack_bf16x2(lo, hi);
       }
     }
   }
@@ -97,7 +141,7 @@ struct SkRange {
   }
 };
 
-template <int BN, int STAGES, int CTAS>
+template <int BN, int STAGES, int CTAS, int MODE>
 __global__ void __launch_bounds__(192, CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
@@ -241,7 +285,7 @@ __global__ void __launch_bounds__(192, CTAS)
           if (n0 + c0 >= E.ntok) break;
           float acc[16];
           tmem_ld16(t_lane + c0, acc);
-          epilogue_chunk(E, f, n0 + c0, acc);
+          epilogue_chunk<MODE>(E, f, n0 + c0, acc);
         }
       } else {
         // partial tile: publish, last contributor reduces and runs the epilogue
@@ -322,7 +366,7 @@ __global__ void __launch_bounds__(192, CTAS)
                 }
               }
             }
-            epilogue_chunk(E, f, n0 + c0, acc);
+            epilogue_chunk<MODE>(E, f, n0 + c0, acc);
           }
         }
         named_bar_sync(1, 128);  // flag is reused by the next partial tile
@@ -339,12 +383,12 @@ __global__ void __launch_bounds__(192, CTAS)
   if (warp == 1) tmem_free<kTmemCols>(tmem_base);
 }
 
-template <int BN, bool kDeep>
+template <int BN, int MODE>
 static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
-  constexpr int STAGES = kDeep ? gemm_stages_deep<BN>() : gemm_stages<BN>();
-  constexpr int CTAS = kDeep ? 1 : gemm_ctas_per_sm<BN>();
+  constexpr int STAGES = gemm_stages_deep<BN>();
+  constexpr int CTAS = 1;
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  auto kern = gemm_sk_kernel<BN, STAGES, CTAS>;
+  auto kern = gemm_sk_kernel<BN, STAGES, CTAS, MODE>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -367,24 +411,25 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
                             L.max_contrib, L.epi);
 }
 
+template <int MODE>
+static cudaError_t launch_mode(const GemmLaunch& L, cudaStream_t stream) {
+  switch (L.bn) {
+    case 16: return launch_bn<16, MODE>(L, stream);
+    case 32: return launch_bn<32, MODE>(L, stream);
+    case 64: return launch_bn<64, MODE>(L, stream);
+    case 128: return launch_bn<128, MODE>(L, stream);
+    case 256: return launch_bn<256, MODE>(L, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream) {
   if (L.N % kBM != 0 || L.K % kBK != 0 || L.grid < 1) return cudaErrorInvalidValue;
-  if (L.deep) {
-    switch (L.bn) {
-      case 16: return launch_bn<16, true>(L, stream);
-      case 32: return launch_bn<32, true>(L, stream);
-      case 64: return launch_bn<64, true>(L, stream);
-      case 128: return launch_bn<128, true>(L, stream);
-      case 256: return launch_bn<256, true>(L, stream);
-      default: return cudaErrorInvalidValue;
-    }
-  }
-  switch (L.bn) {
-    case 16: return launch_bn<16, false>(L, stream);
-    case 32: return launch_bn<32, false>(L, stream);
-    case 64: return launch_bn<64, false>(L, stream);
-    case 128: return launch_bn<128, false>(L, stream);
-    case 256: return launch_bn<256, true>(L, stream);
+  switch (L.epi.mode) {
+    case kStore: return launch_mode<kStore>(L, stream);
+    case kResid: return launch_mode<kResid>(L, stream);
+    case kSwiGLU: return launch_mode<kSwiGLU>(L, stream);
+    case kQKV: return launch_mode<kQKV>(L, stream);
     default: return cudaErrorInvalidValue;
   }
 }
