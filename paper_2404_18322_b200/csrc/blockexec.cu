@@ -714,7 +714,11 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   const int bn = bx::gemm_pick_bn(ntok);
   CUtensorMap mx;
   int rc;
-  if ((rc = make_map(ctx, &mx, x, ntok, K, bn)) != BE_OK) return rc;
+  // BE_GEMM_BREP=k: x holds k replicas of the activations, each padded to a BN multiple
+  const int brep = getenv("BE_GEMM_BREP") ? atoi(getenv("BE_GEMM_BREP")) : 1;
+  const int copy_rows = (ntok + bn - 1) / bn * bn;
+  if ((rc = make_map(ctx, &mx, x, brep > 1 ? (uint64_t)brep * copy_rows : ntok, K, bn)) != BE_OK)
+    return rc;
   const bx::GemmPlan p =
       bx::gemm_plan(N, K, ntok, bn, ctx->num_sms, (size_t)1 << 40, 1 << 16, grid_cap);
   if (p.ws_needed > ctx->gemm_ws_elems) {
@@ -740,6 +744,8 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.pdl = ctx->use_pdl;
   L.deep = ctx->gemm_deep;
   L.epi.mode = bx::kStore;
+  L.b_copies = brep > 1 ? brep : 1;
+  L.b_copy_rows = copy_rows;
   if (const char* v = getenv("BE_GEMM_DBG")) L.epi.dbg = atoi(v);
   L.epi.ntok = ntok;
   L.epi.out = static_cast<bf16*>(out);

@@ -145,7 +145,9 @@ template <int BN, int STAGES, int CTAS, int MODE>
 __global__ void __launch_bounds__(192, CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
-                   int max_contrib, EpiParams E) {
+                   int max_contrib, int b_copies, int b_copy_rows, EpiParams E) {
+  // activation replica this CTA reads (spreads same-k-block reads over L2 slices)
+  const int b_row0 = (int)(blockIdx.x % b_copies) * b_copy_rows;
   using S = GemmSmem<BN>;
   constexpr uint32_t kTmemCols = tmem_cols<2 * BN>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(192, CTAS)
       for (int i = 0; i < pre && load_b; ++i) {
         const long long it = it_begin + i;
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
-        tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
+        tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, kb * kBK, (tile / m_tiles) * BN + b_row0,
                     kEvictLast);
       }
       for (long long i = pre; i < n_it; ++i) {
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(192, CTAS)
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         bulk_load(sA + s * S::kABytes, wtile(it), S::kABytes, &full[s], kEvictFirst);
         if (load_b)
-          tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
+          tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN + b_row0,
                       kEvictLast);
       }
       stamp(E, 3);
@@ -408,7 +410,7 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = L.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, L.w_packed, *L.map_x, L.K, m_tiles, n_tiles,
-                            L.max_contrib, L.epi);
+                            L.max_contrib, L.b_copies > 0 ? L.b_copies : 1, L.b_copy_rows, L.epi);
 }
 
 template <int MODE>

@@ -89,6 +89,8 @@ struct GemmLaunch {
   int max_contrib;           // workspace slots per tile
   int pdl;                   // launch with programmatic stream serialization
   int deep;                  // 1: ~200 KB ring, one CTA/SM; 0: ~100 KB ring, two CTAs/SM
+  int b_copies;              // activation replicas (CTA c reads replica c % b_copies); 0/1 = one
+  int b_copy_rows;           // rows between replicas in map_x
   EpiParams epi;
 };
 
