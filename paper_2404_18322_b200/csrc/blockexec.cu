@@ -768,7 +768,7 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
     cudaFree(trace);
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < p.grid; ++c) t0 = h[c * 8] && h[c * 8] < t0 ? h[c * 8] : t0;
-    const char* names[8] = {"entry", "setup", "pdl_wait", "last_load", "first_full", "last_full",
+    const char* names[8] = {"entry", "setup", "pdl_wait", "last_load", "last_tfull", "epi_done",
                             "first_tfull", "exit"};
     fprintf(stderr, "gemm trace N=%d K=%d ntok=%d grid=%d\n", N, K, ntok, p.grid);
     for (int k = 0; k < 8; ++k) {

@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(192, CTAS)
       mbar_wait(&tfull[a], u & 1u);
       tc_fence_after();
       if (seg == 0 && warp == 2 && lane == 0) stamp(E, 6);
+      if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
       const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
       if (kb0 == 0 && kb1 == nkb) {
 #pragma unroll 1
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(192, CTAS)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
     }
+    if (warp == 2 && lane == 0) stamp(E, 5);
   }
 
   tc_fence_before();

@@ -9,7 +9,8 @@ import torch  # noqa: E402
 from paper_2404_18322_b200 import device as dev  # noqa: E402
 
 ctx = dev.Context(0)
-for N, K, M in [(4096, 4096, 64), (22016, 4096, 64), (4096, 11008, 16)]:
+shapes = [(4096, 4096, 64), (4096, 4096, 16), (22016, 4096, 64), (22016, 4096, 16)]
+for N, K, M in shapes:
     w = dev.pack_weight(ctx, (torch.rand(N, K, device="cuda", dtype=torch.bfloat16) - 0.5) * 0.05)
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
@@ -17,7 +18,6 @@ for N, K, M in [(4096, 4096, 64), (22016, 4096, 64), (4096, 11008, 16)]:
     for _ in range(3):
         dev.gemm_bf16(ctx, w, x, out, packed=True)
     ctx.sync()
-    # flush L2 with a big write so the weights come from HBM
     junk = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     junk.fill_(1)
     torch.cuda.synchronize()
