@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(192, CTAS)
       }
       stamp(E, 3);
     }
+    __syncwarp();  // reconverge before the CTA barrier (barriers are .aligned)
   } else if (warp == 1) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc_bf16(kBM, BN);
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(192, CTAS)
       tc_fence_after();
       if (seg == 0 && warp == 2 && lane == 0) stamp(E, 6);
       if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
+      __syncwarp();
       const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
       if (kb0 == 0 && kb1 == nkb) {
 #pragma unroll 1
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(192, CTAS)
           if (last) *ctr = 0;  // self-reset for the next launch / graph replay
           *flag = last;
         }
+        __syncwarp();
         named_bar_sync(1, 128);
         if (*flag) {
           __threadfence();
@@ -379,6 +382,7 @@ __global__ void __launch_bounds__(192, CTAS)
       if (lane == 0) mbar_arrive(&tempty[a]);
     }
     if (warp == 2 && lane == 0) stamp(E, 5);
+    __syncwarp();
   }
 
   tc_fence_before();
