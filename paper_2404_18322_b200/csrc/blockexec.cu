@@ -780,6 +780,18 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
       fprintf(stderr, "  %-12s min %8.2f  med %8.2f  max %8.2f us (n=%zu)\n", names[k], v.front(),
               v[v.size() / 2], v.back(), v.size());
     }
+    int inverted = 0;
+    for (int c = 0; c < p.grid; ++c)
+      if (h[c * 8 + 7] && h[c * 8 + 5] && h[c * 8 + 7] < h[c * 8 + 5]) ++inverted;
+    fprintf(stderr, "  CTAs with exit stamp < epilogue-done stamp: %d; cta0 epi_done %.2f exit %.2f\n",
+            inverted, (h[5] - t0) / 1e3, (h[7] - t0) / 1e3);
+    int worst = 0;
+    for (int c = 0; c < p.grid; ++c)
+      if (h[c * 8 + 5] > h[worst * 8 + 5]) worst = c;
+    fprintf(stderr, "  slowest epilogue cta %d:", worst);
+    for (int k = 0; k < 8; ++k)
+      fprintf(stderr, " %s=%.2f", names[k], h[worst * 8 + k] ? (h[worst * 8 + k] - t0) / 1e3 : -1.0);
+    fprintf(stderr, "\n");
   }
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "gemm: %s", cudaGetErrorString(e));
 }
