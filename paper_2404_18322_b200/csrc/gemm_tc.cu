@@ -317,11 +317,15 @@ __global__ void __launch_bounds__(192, CTAS)
           for (int j = 0; j < 4; ++j)
             __stcg(slot + (c0 >> 2) + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
         }
-        __threadfence();
+        // Hand-off without sequentially-consistent fences (MEMBAR.SC.GPU stalls for µs while
+        // HBM is saturated): the CTA barrier orders the 128 threads' partial stores before one
+        // acq_rel atomic at GPU scope (release is cumulative); the last arriver's acquire
+        // orders the other contributors' partials before its L2 (.cg) loads.
         named_bar_sync(1, 128);
         if (warp == 2 && lane == 0) {
           int* ctr = E.counters + tile;
-          const int prev = atomicAdd(ctr, 1);
+          int prev;
+          asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
           const int last = prev == n_contrib - 1;
           if (last) *ctr = 0;  // self-reset for the next launch / graph replay
           *flag = last;
@@ -329,7 +333,6 @@ __global__ void __launch_bounds__(192, CTAS)
         __syncwarp();
         named_bar_sync(1, 128);
         if (*flag) {
-          __threadfence();
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             if (n0 + c0 >= E.ntok) break;
