@@ -54,6 +54,11 @@ typedef struct {
   float init_scale; /* weights uniform in [-s, s] */
   uint64_t seed;
   const char* name; /* stream prefix, e.g. "b0" */
+  /* Component sequence of the block, one char per zoo component (ComponentKind, zoo.hpp:12):
+   * 'a' attention (RMSNorm, QKV, RoPE, paged attention, O, residual), 'f' ffn (RMSNorm, SwiGLU
+   * MLP, residual). NULL = n_layers decoder layers "afaf...". Blocks split by the zoo's
+   * partitioner may start or end mid-layer ("fa", "a", "f"). */
+  const char* components;
 } be_block_desc;
 
 /* One token row of an execution batch (decode: one per request; prefill: one per prompt token). */

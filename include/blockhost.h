@@ -98,6 +98,7 @@ typedef struct {
                                   prefill/decode); 1 = lockstep (all prefill, then decode) */
   int use_graphs;              /* capture steady-state decode steps in CUDA graphs */
   uint64_t seed;               /* synthetic prompt embeddings: stream "inputs:req<r>" */
+  int dry_run;                 /* 1: control plane only (no device work; ctx may be NULL) */
 } bh_workload;
 
 typedef struct {

@@ -38,17 +38,20 @@ typedef struct {
   float norm_eps, rope_theta, init_scale;
   uint64_t seed;
   const char* name;
+  const char* components; /* 'a' attention / 'f' ffn per zoo component; NULL = n_layers x "af" */
 } or_block_desc; /* same layout as be_block_desc (include/blockexec.h) */
 
 typedef struct {
-  float *wq, *wk, *wv, *wo, *wg, *wu, *wd; /* logical row-major [out][in] */
+  float *wq, *wk, *wv, *wo, *wg, *wu, *wd; /* logical row-major [out][in]; NULL if absent */
 } or_layer;
 
 typedef struct {
   or_block_desc desc;
   char name[64];
-  or_layer* layers;
-  float* rope_cos; /* [max_pos][hd/2] */
+  char comps[1024];
+  int n_att, n_ffn;
+  or_layer* layers; /* l-th attention component uses wq..wo, l-th ffn wg..wd */
+  float* rope_cos;  /* [max_pos][hd/2] */
   float* rope_sin;
 } or_block;
 
@@ -69,28 +72,44 @@ static void fill_weight(float* w, size_t rows, size_t cols, uint64_t seed, const
 }
 
 or_block* or_block_create(const or_block_desc* d) {
-  if (!d || d->n_layers <= 0 || d->n_heads * d->head_dim != d->d_model || d->max_pos <= 0)
-    return NULL;
+  if (!d || d->n_heads * d->head_dim != d->d_model || d->max_pos <= 0) return NULL;
   or_block* b = (or_block*)calloc(1, sizeof(or_block));
   b->desc = *d;
   snprintf(b->name, sizeof b->name, "%s", d->name ? d->name : "block");
   b->desc.name = b->name;
+  if (d->components) {
+    snprintf(b->comps, sizeof b->comps, "%s", d->components);
+  } else {
+    for (int l = 0; l < d->n_layers && 2 * l + 2 < (int)sizeof b->comps; ++l) strcat(b->comps, "af");
+  }
+  b->desc.components = b->comps;
+  for (const char* c = b->comps; *c; ++c) {
+    if (*c == 'a') ++b->n_att;
+    else if (*c == 'f') ++b->n_ffn;
+    else { free(b); return NULL; }
+  }
+  if (b->n_att + b->n_ffn == 0) { free(b); return NULL; }
+  b->desc.n_layers = b->n_att > b->n_ffn ? b->n_att : b->n_ffn;
   const size_t D = d->d_model, F = d->d_ff;
-  b->layers = (or_layer*)calloc(d->n_layers, sizeof(or_layer));
-  for (int l = 0; l < d->n_layers; ++l) {
+  b->layers = (or_layer*)calloc(b->desc.n_layers, sizeof(or_layer));
+  for (int l = 0; l < b->n_att; ++l) {
     or_layer* L = &b->layers[l];
     L->wq = (float*)malloc(D * D * 4);
     L->wk = (float*)malloc(D * D * 4);
     L->wv = (float*)malloc(D * D * 4);
     L->wo = (float*)malloc(D * D * 4);
-    L->wg = (float*)malloc(F * D * 4);
-    L->wu = (float*)malloc(F * D * 4);
-    L->wd = (float*)malloc(D * F * 4);
-    if (!L->wq || !L->wk || !L->wv || !L->wo || !L->wg || !L->wu || !L->wd) return NULL;
+    if (!L->wq || !L->wk || !L->wv || !L->wo) return NULL;
     fill_weight(L->wq, D, D, d->seed, b->name, l, "wq", d->init_scale);
     fill_weight(L->wk, D, D, d->seed, b->name, l, "wk", d->init_scale);
     fill_weight(L->wv, D, D, d->seed, b->name, l, "wv", d->init_scale);
     fill_weight(L->wo, D, D, d->seed, b->name, l, "wo", d->init_scale);
+  }
+  for (int l = 0; l < b->n_ffn; ++l) {
+    or_layer* L = &b->layers[l];
+    L->wg = (float*)malloc(F * D * 4);
+    L->wu = (float*)malloc(F * D * 4);
+    L->wd = (float*)malloc(D * F * 4);
+    if (!L->wg || !L->wu || !L->wd) return NULL;
     fill_weight(L->wg, F, D, d->seed, b->name, l, "wg", d->init_scale);
     fill_weight(L->wu, F, D, d->seed, b->name, l, "wu", d->init_scale);
     fill_weight(L->wd, D, F, d->seed, b->name, l, "wd", d->init_scale);
@@ -135,7 +154,7 @@ const float* or_block_weight(const or_block* b, int layer, const char* t) {
 
 or_seq* or_seq_create(const or_block* b, int max_tokens) {
   or_seq* s = (or_seq*)calloc(1, sizeof(or_seq));
-  s->n_layers = b->desc.n_layers;
+  s->n_layers = b->n_att; /* K/V planes: one per attention component */
   s->d = b->desc.d_model;
   s->max_tokens = max_tokens;
   s->kv = (float*)calloc((size_t)s->n_layers * 2 * max_tokens * s->d, 4);
@@ -227,7 +246,20 @@ int or_block_forward(const or_block* b, or_seq** seqs, int n, const int* tok_seq
   memcpy(x, x_in, (size_t)n * d * 4);
   const float scale = 1.0f / sqrtf((float)hd);
 
-  for (int l = 0; l < D->n_layers; ++l) {
+  int ia = 0, jf = 0;
+  for (const char* comp = b->comps; *comp; ++comp) {
+    if (*comp == 'f') {
+      /* ffn component */
+      const or_layer* L = &b->layers[jf++];
+      rmsnorm(x, xn, n, d, D->norm_eps);
+      matmul_nt(xn, L->wg, g, n, F, d);
+      matmul_nt(xn, L->wu, u, n, F, d);
+      for (size_t i = 0; i < (size_t)n * F; ++i) g[i] = g[i] / (1.0f + expf(-g[i])) * u[i];
+      matmul_nt(g, L->wd, o, n, d, F);
+      for (size_t i = 0; i < (size_t)n * d; ++i) x[i] += o[i];
+      continue;
+    }
+    const int l = ia++;
     const or_layer* L = &b->layers[l];
     /* attention component */
     rmsnorm(x, xn, n, d, D->norm_eps);
@@ -281,13 +313,6 @@ int or_block_forward(const or_block* b, or_seq** seqs, int n, const int* tok_seq
       free(sc);
     }
     matmul_nt(att, L->wo, o, n, d, d);
-    for (size_t i = 0; i < (size_t)n * d; ++i) x[i] += o[i];
-    /* ffn component */
-    rmsnorm(x, xn, n, d, D->norm_eps);
-    matmul_nt(xn, L->wg, g, n, F, d);
-    matmul_nt(xn, L->wu, u, n, F, d);
-    for (size_t i = 0; i < (size_t)n * F; ++i) g[i] = g[i] / (1.0f + expf(-g[i])) * u[i];
-    matmul_nt(g, L->wd, o, n, d, F);
     for (size_t i = 0; i < (size_t)n * d; ++i) x[i] += o[i];
   }
   memcpy(x_out, x, (size_t)n * d * 4);

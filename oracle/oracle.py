@@ -19,7 +19,7 @@ class OrBlockDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
                 ("head_dim", C.c_int), ("d_ff", C.c_int), ("max_pos", C.c_int),
                 ("norm_eps", C.c_float), ("rope_theta", C.c_float), ("init_scale", C.c_float),
-                ("seed", C.c_uint64), ("name", C.c_char_p)]
+                ("seed", C.c_uint64), ("name", C.c_char_p), ("components", C.c_char_p)]
 
 
 _lib = None
@@ -66,9 +66,11 @@ class OracleBlock:
     def __init__(self, shape, name: str, seed: int = 1):
         self.shape, self.name = shape, name
         self._nb = name.encode()
+        comps = getattr(shape, "comps", None) or "af" * shape.n_layers
+        self._cb = comps.encode()
         d = OrBlockDesc(shape.n_layers, shape.d_model, shape.n_heads, shape.head_dim, shape.d_ff,
                         shape.max_pos, shape.norm_eps, shape.rope_theta, shape.init_scale, seed,
-                        self._nb)
+                        self._nb, self._cb)
         self.h = lib().or_block_create(C.byref(d))
         if not self.h:
             raise ValueError("oracle: bad block shape")
@@ -113,6 +115,7 @@ class OracleSeq:
         lib().or_seq_fill(self.h, length, seed)
 
     def kv(self, layer: int, which: int) -> np.ndarray:
+        """K (which=0) or V (1) cache of the layer-th attention component, [max_tokens][d]."""
         d = self.block.shape.d_model
         ptr = lib().or_seq_kv(self.h, layer, which)
         return np.ctypeslib.as_array(ptr, shape=(self.max_tokens, d)).copy()

@@ -1,1 +1,459 @@
-// placeholder: filled in with the reference control-plane shim
+// TEST INFRASTRUCTURE: a C ABI over the reference's own blocksim classes, compiled together with
+// the unmodified reference sources under /root/reference/proj/core into oracle/_ref/ (see
+// oracle/Makefile). Only tests/ load it, as the parity checker for the host control plane of
+// paper_2404_18322_b200 (csrc/host/*): queue/batch formation (InstancePool, agent.cpp:132-224),
+// paged KV bookkeeping (KvStore, kv.cpp:105-237), the cosine (signature_similarity,
+// zoo.cpp:78-88), migration planning (plan_migration, kv.cpp:16-58), percentiles
+// (metrics.cpp:30-38) and whole-simulation batch traces (Simulation::pump/on_batch_finish,
+// scenario.cpp:465-578).
+#include <cstdint>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <queue>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <unordered_set>
+#include <utility>
+#include <vector>
+
+#include "json.hpp"
+// Page ids and the running batch are private in the reference; the checker reads them.
+#define private public
+#include "blocksim/agent.hpp"
+#include "blocksim/kv.hpp"
+#include "blocksim/metrics.hpp"
+#include "blocksim/scenario.hpp"
+#include "blocksim/zoo.hpp"
+#undef private
+
+using namespace blocksim;
+
+namespace {
+int code_of(const std::exception& e) {
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
+  if (dynamic_cast<const std::logic_error*>(&e)) return 2;
+  return 5;
+}
+template <class F>
+int guard(std::string& err, F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    err = e.what();
+    return code_of(e);
+  }
+}
+}  // namespace
+
+// Same layout as bh_entry (include/blockhost.h)
+struct rs_entry {
+  int32_t request_id, chain_step, phase, tokens, context_tokens, kv_resident;
+  double est_cost_us;
+  uint64_t enqueue_seq;
+};
+
+static rs_entry to_rs(const QueueEntry& e) {
+  rs_entry r;
+  r.request_id = e.request_id;
+  r.chain_step = e.chain_step;
+  r.phase = e.phase == Phase::kDecode ? 1 : 0;
+  r.tokens = e.tokens;
+  r.context_tokens = e.context_tokens;
+  r.kv_resident = e.kv_resident ? 1 : 0;
+  r.est_cost_us = e.est_cost_us;
+  r.enqueue_seq = e.enqueue_seq;
+  return r;
+}
+
+static Cluster big_cluster(int n_devices) {
+  Cluster c;
+  c.add_server({0, 1e12});
+  for (int d = 0; d < n_devices; ++d) c.add_device({d, 0, "std", (std::int64_t)1 << 50, 1e15, 1e15});
+  c.set_inter_default(1e12);
+  return c;
+}
+
+// ---------------------------------------------------------------- InstancePool
+struct rs_pool {
+  Zoo zoo;
+  Cluster cluster;
+  std::unique_ptr<MemoryLedger> ledger;
+  std::unique_ptr<InstancePool> pool;
+  std::string err;
+};
+
+extern "C" {
+
+// n_blocks one-component foundations "m<i>" give blocks "b0".."b<n-1>"
+rs_pool* rs_pool_new(int n_blocks, int n_devices) {
+  auto* h = new rs_pool();
+  for (int i = 0; i < n_blocks; ++i) {
+    ComponentDescriptor c;
+    c.id = "m" + std::to_string(i) + ".att0";
+    c.kind = ComponentKind::kAttention;
+    c.embed_dim = 256;
+    c.model_id = "m" + std::to_string(i);
+    c.contents = {{c.id + ".w", 1000}};
+    h->zoo.add_foundation("m" + std::to_string(i), {c});
+  }
+  h->cluster = big_cluster(n_devices);
+  h->ledger = std::make_unique<MemoryLedger>(h->cluster);
+  h->pool = std::make_unique<InstancePool>(h->zoo, h->cluster, *h->ledger);
+  return h;
+}
+void rs_pool_free(rs_pool* h) { delete h; }
+const char* rs_pool_last_error(const rs_pool* h) { return h->err.c_str(); }
+
+int rs_pool_create_instance(rs_pool* h, const char* block, int device, int64_t now,
+                            int64_t ready_at, char* id_out, int cap) {
+  std::string id;
+  int rc = guard(h->err, [&] { id = h->pool->create(block, device, now, ready_at).id; });
+  if (rc) return rc;
+  if ((int)id.size() >= cap) return 1;
+  std::memcpy(id_out, id.c_str(), id.size() + 1);
+  return 0;
+}
+int rs_pool_mark_ready(rs_pool* h, const char* inst, int64_t now) {
+  return guard(h->err, [&] { h->pool->mark_ready(inst, now); });
+}
+int rs_pool_enqueue(rs_pool* h, const char* inst, const rs_entry* e) {
+  QueueEntry q;
+  q.request_id = e->request_id;
+  q.chain_step = e->chain_step;
+  q.phase = e->phase ? Phase::kDecode : Phase::kPrefill;
+  q.tokens = e->tokens;
+  q.context_tokens = e->context_tokens;
+  q.kv_resident = e->kv_resident != 0;
+  q.est_cost_us = e->est_cost_us;
+  return guard(h->err, [&] { h->pool->enqueue(inst, q); });
+}
+static int put(const std::vector<QueueEntry>& v, rs_entry* out, int cap, int* n) {
+  if (n) *n = (int)v.size();
+  if ((int)v.size() > cap) return 1;
+  for (size_t i = 0; i < v.size(); ++i) out[i] = to_rs(v[i]);
+  return 0;
+}
+int rs_pool_pop_batch(rs_pool* h, const char* inst, int budget, int64_t now, rs_entry* out, int cap,
+                      int* n, int* phase) {
+  ExecBatch b;
+  int rc = guard(h->err, [&] { b = h->pool->pop_batch(inst, budget, now); });
+  if (rc) return rc;
+  if (phase) *phase = b.phase == Phase::kDecode ? 1 : 0;
+  return put(b.members, out, cap, n);
+}
+int rs_pool_finish_batch(rs_pool* h, const char* inst, int64_t now) {
+  return guard(h->err, [&] { h->pool->finish_batch(inst, now); });
+}
+int rs_pool_next_runnable(rs_pool* h, int device, int64_t now, char* id_out, int cap) {
+  Instance* in = h->pool->next_runnable(device, now);
+  if (!in) return 0;
+  if ((int)in->id.size() >= cap) return -1;
+  std::memcpy(id_out, in->id.c_str(), in->id.size() + 1);
+  return 1;
+}
+int rs_pool_remove_queued(rs_pool* h, const char* inst, int req, rs_entry* out, int cap, int* n) {
+  std::vector<QueueEntry> v;
+  int rc = guard(h->err, [&] { v = h->pool->remove_queued(inst, req); });
+  return rc ? rc : put(v, out, cap, n);
+}
+int rs_pool_take_tail(rs_pool* h, const char* inst, int count, rs_entry* out, int cap, int* n) {
+  std::vector<QueueEntry> v;
+  int rc = guard(h->err, [&] { v = h->pool->take_tail(inst, (size_t)count); });
+  return rc ? rc : put(v, out, cap, n);
+}
+int rs_pool_queue(rs_pool* h, const char* inst, rs_entry* out, int cap, int* n, double* cost,
+                  int* executing) {
+  Instance* in = h->pool->find(inst);
+  if (!in) {
+    h->err = std::string("pool: unknown instance ") + inst;
+    return 2;
+  }
+  if (cost) *cost = in->queued_cost_us;
+  if (executing) *executing = in->executing ? 1 : 0;
+  std::vector<QueueEntry> v(in->queue.begin(), in->queue.end());
+  return put(v, out, cap, n);
+}
+
+// ---------------------------------------------------------------- KvStore
+struct rs_kv {
+  Cluster cluster;
+  std::unique_ptr<MemoryLedger> ledger;
+  std::unique_ptr<KvStore> kv;
+  std::string err;
+};
+
+rs_kv* rs_kv_new(int n_devices) {
+  auto* h = new rs_kv();
+  h->cluster = big_cluster(n_devices);
+  h->ledger = std::make_unique<MemoryLedger>(h->cluster);
+  h->kv = std::make_unique<KvStore>(*h->ledger);
+  return h;
+}
+void rs_kv_free(rs_kv* h) { delete h; }
+const char* rs_kv_last_error(const rs_kv* h) { return h->err.c_str(); }
+int rs_kv_create_segment(rs_kv* h, uint64_t r, const char* b, int dev, int64_t bpt) {
+  return guard(h->err, [&] { h->kv->create_segment(r, b, dev, bpt); });
+}
+int rs_kv_append_tokens(rs_kv* h, uint64_t r, const char* b, int n, int* added) {
+  return guard(h->err, [&] {
+    int a = h->kv->append_tokens(r, b, n);
+    if (added) *added = a;
+  });
+}
+int rs_kv_share_prefix(rs_kv* h, uint64_t r, uint64_t from, const char* b, int t, int* covered) {
+  return guard(h->err, [&] {
+    int c = h->kv->share_prefix(r, from, b, t);
+    if (covered) *covered = c;
+  });
+}
+int rs_kv_release(rs_kv* h, uint64_t r, const char* b) {
+  return guard(h->err, [&] { h->kv->release(r, b); });
+}
+int rs_kv_release_request(rs_kv* h, uint64_t r) {
+  return guard(h->err, [&] { h->kv->release_request(r); });
+}
+int rs_kv_move_segment(rs_kv* h, uint64_t r, const char* b, int dst) {
+  return guard(h->err, [&] { h->kv->move_segment(r, b, dst); });
+}
+int64_t rs_kv_query(const rs_kv* h, uint64_t r, const char* b, int what) {
+  switch (what) {
+    case 0: return h->kv->device_of(r, b);
+    case 1: return h->kv->tokens(r, b);
+    case 2: return h->kv->pages(r, b);
+    case 3: return h->kv->shared_pages(r, b);
+    case 4: return h->kv->segment_bytes(r, b);
+    case 5: return h->kv->has_segment(r, b) ? 1 : 0;
+    default: return -1;
+  }
+}
+int64_t rs_kv_bytes_saved(const rs_kv* h) { return h->kv->bytes_saved_by_sharing(); }
+int64_t rs_kv_used(const rs_kv* h, int dev) {
+  return h->ledger->used(dev, MemoryLedger::Category::kKv);
+}
+int rs_kv_page_ids(const rs_kv* h, uint64_t r, const char* b, uint64_t* out, int cap, int* n) {
+  auto it = h->kv->segments_.find({r, std::string(b)});
+  if (it == h->kv->segments_.end()) {
+    if (n) *n = 0;
+    return 0;
+  }
+  const auto& ids = it->second.page_ids;
+  if (n) *n = (int)ids.size();
+  if ((int)ids.size() > cap) return 1;
+  for (size_t i = 0; i < ids.size(); ++i) out[i] = ids[i];
+  return 0;
+}
+
+// ---------------------------------------------------------------- scalar functions
+double rs_cosine(const double* a, int na, const double* b, int nb, int* err) {
+  std::vector<double> va(a, a + na), vb(b, b + nb);
+  try {
+    *err = 0;
+    return signature_similarity(va, vb);
+  } catch (const std::exception& e) {
+    *err = code_of(e);
+    return 0.0;
+  }
+}
+int rs_plan_migration(int pages, int64_t rec, int64_t cp, int64_t* out /*[6]*/) {
+  try {
+    MigrationPlan p = plan_migration(pages, rec, cp);
+    out[0] = p.pages;
+    out[1] = p.rec_us_per_page;
+    out[2] = p.cp_us_per_page;
+    out[3] = p.recompute_pages;
+    out[4] = p.copy_pages;
+    out[5] = p.completion_us;
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+int rs_percentile(const double* v, int n, double q, double* out) {
+  try {
+    *out = percentile(std::vector<double>(v, v + n), q);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// ---------------------------------------------------------------- whole simulation trace
+// Zoo: foundation "base" of n_layers (attention, ffn) layers at `dim`, plus n_lora LoRA variants
+// whose attention is fused (attach "fuse") from layer `first_adapted` upward; served models are
+// the LoRAs. One device, instant parameter loads, no speculation/adaptivity/scaling, reviews
+// beyond the horizon: on one lane the batch sequence is independent of the cost tables.
+struct rs_sim {
+  std::vector<std::string> blocks;                 // block ids in zoo order
+  std::vector<std::string> block_kinds;            // per block: "a"/"f" per component
+  std::vector<std::vector<int>> chains;            // served model -> block indices
+  std::vector<int> req_model;                      // per request: served model index
+  // trace: per batch (instance, block, phase, members...)
+  std::vector<std::tuple<int, int, int>> recs;     // (instance index, block index, phase)
+  std::vector<std::vector<std::tuple<int, int, int>>> members;  // (req, step, ctx)
+  std::string err;
+  std::string report;
+};
+
+rs_sim* rs_sim_run(int n_layers, int dim, int n_lora, int first_adapted, int n_requests,
+                   const int32_t* prompts, const int32_t* outputs, int max_batch_tokens,
+                   int64_t arrival_gap_us) {
+  auto* h = new rs_sim();
+  try {
+    Zoo zoo;
+    std::vector<ComponentDescriptor> base;
+    for (int l = 0; l < n_layers; ++l) {
+      for (int k = 0; k < 2; ++k) {
+        ComponentDescriptor c;
+        c.id = "base." + std::string(k ? "ffn" : "att") + std::to_string(l);
+        c.kind = k ? ComponentKind::kFfn : ComponentKind::kAttention;
+        c.embed_dim = dim;
+        c.model_id = "base";
+        c.layer = l;
+        c.slot = k;
+        c.contents = {{c.id + ".w", k ? 3000 : 1000}};
+        base.push_back(c);
+      }
+    }
+    zoo.add_foundation("base", base);
+    for (int v = 0; v < n_lora; ++v) {
+      const std::string m = "lora" + std::to_string(v);
+      std::vector<ComponentDescriptor> comps;
+      for (int l = 0; l < n_layers; ++l) {
+        if (l >= first_adapted) {
+          ComponentDescriptor att;
+          att.id = m + ".att" + std::to_string(l);
+          att.kind = ComponentKind::kAttention;
+          att.embed_dim = dim;
+          att.model_id = m;
+          att.layer = l;
+          att.slot = 0;
+          att.attach = "fuse";
+          att.contents = {{"base.att" + std::to_string(l) + ".w", 1000}, {m + ".delta" + std::to_string(l), 8}};
+          comps.push_back(att);
+        } else {
+          comps.push_back(zoo.component("base.att" + std::to_string(l)));
+        }
+        comps.push_back(zoo.component("base.ffn" + std::to_string(l)));
+      }
+      zoo.add_model_pe(m, TuningKind::kLora, "base", comps);
+    }
+    Cluster cl;
+    cl.add_server({0, 1e12});
+    cl.add_device({0, 0, "std", (std::int64_t)1 << 50, 1e15, 1e18});
+    CostModel cost;
+    cost.set_device_class("std", 1.0);
+    auto grid = [](double coef) {
+      Interp2D g;
+      g.xs = {1, 64};
+      g.ys = {1, 4096};
+      g.v = {{coef, coef * 4096}, {coef * 64, coef * 64 * 4096}};
+      return g;
+    };
+    ComponentClassProfile att;
+    att.prefill = grid(3.0);
+    att.decode = grid(0.5);
+    cost.add_class(CostModel::class_key(ComponentKind::kAttention, dim), att);
+    ComponentClassProfile ffn;
+    ffn.prefill = grid(5.0);
+    ffn.decode = grid(0.7);
+    cost.add_class(CostModel::class_key(ComponentKind::kFfn, dim), ffn);
+    std::vector<Request> reqs;
+    for (int i = 0; i < n_requests; ++i) {
+      Request r;
+      r.id = (std::uint64_t)(i + 1);
+      r.app_id = i;
+      r.arrival_us = arrival_gap_us * i;
+      r.prompt_tokens = prompts[i];
+      r.output_tokens = outputs[i];
+      reqs.push_back(r);
+    }
+    ScenarioConfig cfg;
+    cfg.name = "parity";
+    cfg.speculation = false;
+    cfg.adaptive = false;
+    cfg.scaling = false;
+    cfg.max_batch_tokens = max_batch_tokens;
+    cfg.review_period_us = us_from_s(1e6);
+    cfg.kv_review_period_us = us_from_s(1e6);
+    cfg.metrics_tick_us = us_from_s(1e6);
+    Simulation sim(cfg, zoo, cl, cost, reqs);
+    // export zoo structure
+    const auto& pz = sim.plan().zoo;
+    std::map<std::string, int> bidx;
+    for (const auto& b : pz.block_ids()) {
+      bidx[b] = (int)h->blocks.size();
+      h->blocks.push_back(b);
+      std::string kinds;
+      for (const auto& c : pz.block_components(b))
+        kinds += c.kind == ComponentKind::kAttention ? "a" : "f";
+      h->block_kinds.push_back(kinds);
+    }
+    for (const auto& mid : sim.plan().served_models) {
+      std::vector<int> ch;
+      for (const auto& b : sim.plan().chains.at(mid)) ch.push_back(bidx.at(b));
+      h->chains.push_back(ch);
+    }
+    for (const auto& r : reqs)
+      h->req_model.push_back((int)(r.app_id % sim.plan().served_models.size()));
+    Simulation* sp = &sim;
+    std::map<std::string, int> inst_index;
+    sim.engine().set_trace_hook([h, sp, &bidx, &inst_index](SimTime, std::uint64_t, EventKind kind) {
+      if (kind != EventKind::kBatchFinish) return;
+      for (const auto& [dev, rb] : sp->running_) {
+        const Instance* in = sp->pool().find(rb.instance_id);
+        auto it = inst_index.find(rb.instance_id);
+        if (it == inst_index.end())
+          it = inst_index.emplace(rb.instance_id, std::stoi(rb.instance_id.substr(1)) - 1).first;
+        h->recs.emplace_back(it->second, bidx.at(in->block_id),
+                             rb.batch.phase == Phase::kDecode ? 1 : 0);
+        std::vector<std::tuple<int, int, int>> mem;
+        for (const auto& m : rb.batch.members)
+          mem.emplace_back(m.request_id, m.chain_step, m.context_tokens);
+        h->members.push_back(mem);
+      }
+    });
+    auto rep = sim.run();
+    h->report = rep.dump();
+  } catch (const std::exception& e) {
+    h->err = e.what();
+  }
+  return h;
+}
+void rs_sim_free(rs_sim* h) { delete h; }
+const char* rs_sim_error(const rs_sim* h) { return h->err.c_str(); }
+const char* rs_sim_report(const rs_sim* h) { return h->report.c_str(); }
+int rs_sim_n_blocks(const rs_sim* h) { return (int)h->blocks.size(); }
+const char* rs_sim_block_id(const rs_sim* h, int i) { return h->blocks[i].c_str(); }
+const char* rs_sim_block_kinds(const rs_sim* h, int i) { return h->block_kinds[i].c_str(); }
+int rs_sim_n_chains(const rs_sim* h) { return (int)h->chains.size(); }
+int rs_sim_chain(const rs_sim* h, int m, int32_t* out, int cap) {
+  const auto& c = h->chains[m];
+  for (size_t i = 0; i < c.size() && (int)i < cap; ++i) out[i] = c[i];
+  return (int)c.size();
+}
+int rs_sim_req_model(const rs_sim* h, int r) { return h->req_model[r]; }
+int rs_sim_n_batches(const rs_sim* h) { return (int)h->recs.size(); }
+// rec: [instance, block, phase, n_members]; members: (req, step, ctx) triples
+int rs_sim_batch(const rs_sim* h, int i, int32_t* rec, int32_t* members, int cap) {
+  rec[0] = std::get<0>(h->recs[i]);
+  rec[1] = std::get<1>(h->recs[i]);
+  rec[2] = std::get<2>(h->recs[i]);
+  const auto& m = h->members[i];
+  rec[3] = (int)m.size();
+  for (size_t j = 0; j < m.size() && (int)j < cap; ++j) {
+    members[3 * j] = std::get<0>(m[j]);
+    members[3 * j + 1] = std::get<1>(m[j]);
+    members[3 * j + 2] = std::get<2>(m[j]);
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+"""TEST INFRASTRUCTURE: Python handles over oracle/_ref/libblocksim_ref.so, i.e. the reference's
+own blocksim classes (compiled in place from /root/reference by oracle/Makefile). Only tests/
+use this, as the parity checker for paper_2404_18322_b200.host and the runner's batch traces.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from paper_2404_18322_b200 import host as H
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+REF_LIB = os.path.join(_HERE, "_ref", "libblocksim_ref.so")
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(REF_LIB)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(REF_LIB)
+        P, I, I64, D = C.c_void_p, C.c_int, C.c_int64, C.c_double
+        L.rs_cosine.restype = D
+        L.rs_cosine.argtypes = [P, I, P, I, C.POINTER(I)]
+        L.rs_plan_migration.restype = I
+        L.rs_plan_migration.argtypes = [I, I64, I64, C.POINTER(I64)]
+        L.rs_percentile.restype = I
+        L.rs_percentile.argtypes = [P, I, D, C.POINTER(D)]
+        L.rs_sim_run.restype = P
+        L.rs_sim_run.argtypes = [I, I, I, I, I, P, P, I, I64]
+        for n, r, a in [("rs_sim_free", None, [P]), ("rs_sim_error", C.c_char_p, [P]),
+                        ("rs_sim_report", C.c_char_p, [P]), ("rs_sim_n_blocks", I, [P]),
+                        ("rs_sim_block_id", C.c_char_p, [P, I]),
+                        ("rs_sim_block_kinds", C.c_char_p, [P, I]), ("rs_sim_n_chains", I, [P]),
+                        ("rs_sim_chain", I, [P, I, P, I]), ("rs_sim_req_model", I, [P, I]),
+                        ("rs_sim_n_batches", I, [P]), ("rs_sim_batch", I, [P, I, P, P, I])]:
+            fn = getattr(L, n)
+            fn.restype, fn.argtypes = r, a
+        _lib = L
+    return _lib
+
+
+class RefPool(H.Pool):
+    prefix = "rs_"
+
+    def __init__(self, n_blocks: int = 8, n_devices: int = 2):
+        L = lib()
+        H._bind("rs_", L)
+        super().__init__(_lib=L, _handle=L.rs_pool_new(n_blocks, n_devices))
+
+
+class RefKvStore(H.KvStore):
+    prefix = "rs_"
+
+    def __init__(self, n_devices: int = 2):
+        L = lib()
+        H._bind("rs_", L)
+        super().__init__(_lib=L, _handle=L.rs_kv_new(n_devices))
+
+
+def cosine(a, b) -> float:
+    import numpy as np
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    err = C.c_int(0)
+    v = lib().rs_cosine(a.ctypes.data, a.size, b.ctypes.data, b.size, C.byref(err))
+    if err.value:
+        raise ValueError("signature_similarity rejected its input")
+    return v
+
+
+def plan_migration(pages: int, rec_us: int, cp_us: int):
+    out = (C.c_int64 * 6)()
+    rc = lib().rs_plan_migration(pages, rec_us, cp_us, out)
+    if rc:
+        raise ValueError("plan_migration rejected its input")
+    return tuple(int(x) for x in out)
+
+
+def percentile(values, q: float) -> float:
+    import numpy as np
+    v = np.ascontiguousarray(values, np.float64)
+    out = C.c_double(0)
+    rc = lib().rs_percentile(v.ctypes.data, v.size, q, C.byref(out))
+    if rc:
+        raise ValueError("percentile rejected q")
+    return out.value
+
+
+def simulate(n_layers: int, dim: int, n_lora: int, first_adapted: int, prompts, outputs,
+             max_batch_tokens: int = 4096, arrival_gap_us: int = 0):
+    """Runs the reference Simulation; returns (blocks, kinds, chains, req_model, trace)."""
+    import numpy as np
+    p = np.ascontiguousarray(prompts, np.int32)
+    o = np.ascontiguousarray(outputs, np.int32)
+    L = lib()
+    h = L.rs_sim_run(n_layers, dim, n_lora, first_adapted, len(p), p.ctypes.data, o.ctypes.data,
+                     max_batch_tokens, arrival_gap_us)
+    try:
+        err = L.rs_sim_error(h).decode()
+        if err:
+            raise RuntimeError(err)
+        nb = L.rs_sim_n_blocks(h)
+        blocks = [L.rs_sim_block_id(h, i).decode() for i in range(nb)]
+        kinds = [L.rs_sim_block_kinds(h, i).decode() for i in range(nb)]
+        chains = []
+        buf = (C.c_int32 * 4096)()
+        for m in range(L.rs_sim_n_chains(h)):
+            n = L.rs_sim_chain(h, m, buf, 4096)
+            chains.append([int(buf[i]) for i in range(n)])
+        req_model = [L.rs_sim_req_model(h, r) for r in range(len(p))]
+        trace = []
+        rec = (C.c_int32 * 4)()
+        mem = (C.c_int32 * (3 * 65536))()
+        for i in range(L.rs_sim_n_batches(h)):
+            L.rs_sim_batch(h, i, rec, mem, 65536)
+            members = [(int(mem[3 * j]), int(mem[3 * j + 1]), int(mem[3 * j + 2]))
+                       for j in range(rec[3])]
+            trace.append((int(rec[0]), int(rec[1]), int(rec[2]), members))
+        return blocks, kinds, chains, req_model, trace
+    finally:
+        L.rs_sim_free(h)

@@ -31,7 +31,7 @@ class BlockDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
                 ("head_dim", C.c_int), ("d_ff", C.c_int), ("max_pos", C.c_int),
                 ("norm_eps", C.c_float), ("rope_theta", C.c_float), ("init_scale", C.c_float),
-                ("seed", C.c_uint64), ("name", C.c_char_p)]
+                ("seed", C.c_uint64), ("name", C.c_char_p), ("components", C.c_char_p)]
 
 
 class Token(C.Structure):

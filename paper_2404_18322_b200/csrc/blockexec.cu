@@ -77,9 +77,11 @@ struct be_block {
   size_t slab_elems = 0;
   float2* rope = nullptr;
   struct Layer {
-    bf16 *wqkv, *wo, *wgu, *wd;  // packed tile layout (ptx.cuh packed_index)
+    bf16 *wqkv, *wo, *wgu, *wd;  // packed tile layout (ptx.cuh packed_index); null if absent
   };
-  std::vector<Layer> layers;
+  std::vector<Layer> layers;  // l-th attention component uses wqkv/wo, l-th ffn wgu/wd
+  std::string comps;          // component sequence, 'a' attention / 'f' ffn
+  int n_att = 0, n_ffn = 0;
 };
 
 struct be_kv_pool {
@@ -256,7 +258,16 @@ extern "C" int be_synchronize(be_ctx* ctx) {
 extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out) {
   if (ctx == nullptr || d == nullptr || out == nullptr) return BE_ERR_INVALID;
   *out = nullptr;
-  if (d->n_layers <= 0 || d->d_model <= 0 || d->n_heads <= 0 || d->head_dim <= 0 ||
+  // component sequence: explicit ("a" attention, "f" ffn, zoo.hpp:12), else n_layers x "af"
+  std::string comps;
+  if (d->components != nullptr) {
+    comps = d->components;
+    for (char c : comps)
+      if (c != 'a' && c != 'f') return fail(ctx, BE_ERR_INVALID, "block: component kinds are 'a'/'f'");
+  } else {
+    for (int l = 0; l < d->n_layers; ++l) comps += "af";
+  }
+  if (comps.empty() || d->d_model <= 0 || d->n_heads <= 0 || d->head_dim <= 0 ||
       d->d_ff <= 0 || d->n_heads * d->head_dim != d->d_model)
     return fail(ctx, BE_ERR_INVALID, "block: inconsistent shape");
   if (d->d_model % 128 != 0 || d->d_ff % 64 != 0 || (2 * d->d_ff) % 128 != 0)
@@ -270,9 +281,14 @@ extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out
   b->desc = *d;
   b->name = d->name ? d->name : "block";
   b->desc.name = nullptr;
+  b->desc.components = nullptr;
+  b->comps = comps;
+  b->n_att = (int)std::count(comps.begin(), comps.end(), 'a');
+  b->n_ffn = (int)comps.size() - b->n_att;
+  b->desc.n_layers = std::max(b->n_att, b->n_ffn);
   const size_t D = d->d_model, F = d->d_ff;
-  const size_t per_layer = 3 * D * D + D * D + 2 * F * D + D * F;
-  b->slab_elems = per_layer * d->n_layers;
+  const size_t att_elems = 3 * D * D + D * D, ffn_elems = 2 * F * D + D * F;
+  b->slab_elems = att_elems * b->n_att + ffn_elems * b->n_ffn;
   if (cudaMalloc(&b->slab, b->slab_elems * sizeof(bf16)) != cudaSuccess) {
     delete b;
     return fail(ctx, BE_ERR_NOMEM, "block: weight slab (%zu B) allocation failed",
@@ -286,20 +302,32 @@ extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out
   cudaStream_t st = ctx->stream;
   bx::launch_rope_table(b->rope, d->max_pos, d->head_dim, (double)d->rope_theta, st);
   const float s = d->init_scale;
-  b->layers.resize(d->n_layers);
-  for (int l = 0; l < d->n_layers; ++l) {
-    auto& L = b->layers[l];
-    L.wqkv = b->slab + per_layer * l;
-    L.wo = L.wqkv + 3 * D * D;
-    L.wgu = L.wo + D * D;
-    L.wd = L.wgu + 2 * F * D;
-    auto key = [&](const char* t) { return stream_key(d->seed, weight_stream(b->name, l, t)); };
-    bx::launch_synth_weight(L.wqkv, (int)D, (int)D, key("wq"), 0, s, 1, d->head_dim, nullptr, st);
-    bx::launch_synth_weight(L.wqkv + D * D, (int)D, (int)D, key("wk"), 0, s, 1, d->head_dim, nullptr, st);
-    bx::launch_synth_weight(L.wqkv + 2 * D * D, (int)D, (int)D, key("wv"), 0, s, 0, d->head_dim, nullptr, st);
-    bx::launch_synth_weight(L.wo, (int)D, (int)D, key("wo"), 0, s, 0, d->head_dim, nullptr, st);
-    bx::launch_synth_weight(L.wgu, (int)(2 * F), (int)D, key("wg"), key("wu"), s, 2, d->head_dim, nullptr, st);
-    bx::launch_synth_weight(L.wd, (int)D, (int)F, key("wd"), 0, s, 0, d->head_dim, nullptr, st);
+  // weights in component order; the l-th attention (ffn) component is "layer" l of its kind
+  b->layers.assign(b->desc.n_layers, be_block::Layer{nullptr, nullptr, nullptr, nullptr});
+  bf16* cur = b->slab;
+  int ia = 0, jf = 0;
+  for (char c : comps) {
+    if (c == 'a') {
+      auto& L = b->layers[ia];
+      auto key = [&](const char* t) { return stream_key(d->seed, weight_stream(b->name, ia, t)); };
+      L.wqkv = cur;
+      L.wo = cur + 3 * D * D;
+      cur += att_elems;
+      bx::launch_synth_weight(L.wqkv, (int)D, (int)D, key("wq"), 0, s, 1, d->head_dim, nullptr, st);
+      bx::launch_synth_weight(L.wqkv + D * D, (int)D, (int)D, key("wk"), 0, s, 1, d->head_dim, nullptr, st);
+      bx::launch_synth_weight(L.wqkv + 2 * D * D, (int)D, (int)D, key("wv"), 0, s, 0, d->head_dim, nullptr, st);
+      bx::launch_synth_weight(L.wo, (int)D, (int)D, key("wo"), 0, s, 0, d->head_dim, nullptr, st);
+      ++ia;
+    } else {
+      auto& L = b->layers[jf];
+      auto key = [&](const char* t) { return stream_key(d->seed, weight_stream(b->name, jf, t)); };
+      L.wgu = cur;
+      L.wd = cur + 2 * F * D;
+      cur += ffn_elems;
+      bx::launch_synth_weight(L.wgu, (int)(2 * F), (int)D, key("wg"), key("wu"), s, 2, d->head_dim, nullptr, st);
+      bx::launch_synth_weight(L.wd, (int)D, (int)F, key("wd"), 0, s, 0, d->head_dim, nullptr, st);
+      ++jf;
+    }
   }
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
@@ -324,7 +352,7 @@ extern "C" int64_t be_block_param_bytes(const be_block* b) {
 }
 
 extern "C" int64_t be_block_kv_bytes_per_token(const be_block* b) {
-  return b ? 4LL * b->desc.d_model * b->desc.n_layers : 0;
+  return b ? 4LL * b->desc.d_model * b->n_att : 0;
 }
 
 extern "C" int be_block_read_weight(be_block* b, int layer, const char* tensor, float* host_out) {
@@ -334,6 +362,9 @@ extern "C" int be_block_read_weight(be_block* b, int layer, const char* tensor, 
   const int D = b->desc.d_model, F = b->desc.d_ff, hd = b->desc.head_dim;
   const auto& L = b->layers[layer];
   const std::string t = tensor;
+  const bool att_t = t == "wq" || t == "wk" || t == "wv" || t == "wo";
+  if ((att_t && L.wqkv == nullptr) || (!att_t && L.wgu == nullptr))
+    return fail(ctx, BE_ERR_INVALID, "block has no %s of component %d", tensor, layer);
   const bf16* src = nullptr;
   int rows = 0, cols = 0, perm = 0, parity = 0;
   if (t == "wq") { src = L.wqkv; rows = D; cols = D; perm = 1; }
@@ -370,17 +401,19 @@ extern "C" int be_kv_pool_create(be_ctx* ctx, const be_block* b, int n_pages, be
   auto* p = new be_kv_pool();
   p->ctx = ctx;
   p->n_pages = n_pages;
-  p->n_layers = b->desc.n_layers;
+  p->n_layers = b->n_att;  // one K/V plane pair per attention component of the block
   p->n_heads = b->desc.n_heads;
   p->head_dim = b->desc.head_dim;
   p->layer_elems = 2LL * p->n_heads * 16 * p->head_dim;
   p->page_elems = p->layer_elems * p->n_layers;
   const size_t bytes = (size_t)p->page_elems * n_pages * sizeof(bf16);
-  if (cudaMalloc(&p->base, bytes) != cudaSuccess) {
-    delete p;
-    return fail(ctx, BE_ERR_NOMEM, "kv pool: %zu B allocation failed", bytes);
+  if (bytes > 0) {  // ffn-only blocks keep no KV
+    if (cudaMalloc(&p->base, bytes) != cudaSuccess) {
+      delete p;
+      return fail(ctx, BE_ERR_NOMEM, "kv pool: %zu B allocation failed", bytes);
+    }
+    cudaMemsetAsync(p->base, 0, bytes, ctx->stream);
   }
-  cudaMemsetAsync(p->base, 0, bytes, ctx->stream);
   *out = p;
   return BE_OK;
 }
@@ -517,7 +550,7 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
   if (ws->d != d || ws->dff != F || ws->H != H)
     return fail(ctx, BE_ERR_INVALID, "workspace shape does not match block");
   if (ntok > ws->max_tok) return fail(ctx, BE_ERR_INVALID, "batch of %d tokens > workspace %d", ntok, ws->max_tok);
-  if (pool->n_layers != D.n_layers || pool->n_heads != H || pool->head_dim != hd)
+  if (pool->n_layers != blk->n_att || pool->n_heads != H || pool->head_dim != hd)
     return fail(ctx, BE_ERR_INVALID, "kv pool shape does not match block");
   if (ntok == 0) return BE_OK;
   const int* tok = reinterpret_cast<const int*>(d_tok);
@@ -533,9 +566,32 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
   if ((size_t)ntok * H * splits * (hd + 2) > ws->attn_part_elems && splits > 1)
     return fail(ctx, BE_ERR_INVALID, "attention partial buffer too small");
 
-  for (int l = 0; l < D.n_layers; ++l) {
-    const auto& L = blk->layers[l];
+  int ia = 0, jf = 0;
+  for (char kind : blk->comps) {
     int rc;
+    if (kind == 'f') {
+      // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
+      const auto& L = blk->layers[jf++];
+      e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
+      if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
+      EpiParams eg{};
+      eg.mode = bx::kSwiGLU;
+      eg.ntok = ntok;
+      eg.rstd = ws->rstd;
+      eg.out = ws->h;
+      eg.ldo = F;
+      if ((rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st)) != BE_OK) return rc;
+      EpiParams ed{};
+      ed.mode = bx::kResid;
+      ed.ntok = ntok;
+      ed.xres = ws->X;
+      ed.xres_b = ws->Xb;
+      ed.ldr = d;
+      if ((rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st)) != BE_OK) return rc;
+      continue;
+    }
+    const int l = ia++;
+    const auto& L = blk->layers[l];
     // ---- attention component: RMSNorm (fused) -> QKV + RoPE + KV append -> paged attn -> O + residual
     e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
     if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
@@ -582,24 +638,6 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eo.xres_b = ws->Xb;
     eo.ldr = d;
     if ((rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st)) != BE_OK) return rc;
-
-    // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
-    e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
-    if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
-    EpiParams eg{};
-    eg.mode = bx::kSwiGLU;
-    eg.ntok = ntok;
-    eg.rstd = ws->rstd;
-    eg.out = ws->h;
-    eg.ldo = F;
-    if ((rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st)) != BE_OK) return rc;
-    EpiParams ed{};
-    ed.mode = bx::kResid;
-    ed.ntok = ntok;
-    ed.xres = ws->X;
-    ed.xres_b = ws->Xb;
-    ed.ldr = d;
-    if ((rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st)) != BE_OK) return rc;
   }
   // K2: scatter the block outputs to their next-hop rows
   e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st);
@@ -662,7 +700,8 @@ extern "C" int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_to
                                       int pt_stride) {
   if (ctx == nullptr || blk == nullptr || n_tokens <= 0) return 0;
   const int splits = attn_splits(ctx, n_tokens, blk->desc.n_heads, pt_stride);
-  return 2 + blk->desc.n_layers * (7 + (splits > 1 ? 1 : 0));
+  // gather + scatter; attention: rms, qkv, attention (+combine), o; ffn: rms, gate/up, down
+  return 2 + blk->n_att * (4 + (splits > 1 ? 1 : 0)) + blk->n_ffn * 3;
 }
 
 // ------------------------------------------------------------------------------ row kernels

@@ -98,6 +98,10 @@ class Runner {
 
   be_ctx* ctx_;
   cudaStream_t st_;
+  bool dry_ = false;  // control plane only
+  std::vector<std::string> comps_;
+  std::vector<std::int64_t> kv_bpt_;  // per block
+  int n_created_ = 0;
   int mode_ = 0;
   bool use_graphs_ = false;
   int max_batch_tokens_ = 4096;
@@ -137,7 +141,9 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   if (w.n_blocks <= 0 || w.n_tenants <= 0 || w.n_requests <= 0 || !w.blocks || !w.chain_ptr ||
       !w.chain_blocks || !w.req_tenant || !w.req_prompt || !w.req_output)
     throw BeError(BE_ERR_INVALID, "runner: incomplete workload");
-  st_ = static_cast<cudaStream_t>(be_ctx_stream(ctx));
+  dry_ = w.dry_run != 0;
+  if (!dry_ && ctx == nullptr) throw BeError(BE_ERR_INVALID, "runner: no device context");
+  st_ = dry_ ? nullptr : static_cast<cudaStream_t>(be_ctx_stream(ctx));
   mode_ = w.mode;
   use_graphs_ = w.use_graphs != 0;
   max_batch_tokens_ = w.max_batch_tokens > 0 ? w.max_batch_tokens : 4096;
@@ -180,28 +186,44 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   }
   int dff = 0, H = 0;
   for (int b = 0; b < w.n_blocks; ++b) {
+    // component sequence -> KV bytes per token (4 * d per attention component,
+    // CostModel::kv_bytes_per_token, costmodel.cpp:114-127)
+    int n_att = 0;
+    if (w.blocks[b].components != nullptr) {
+      for (const char* c = w.blocks[b].components; *c; ++c) n_att += *c == 'a' ? 1 : 0;
+      comps_.push_back(w.blocks[b].components);
+    } else {
+      n_att = w.blocks[b].n_layers;
+      comps_.push_back(std::string());
+    }
+    kv_bpt_.push_back(4LL * d_ * n_att);
+    descs_[b].components = nullptr;  // re-pointed at comps_ when loading
     if (descs_[b].max_pos < max_ctx_) descs_[b].max_pos = max_ctx_ + 16;
-    be_block_desc d = descs_[b];
-    d.name = names_[b].c_str();
-    be_block* blk = nullptr;
-    int rc = be_block_load(ctx, &d, &blk);
-    if (rc != BE_OK) throw BeError(rc, std::string("block load: ") + be_last_error(ctx));
-    blocks_.push_back(blk);
-    be_kv_pool* kp = nullptr;
     const int np = static_cast<int>(std::max<long long>(1, pages_needed[b]));
-    rc = be_kv_pool_create(ctx, blk, np, &kp);
-    if (rc != BE_OK) throw BeError(rc, std::string("kv pool: ") + be_last_error(ctx));
-    pools_.push_back(kp);
-    kv_.attach_pool(names_[b], 0, np);
+    if (kv_bpt_[b] > 0) kv_.attach_pool(names_[b], 0, np);
     if (dff == 0) {
       dff = descs_[b].d_ff;
       H = descs_[b].n_heads;
     } else if (dff != descs_[b].d_ff || H != descs_[b].n_heads) {
       throw BeError(BE_ERR_INVALID, "runner: blocks differ in d_ff / heads");
     }
+    if (dry_) continue;
+    be_block_desc d = descs_[b];
+    d.name = names_[b].c_str();
+    d.components = comps_[b].empty() ? nullptr : comps_[b].c_str();
+    be_block* blk = nullptr;
+    int rc = be_block_load(ctx, &d, &blk);
+    if (rc != BE_OK) throw BeError(rc, std::string("block load: ") + be_last_error(ctx));
+    blocks_.push_back(blk);
+    be_kv_pool* kp = nullptr;
+    rc = be_kv_pool_create(ctx, blk, np, &kp);
+    if (rc != BE_OK) throw BeError(rc, std::string("kv pool: ") + be_last_error(ctx));
+    pools_.push_back(kp);
   }
   inst_of_block_.assign(w.n_blocks, "");
   inst_index_.assign(w.n_blocks, -1);
+  n_created_ = 0;
+  if (dry_) return;
   const int max_tok = std::max(std::min(poff, std::max(max_batch_tokens_, max_prompt)), w.n_requests);
   int rc = be_workspace_create(ctx, d_, dff, H, max_tok, w.n_requests, pages_for(max_ctx_) + 1, &ws_);
   if (rc != BE_OK) throw BeError(rc, std::string("workspace: ") + be_last_error(ctx));
@@ -239,9 +261,7 @@ std::string Runner::instance_for(int block) {
     // created on first dispatch, ready at once (parameters resident: no load time here)
     Instance& in = pool_.create(names_[block], 0, 0, 0);
     inst_of_block_[block] = in.id;
-    int created = 0;
-    for (int b : inst_index_) created += b >= 0 ? 1 : 0;
-    inst_index_[block] = created;
+    inst_index_[block] = n_created_++;
   }
   return inst_of_block_[block];
 }
@@ -274,11 +294,18 @@ PlannedBatch Runner::plan(const std::string& inst_id, const Batch& b) {
     const Entry& e = b.members[m];
     Request& r = reqs_[e.request_id - 1];
     const std::string& bn = names_[block];
-    const int have = kv_.tokens(r.id, bn);
-    const int first = b.phase == Phase::kPrefill ? 0 : have;
+    // the decode token sits at position context - 1 (the segment holds the tokens before it)
+    const int first = b.phase == Phase::kPrefill ? 0 : r.ctx - 1;
     const int count = b.phase == Phase::kPrefill ? r.prompt : 1;
-    const std::vector<int> row = kv_.reserve_slots(r.id, bn, bn, 0, pages_for(first + count));
-    std::copy(row.begin(), row.end(), pb.pt.begin() + (size_t)m * pb.stride);
+    std::vector<int> row;
+    if (kv_bpt_[block] > 0) {
+      if (b.phase == Phase::kDecode && kv_.tokens(r.id, bn) != first)
+        throw BeError(BE_ERR_STATE, "runner: kv segment out of step with the context");
+      row = kv_.reserve_slots(r.id, bn, bn, 0, pages_for(first + count));
+      std::copy(row.begin(), row.end(), pb.pt.begin() + (size_t)m * pb.stride);
+    } else {
+      row.assign(pages_for(first + count), 0);  // ffn-only block: no KV is written or read
+    }
     for (int i = 0; i < count; ++i) {
       const int pos = first + i;
       be_token t;
@@ -308,6 +335,7 @@ void Runner::launch(const PlannedBatch& pb, const be_token* d_tok, const int32_t
 }
 
 void Runner::execute_direct(const PlannedBatch& pb) {
+  if (dry_) return;
   void* arena = pb.phase == Phase::kPrefill ? parena_ : arena_;
   const int rc = be_exec_batch(ctx_, blocks_[pb.block], pools_[pb.block], ws_,
                                pb.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE,
@@ -335,15 +363,20 @@ void Runner::record(const PlannedBatch& pb, const Batch& b) {
 
 void Runner::account(const PlannedBatch& pb) {
   const be_block_desc& D = descs_[pb.block];
-  const double d = D.d_model, F = D.d_ff, L = D.n_layers;
+  const double d = D.d_model, F = D.d_ff;
+  const double La = static_cast<double>(kv_bpt_[pb.block]) / (4.0 * d);  // attention components
+  const std::string& cs = comps_[pb.block];
+  const double Lf = cs.empty() ? D.n_layers : static_cast<double>(cs.size()) - La;
   const double n = static_cast<double>(pb.toks.size());
-  stats.weight_bytes += (double)be_block_param_bytes(blocks_[pb.block]);
+  stats.weight_bytes += 2.0 * (La * 4.0 * d * d + Lf * 3.0 * d * F);
   double ctx_sum = 0.0;
   for (const auto& t : pb.toks) ctx_sum += t.pos + 1;
-  stats.kv_bytes += ctx_sum * L * 2.0 * d * 2.0;
+  stats.kv_bytes += ctx_sum * La * 2.0 * d * 2.0;
   stats.act_bytes += 2.0 * n * d * 2.0;
-  stats.flops += 2.0 * n * L * (4.0 * d * d + 3.0 * d * F) + 4.0 * ctx_sum * d * L;
-  stats.launches += be_exec_batch_launches(ctx_, blocks_[pb.block], static_cast<int>(pb.toks.size()), pb.stride);
+  stats.flops += 2.0 * n * (La * 4.0 * d * d + Lf * 3.0 * d * F) + 4.0 * ctx_sum * d * La;
+  if (!dry_)
+    stats.launches += be_exec_batch_launches(ctx_, blocks_[pb.block],
+                                             static_cast<int>(pb.toks.size()), pb.stride);
 }
 
 void Runner::pump() {
@@ -371,9 +404,10 @@ void Runner::finish_running() {
 
 void Runner::advance_after_step(Request& r, int step) {
   if (r.phase == Phase::kPrefill) {
-    const std::string& bn = names_[chain_block(r, step)];
-    if (!kv_.has_segment(r.id, bn)) {
-      kv_.create_segment(r.id, bn, 0, be_block_kv_bytes_per_token(blocks_[chain_block(r, step)]));
+    const int block = chain_block(r, step);
+    const std::string& bn = names_[block];
+    if (kv_bpt_[block] > 0 && !kv_.has_segment(r.id, bn)) {
+      kv_.create_segment(r.id, bn, 0, kv_bpt_[block]);
       kv_.append_tokens(r.id, bn, r.prompt);
     }
   }
@@ -388,10 +422,11 @@ void Runner::advance_from(Request& r, int step) {
   }
   if (r.phase == Phase::kPrefill) {
     // first token: the last prompt row's output becomes the first decode input
-    ck(cudaMemcpyAsync(static_cast<char*>(arena_) + (size_t)r.idx * d_ * 2,
-                       static_cast<char*>(parena_) + (size_t)(r.poff + r.prompt - 1) * d_ * 2,
-                       (size_t)d_ * 2, cudaMemcpyDeviceToDevice, st_),
-       "first token row");
+    if (!dry_)
+      ck(cudaMemcpyAsync(static_cast<char*>(arena_) + (size_t)r.idx * d_ * 2,
+                         static_cast<char*>(parena_) + (size_t)(r.poff + r.prompt - 1) * d_ * 2,
+                         (size_t)d_ * 2, cudaMemcpyDeviceToDevice, st_),
+         "first token row");
     r.generated = 1;
     ++tokens_generated_;
     r.ctx = r.prompt + 1;
@@ -439,7 +474,7 @@ void Runner::run(int max_batches) {
     finish_running();
     ++n;
   }
-  ck(cudaStreamSynchronize(st_), "run");
+  if (!dry_) ck(cudaStreamSynchronize(st_), "run");
   if (mode_ == 1 && !has_running_) {
     // lockstep: decode starts for everyone together, in request order
     step_done_order_.clear();
@@ -471,7 +506,7 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches) {
       i = j;
     }
   };
-  if (host_in != nullptr) copy_rows(true, const_cast<void*>(host_in));
+  if (host_in != nullptr && !dry_) copy_rows(true, const_cast<void*>(host_in));
   for (int idx : order) dispatch(reqs_[idx]);
   // plan the whole step on the host (bookkeeping does not depend on GPU results)
   std::vector<PlannedBatch> plans;
@@ -489,6 +524,7 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches) {
     for (const auto& m : running_.members) advance_after_step(reqs_[m.request_id - 1], m.chain_step);
   }
   if (n_batches) *n_batches = static_cast<int>(plans.size());
+  if (dry_) return;
   // metadata layout: per batch [tokens][page table], 256-byte aligned
   std::vector<size_t> off_tok(plans.size()), off_pt(plans.size());
   size_t total = 0;
@@ -589,7 +625,7 @@ int guard(bh_runner* h, F&& f) {
 }  // namespace
 
 extern "C" int bh_runner_create(be_ctx* ctx, const bh_workload* w, bh_runner** out) {
-  if (ctx == nullptr || w == nullptr || out == nullptr) return BE_ERR_INVALID;
+  if (w == nullptr || out == nullptr || (ctx == nullptr && !w->dry_run)) return BE_ERR_INVALID;
   *out = nullptr;
   auto* h = new bh_runner();
   const int rc = guard(h, [&] { h->r = std::make_unique<bh::Runner>(ctx, *w); });

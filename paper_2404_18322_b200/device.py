@@ -26,20 +26,29 @@ class BlockShape:
     norm_eps: float = 1e-5
     rope_theta: float = 10000.0
     init_scale: float = 0.02 * 3 ** 0.5  # uniform with std 0.02
+    components: str | None = None  # 'a'/'f' sequence (zoo components); None = n_layers x "af"
 
     @property
     def head_dim(self) -> int:
         return self.d_model // self.n_heads
 
     @property
+    def comps(self) -> str:
+        return self.components if self.components is not None else "af" * self.n_layers
+
+    @property
+    def n_attention(self) -> int:
+        return self.comps.count("a")
+
+    @property
     def kv_bytes_per_token(self) -> int:
         # CostModel::kv_bytes_per_token: 4 * embed_dim per attention component (costmodel.cpp:114-127)
-        return 4 * self.d_model * self.n_layers
+        return 4 * self.d_model * self.n_attention
 
     @property
     def param_bytes(self) -> int:
         d, f = self.d_model, self.d_ff
-        return 2 * self.n_layers * (4 * d * d + 3 * d * f)
+        return 2 * (self.comps.count("a") * 4 * d * d + self.comps.count("f") * 3 * d * f)
 
 
 def _ptr(t) -> C.c_void_p:
@@ -84,9 +93,10 @@ class Block:
     def __init__(self, ctx: Context, shape: BlockShape, name: str, seed: int = 1):
         self.ctx, self.shape, self.name, self.seed = ctx, shape, name, seed
         self._name_b = name.encode()
+        self._comps_b = shape.comps.encode()
         desc = BlockDesc(shape.n_layers, shape.d_model, shape.n_heads, shape.head_dim, shape.d_ff,
                          shape.max_pos, shape.norm_eps, shape.rope_theta, shape.init_scale, seed,
-                         self._name_b)
+                         self._name_b, self._comps_b)
         h = C.c_void_p()
         check(lib().be_block_load(ctx.h, C.byref(desc), C.byref(h)), ctx.h)
         self.h = h

@@ -27,7 +27,7 @@ class WorkloadC(C.Structure):
                 ("n_requests", C.c_int), ("req_tenant", C.c_void_p),
                 ("req_prompt", C.c_void_p), ("req_output", C.c_void_p),
                 ("max_batch_tokens", C.c_int), ("mode", C.c_int), ("use_graphs", C.c_int),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("dry_run", C.c_int)]
 
 
 _bound = False
@@ -64,15 +64,20 @@ class Runner:
     mode 1: lockstep (all prompts prefilled, then decode one token for everyone per step).
     """
 
-    def __init__(self, ctx: Context, wl: Workload, mode: int = 1, use_graphs: bool = True):
+    def __init__(self, ctx: Context | None, wl: Workload, mode: int = 1, use_graphs: bool = True,
+                 dry_run: bool = False):
+        """ctx None with dry_run=True runs the control plane alone (no GPU work)."""
         _bind()
         self.ctx, self.wl = ctx, wl
         s = wl.shape
         self._names = [n.encode() for n in wl.block_names]
+        comps = wl.block_comps or [s.comps] * len(wl.block_names)
+        self._comps = [c.encode() for c in comps]
         descs = (BlockDesc * len(wl.block_names))()
         for i, nm in enumerate(self._names):
             descs[i] = BlockDesc(s.n_layers, s.d_model, s.n_heads, s.head_dim, s.d_ff, s.max_pos,
-                                 s.norm_eps, s.rope_theta, s.init_scale, wl.seed, nm)
+                                 s.norm_eps, s.rope_theta, s.init_scale, wl.seed, nm,
+                                 self._comps[i])
         ptr = np.zeros(len(wl.chains) + 1, np.int32)
         flat = []
         for t, ch in enumerate(wl.chains):
@@ -85,12 +90,12 @@ class Runner:
         w = WorkloadC(len(wl.block_names), C.cast(descs, C.c_void_p), len(wl.chains),
                       k[1].ctypes.data, k[2].ctypes.data, wl.n_requests, k[3].ctypes.data,
                       k[4].ctypes.data, k[5].ctypes.data, wl.max_batch_tokens, mode,
-                      1 if use_graphs else 0, wl.seed)
+                      1 if use_graphs else 0, wl.seed, 1 if dry_run else 0)
         h = C.c_void_p()
-        rc = lib().bh_runner_create(ctx.h, C.byref(w), C.byref(h))
+        rc = lib().bh_runner_create(ctx.h if ctx is not None else None, C.byref(w), C.byref(h))
         if rc != 0:
-            raise BlockExecError(rc, "bh_runner_create failed (see stderr): "
-                                 + lib().be_last_error(ctx.h).decode())
+            msg = lib().be_last_error(ctx.h).decode() if ctx is not None else ""
+            raise BlockExecError(rc, "bh_runner_create failed (see stderr): " + msg)
         self.h = h
 
     def _check(self, rc):

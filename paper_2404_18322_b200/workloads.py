@@ -24,6 +24,7 @@ class Workload:
     max_batch_tokens: int = 4096      # configs/base.json:27
     seed: int = 1
     notes: dict = field(default_factory=dict)
+    block_comps: list[str] | None = None  # per block 'a'/'f' component sequence (zoo blocks)
 
     @property
     def n_requests(self) -> int:
