@@ -293,92 +293,76 @@ __global__ void __launch_bounds__(192, CTAS)
           epilogue_chunk<MODE>(E, f, n0 + c0, acc);
         }
       } else {
-        // partial tile: publish, last contributor reduces and runs the epilogue
+        // Partial tile. Its owner is the CTA holding the tile's first k-block (c_first): for
+        // that CTA the tile is its LAST segment, so it finishes last. Every other contributor
+        // holds the tile as its FIRST (or only) segment: it writes its partial to its single
+        // slot and releases one count on the tile's counter, usually long before the owner
+        // gets there. The owner never writes its own partial: it acquires the counter (all
+        // contributors are resident: grid <= #SMs, one CTA per SM), reads the partials with
+        // every load in flight and runs the epilogue. Sum order is contributor order.
         const long long tile_it0 = (long long)tile * nkb;
         const int c_first = R.cta_of(tile_it0);
         const int c_last = R.cta_of(tile_it0 + nkb - 1);
         const int n_contrib = c_last - c_first + 1;
-        const int me = (int)blockIdx.x - c_first;
-        // a CTA owns two partial slots: its first segment (range starts inside the tile) and
-        // its last one; a tile's contributors are the CTAs c_first..c_last
-        auto slot_of = [&](int c) {
-          const int which = R.begin(c) >= tile_it0 ? 0 : 1;
-          return E.ws + ((size_t)(c * 2 + which) * BN) * kBM;
-        };
-        // partial layout [feature][BN]: each thread moves its 16-column chunks as float4s
-        const size_t frow = (size_t)(q * 32 + lane) * BN;
-        float4* slot = reinterpret_cast<float4*>(slot_of(blockIdx.x) + frow);
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          if (n0 + c0 >= E.ntok) break;
-          float acc[16];
-          tmem_ld16(t_lane + c0, acc);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            __stcg(slot + (c0 >> 2) + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
-        }
-        // Hand-off without sequentially-consistent fences (MEMBAR.SC.GPU stalls for µs while
-        // HBM is saturated): the CTA barrier orders the 128 threads' partial stores before one
-        // acq_rel atomic at GPU scope (release is cumulative); the last arriver's acquire
-        // orders the other contributors' partials before its L2 (.cg) loads.
-        named_bar_sync(1, 128);
-        if (warp == 2 && lane == 0) {
-          int* ctr = E.counters + tile;
-          int prev;
-          asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
-          const int last = prev == n_contrib - 1;
-          if (last) *ctr = 0;  // self-reset for the next launch / graph replay
-          *flag = last;
-        }
-        __syncwarp();
-        named_bar_sync(1, 128);
-        if (*flag) {
+        const size_t frow = (size_t)(q * 32 + lane) * BN;  // partial layout [feature][BN]
+        int* ctr = E.counters + tile;
+        if ((int)blockIdx.x != c_first) {
+          float4* slot = reinterpret_cast<float4*>(E.ws + (size_t)blockIdx.x * BN * kBM + frow);
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             if (n0 + c0 >= E.ntok) break;
-            float own[16], acc[16];
-            tmem_ld16(t_lane + c0, own);
+            float acc[16];
+            tmem_ld16(t_lane + c0, acc);
 #pragma unroll
-            for (int i2 = 0; i2 < 16; ++i2) acc[i2] = 0.f;
-            // contributors summed in a fixed order (deterministic whoever arrives last); loads
-            // of four contributors are in flight together
-            for (int o0 = 0; o0 < n_contrib; o0 += 4) {
+            for (int j = 0; j < 4; ++j)
+              __stcg(slot + (c0 >> 2) + j,
+                     make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
+          }
+          // the CTA barrier orders the 128 threads' stores before one release at GPU scope
+          // (release is cumulative; no sequentially-consistent fence on the hot path)
+          named_bar_sync(1, 128);
+          if (warp == 2 && lane == 0)
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
+        } else {
+          if (warp == 2 && lane == 0) {
+            int seen = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+            } while (seen < n_contrib - 1);
+            *ctr = 0;  // reset for the next launch / graph replay (ordered by kernel boundary)
+          }
+          __syncwarp();
+          named_bar_sync(1, 128);  // everyone's loads are ordered after the acquire
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            if (n0 + c0 >= E.ntok) break;
+            float acc[16];
+            tmem_ld16(t_lane + c0, acc);  // the owner's share is contributor 0
+            for (int o0 = 1; o0 < n_contrib; o0 += 4) {
               float4 v[4][4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const int o = o0 + j;
-                if (o < n_contrib && o != me) {
-                  const float4* p =
-                      reinterpret_cast<const float4*>(slot_of(c_first + o) + frow) + (c0 >> 2);
+                const float4* p = reinterpret_cast<const float4*>(
+                                      E.ws + (size_t)(c_first + o) * BN * kBM + frow) + (c0 >> 2);
 #pragma unroll
-                  for (int k = 0; k < 4; ++k) v[j][k] = __ldcg(p + k);
-                } else {
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) v[j][k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
+                for (int k = 0; k < 4; ++k)
+                  v[j][k] = o < n_contrib ? __ldcg(p + k) : make_float4(0.f, 0.f, 0.f, 0.f);
               }
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const int o = o0 + j;
-                if (o >= n_contrib) break;
-                if (o == me) {
 #pragma unroll
-                  for (int i2 = 0; i2 < 16; ++i2) acc[i2] += own[i2];
-                } else {
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) {
-                    acc[4 * k] += v[j][k].x;
-                    acc[4 * k + 1] += v[j][k].y;
-                    acc[4 * k + 2] += v[j][k].z;
-                    acc[4 * k + 3] += v[j][k].w;
-                  }
+                for (int k = 0; k < 4; ++k) {
+                  acc[4 * k] += v[j][k].x;
+                  acc[4 * k + 1] += v[j][k].y;
+                  acc[4 * k + 2] += v[j][k].z;
+                  acc[4 * k + 3] += v[j][k].w;
                 }
               }
             }
             epilogue_chunk<MODE>(E, f, n0 + c0, acc);
           }
         }
-        named_bar_sync(1, 128);  // flag is reused by the next partial tile
       }
       tc_fence_before();
       __syncwarp();
@@ -465,12 +449,12 @@ GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems,
   long long g = num_sms;
   if (grid_cap > 0 && g > grid_cap) g = grid_cap;
   if (g > total / 4) g = total / 4 > 0 ? total / 4 : 1;
-  // partial-tile slots: two per CTA (its first and its last segment)
-  while (g > 1 && (size_t)g * 2 * bn * kBM > ws_elems) g /= 2;
+  // partial-tile slots: one per CTA (its first segment; owners never publish theirs)
+  while (g > 1 && (size_t)g * bn * kBM > ws_elems) g /= 2;
   (void)n_counters;
   p.grid = (int)g;
-  p.max_contrib = 2;
-  p.ws_needed = (size_t)g * 2 * bn * kBM;
+  p.max_contrib = 1;
+  p.ws_needed = (size_t)g * bn * kBM;
   p.tiles = tiles;
   return p;
 }
