@@ -808,8 +808,20 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < p.grid; ++c) t0 = h[c * 8] && h[c * 8] < t0 ? h[c * 8] : t0;
     const char* names[8] = {"entry", "setup", "pdl_wait", "last_load", "last_tfull", "epi_done",
-                            "first_tfull", "exit"};
+                            "role", "exit"};
     fprintf(stderr, "gemm trace N=%d K=%d ntok=%d grid=%d\n", N, K, ntok, p.grid);
+    // the five slowest final epilogues: role 1000000+n = owner of an n-way partial tile,
+    // 2000000 = non-owner contributor, 0 = full tile
+    std::vector<int> order(p.grid);
+    for (int c = 0; c < p.grid; ++c) order[c] = c;
+    std::sort(order.begin(), order.end(), [&](int a, int b2) { return h[a * 8 + 5] > h[b2 * 8 + 5]; });
+    for (int i = 0; i < 5 && i < p.grid; ++i) {
+      const int c = order[i];
+      fprintf(stderr, "  slow cta %3d: last_tfull %.2f epi_done %.2f role %llu\n", c,
+              (h[c * 8 + 4] - t0) / 1e3, (h[c * 8 + 5] - t0) / 1e3,
+              (unsigned long long)h[c * 8 + 6]);
+    }
+    for (int c = 0; c < p.grid; ++c) h[c * 8 + 6] = 0;
     for (int k = 0; k < 8; ++k) {
       std::vector<double> v;
       for (int c = 0; c < p.grid; ++c)

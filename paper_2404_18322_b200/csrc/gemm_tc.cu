@@ -280,7 +280,6 @@ __global__ void __launch_bounds__(192, CTAS)
       const uint32_t u = (uint32_t)(seg >> 1);
       mbar_wait(&tfull[a], u & 1u);
       tc_fence_after();
-      if (seg == 0 && warp == 2 && lane == 0) stamp(E, 6);
       if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
       __syncwarp();
       const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
@@ -306,6 +305,8 @@ __global__ void __launch_bounds__(192, CTAS)
         const int n_contrib = c_last - c_first + 1;
         const size_t frow = (size_t)(q * 32 + lane) * BN;  // partial layout [feature][BN]
         int* ctr = E.counters + tile;
+        if (E.trace != nullptr && warp == 2 && lane == 0)  // diagnostics: last segment's role
+          E.trace[blockIdx.x * 8 + 6] = (int)blockIdx.x == c_first ? 1000000 + n_contrib : 2000000;
         if ((int)blockIdx.x != c_first) {
           float4* slot = reinterpret_cast<float4*>(E.ws + (size_t)blockIdx.x * BN * kBM + frow);
 #pragma unroll 1
