@@ -446,9 +446,25 @@ GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems,
   const long long tiles = (long long)m_tiles * n_tiles;
   const int nkb = K / kBK;
   const long long total = tiles * nkb;
-  // grid: one CTA per SM, at least 4 k-blocks per CTA
-  long long g = num_sms;
-  if (grid_cap > 0 && g > grid_cap) g = grid_cap;
+  // Grid. A deep ring keeps ~190 KB in flight per SM (~100 GB/s per SM measured), so about
+  // half the SMs already saturate HBM (kMinStreamCtas); partial tiles cost a serial fixup at the
+  // end of the kernel. Prefer whole tiles per CTA when the tile count allows, else the fewest
+  // splits per tile that still reach kMinStreamCtas; large prefill grids use every SM.
+  static const int kMinStreamCtas = [] {
+    const char* e = getenv("BE_GEMM_GMIN");
+    return e ? atoi(e) : 74;
+  }();
+  const long long sms = grid_cap > 0 && grid_cap < num_sms ? grid_cap : num_sms;
+  long long g = sms;
+  if (tiles >= sms) {
+    const long long k = (tiles + sms - 1) / sms;  // whole tiles per CTA
+    if (tiles % k == 0 && tiles / k >= kMinStreamCtas) g = tiles / k;
+  } else if (tiles >= kMinStreamCtas) {
+    g = tiles;  // one whole tile per CTA
+  } else {
+    const long long s = (kMinStreamCtas + tiles - 1) / tiles;  // even k-splits per tile
+    g = tiles * s < sms ? tiles * s : sms;
+  }
   if (g > total / 4) g = total / 4 > 0 ? total / 4 : 1;
   // partial-tile slots: one per CTA (its first segment; owners never publish theirs)
   while (g > 1 && (size_t)g * bn * kBM > ws_elems) g /= 2;
