@@ -446,13 +446,13 @@ GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems,
   const long long tiles = (long long)m_tiles * n_tiles;
   const int nkb = K / kBK;
   const long long total = tiles * nkb;
-  // Grid. A deep ring keeps ~190 KB in flight per SM (~100 GB/s per SM measured), so about
-  // half the SMs already saturate HBM (kMinStreamCtas); partial tiles cost a serial fixup at the
-  // end of the kernel. Prefer whole tiles per CTA when the tile count allows, else the fewest
-  // splits per tile that still reach kMinStreamCtas; large prefill grids use every SM.
+  // Grid. Partial tiles cost a serial fixup at the end of the kernel, so prefer whole tiles per
+  // CTA when the tile count allows, else the fewest even splits per tile that still put
+  // kMinStreamCtas CTAs on the weight stream (measured sweep, profiles/r01_gemm_sweep_gmin.log:
+  // 120 is best; ~86 CTAs do not saturate HBM through this pipeline); prefill uses every SM.
   static const int kMinStreamCtas = [] {
     const char* e = getenv("BE_GEMM_GMIN");
-    return e ? atoi(e) : 74;
+    return e ? atoi(e) : 120;
   }();
   const long long sms = grid_cap > 0 && grid_cap < num_sms ? grid_cap : num_sms;
   long long g = sms;

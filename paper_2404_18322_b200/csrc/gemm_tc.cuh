@@ -66,8 +66,9 @@ __host__ __device__ constexpr int gemm_stages() {
 }
 template <int BN>
 __host__ __device__ constexpr int gemm_stages_deep() {
-  const int s = (200 * 1024) / GemmSmem<BN>::kStageBytes;
-  return s > 8 ? 8 : s;
+  // ~216 KB of ring (+ alignment and barriers stays under the 227 KB per-CTA limit)
+  const int s = (216 * 1024) / GemmSmem<BN>::kStageBytes;
+  return s > 12 ? 12 : s;
 }
 template <int BN>
 __host__ __device__ constexpr int gemm_ctas_per_sm() {
