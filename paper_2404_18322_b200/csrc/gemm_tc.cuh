@@ -66,9 +66,9 @@ __host__ __device__ constexpr int gemm_stages() {
 }
 template <int BN>
 __host__ __device__ constexpr int gemm_stages_deep() {
-  // ~216 KB of ring (+ alignment and barriers stays under the 227 KB per-CTA limit)
-  const int s = (216 * 1024) / GemmSmem<BN>::kStageBytes;
-  return s > 12 ? 12 : s;
+  // up to 8 stages / ~200 KB; deeper rings (12 x 18-24 KB) measured slower on every shape
+  const int s = (200 * 1024) / GemmSmem<BN>::kStageBytes;
+  return s > 8 ? 8 : s;
 }
 template <int BN>
 __host__ __device__ constexpr int gemm_ctas_per_sm() {
