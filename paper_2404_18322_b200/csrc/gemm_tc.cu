@@ -334,6 +334,32 @@ __global__ void __launch_bounds__(192, CTAS)
           }
           __syncwarp();
           named_bar_sync(1, 128);  // everyone's loads are ordered after the acquire
+          if constexpr (BN <= 64) {
+            // whole tile in registers: one L2 round trip per contributor, not one per chunk
+            float acc[BN];
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 16)
+              tmem_ld16(t_lane + c0, *reinterpret_cast<float(*)[16]>(acc + c0));
+            for (int o = 1; o < n_contrib; ++o) {
+              const float4* p = reinterpret_cast<const float4*>(
+                  E.ws + (size_t)(c_first + o) * BN * kBM + frow);
+              float4 v[BN / 4];
+#pragma unroll
+              for (int k = 0; k < BN / 4; ++k) v[k] = __ldcg(p + k);
+#pragma unroll
+              for (int k = 0; k < BN / 4; ++k) {
+                acc[4 * k] += v[k].x;
+                acc[4 * k + 1] += v[k].y;
+                acc[4 * k + 2] += v[k].z;
+                acc[4 * k + 3] += v[k].w;
+              }
+            }
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              if (n0 + c0 >= E.ntok) break;
+              epilogue_chunk<MODE>(E, f, n0 + c0, *reinterpret_cast<float(*)[16]>(acc + c0));
+            }
+          } else {
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             if (n0 + c0 >= E.ntok) break;
@@ -362,6 +388,7 @@ __global__ void __launch_bounds__(192, CTAS)
               }
             }
             epilogue_chunk<MODE>(E, f, n0 + c0, acc);
+          }
           }
         }
       }
