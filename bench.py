@@ -225,6 +225,81 @@ def kernel_rooflines(ctx, wl, peaks):
     return res
 
 
+def run_pipeline(args, world, rank, local):
+    """N > 1 with block placement: chain positions placed as pipeline stages over the GPUs,
+    N micro-batches in flight, activation hops by NCCL P2P (paper_2404_18322_b200/pipeline.py)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2404_18322_b200.device import Context
+    from paper_2404_18322_b200.pipeline import PipelineStage, ticks_needed, \
+        tokens_per_request_needed
+    from paper_2404_18322_b200.workloads import CONFIGS
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peaks_kind = load_peaks()
+    total = ticks_needed(world, args.steps, args.warmup)
+    need = tokens_per_request_needed(world, total, world) + 1
+    out = max(args.output, need)
+    wl = CONFIGS[args.config](prompt=args.prompt, output=out) if args.config != "c1" \
+        else CONFIGS["c1"](output=out)
+    ctx = Context(local)
+    stage = PipelineStage(ctx, wl, world, rank)
+    t0 = time.time()
+    stage.prefill()
+    prefill_s = time.time() - t0
+    warm = args.warmup + world  # fill the pipeline
+    for t in range(warm):
+        stage.tick(t, total)
+    ctx.sync()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stage.stream)
+    before = stage.stats.finished
+    for t in range(warm, warm + args.steps):
+        stage.tick(t, total)
+    e1.record(stage.stream)
+    ctx.sync()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    tm = torch.tensor([ms], device="cuda")
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm.item())
+    fin = torch.tensor([stage.stats.finished - before], device="cuda", dtype=torch.float64)
+    dist.all_reduce(fin, op=dist.ReduceOp.SUM)  # only the last stage counts tokens
+    tokens = float(fin.item())
+    stats = stage.run.step_stats()
+    if rank == 0:
+        line = {
+            "metric": "block-chain decode tokens/s", "value": round(tokens / (ms / 1e3), 2),
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": warm,
+            "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, synthetic prompts; greedy feedback)",
+            "config": {"workload": wl.name, "tenants": len(wl.chains),
+                       "global_batch": wl.n_requests * world, "prompt": wl.req_prompt[0],
+                       "decode": wl.req_output[0],
+                       "parallelism": f"block placement: {world} pipeline stages over chain "
+                                      f"positions {stage.stages}, {world} micro-batches of "
+                                      f"{wl.n_requests}, NCCL P2P hops",
+                       "stage_cost_bytes": [round(c) for c in stage.stage_costs],
+                       "l2": "inputs larger than L2"},
+            "roofline": None, "e2e": None, "cpu_baseline": None,
+            "gpu_launches": int(stats["launches"]) * args.steps, "clocks": clk,
+            "prefill_s": round(prefill_s, 2),
+            "note": "one step = one pipeline tick = one micro-batch token leaving the last stage",
+        }
+        print(json.dumps(line), flush=True)
+    stage.close()
+    ctx.close()
+    dist.destroy_process_group()
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
@@ -232,6 +307,8 @@ def run_ours(args, world, rank, local):
     from paper_2404_18322_b200.runner import Runner
     from paper_2404_18322_b200.workloads import CONFIGS
 
+    if world > 1 and args.placement == "pipeline":
+        return run_pipeline(args, world, rank, local)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -411,6 +488,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--placement", default="pipeline", choices=["pipeline", "replica"],
+                    help="N>1: block placement as pipeline stages with NCCL P2P hops, or one "
+                         "independent replica of the workload per GPU")
     ap.add_argument("--profile", action="store_true",
                     help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
     args = ap.parse_args()

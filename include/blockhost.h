@@ -119,6 +119,11 @@ int bh_runner_run(bh_runner* r, int max_batches);
  * host_out optional pinned or pageable [n_live][d] bf16 rows (request order) copied in before
  * and out after the step; *n_batches receives the batches executed. */
 int bh_runner_decode_step(bh_runner* r, const void* host_in, void* host_out, int* n_batches);
+/* Lockstep decode of one request group (a pipeline micro-batch): only requests reqs[0..n) step;
+ * host_in/host_out rows are the group's live requests in request order. Each group keeps its
+ * own CUDA graph. */
+int bh_runner_decode_group(bh_runner* r, int group, const int32_t* reqs, int n,
+                           const void* host_in, void* host_out, int* n_batches);
 int bh_runner_live_requests(const bh_runner* r);
 int64_t bh_runner_tokens_generated(const bh_runner* r);
 /* Batch trace since creation. members: request ids, steps, context tokens (may be NULL). */
@@ -128,6 +133,9 @@ int bh_runner_trace(const bh_runner* r, bh_batch_rec* recs, int cap, int* n_out,
 int bh_runner_clear_trace(bh_runner* r);
 /* Device pointer of the decode activation arena ([n_requests][d] bf16, row = request). */
 void* bh_runner_arena(bh_runner* r);
+/* Device pointer of the prefill arena ([sum of prompts][d] bf16, requests in order) and its
+ * row count; a pipeline stage receives its prompts' hidden states here before bh_runner_run. */
+void* bh_runner_prefill_arena(bh_runner* r, int64_t* rows);
 /* Per-step accounting of the last decode step for roofline reporting. */
 typedef struct {
   double weight_bytes;   /* bytes of block weights streamed */

@@ -71,10 +71,14 @@ class Runner {
   Runner(be_ctx* ctx, const bh_workload& w);
   ~Runner();
   void run(int max_batches);
-  void decode_step(const void* host_in, void* host_out, int* n_batches);
+  // group -1 / members null: every live request; else one micro-batch (own CUDA graph)
+  void decode_step(const void* host_in, void* host_out, int* n_batches, int group = -1,
+                   const std::vector<int>* members = nullptr);
   int live() const;
   std::int64_t generated() const { return tokens_generated_; }
   void* arena() { return arena_; }
+  void* prefill_arena() { return parena_; }
+  std::int64_t prefill_rows() const { return prefill_rows_; }
 
   std::vector<bh_batch_rec> recs;
   std::vector<int32_t> m_req, m_step, m_ctx;
@@ -120,6 +124,7 @@ class Runner {
   be_workspace* ws_ = nullptr;
   void* arena_ = nullptr;   // decode rows [n_req][d]
   void* parena_ = nullptr;  // prefill rows [sum prompt][d]
+  std::int64_t prefill_rows_ = 0;
   bool has_running_ = false;
   std::string running_inst_;
   Batch running_;
@@ -128,11 +133,24 @@ class Runner {
   bool in_lockstep_step_ = false;
   std::int64_t tokens_generated_ = 0;
   int batches_run_ = 0;
-  // graph replay of a steady-state lockstep decode step
-  std::vector<std::tuple<int, int, int>> graph_sig_;  // (block, n_tokens, stride) per batch
-  cudaGraphExec_t graph_exec_ = nullptr;
-  cudaGraph_t graph_ = nullptr;
-  char* meta_host_ = nullptr;  // pinned staging
+  // graph replay of a steady-state lockstep decode step, one per request group
+  struct GraphSlot {
+    std::vector<std::tuple<int, int, int>> sig;  // (block, n_tokens, stride) per batch
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    void reset() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      exec = nullptr;
+      graph = nullptr;
+    }
+  };
+  std::map<int, GraphSlot> graphs_;
+  // pinned staging ring: the host plans step s+1 while step s still runs; slot k is rewritten
+  // only after its previous upload (two steps back) has executed
+  char* meta_host_[2] = {nullptr, nullptr};
+  cudaEvent_t meta_ev_[2] = {nullptr, nullptr};
+  int meta_slot_ = 0;
   char* meta_dev_ = nullptr;
   size_t meta_cap_ = 0;
 };
@@ -229,6 +247,7 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   if (rc != BE_OK) throw BeError(rc, std::string("workspace: ") + be_last_error(ctx));
   ck(cudaMalloc(&arena_, (size_t)w.n_requests * d_ * 2), "arena");
   ck(cudaMalloc(&parena_, (size_t)poff * d_ * 2), "prefill arena");
+  prefill_rows_ = poff;
   for (const auto& r : reqs_) {
     const std::string sid = "inputs:req" + std::to_string(r.id);
     rc = be_synth_rows(ctx, static_cast<char*>(parena_) + (size_t)r.poff * d_ * 2,
@@ -239,9 +258,12 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
 }
 
 Runner::~Runner() {
-  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-  if (graph_) cudaGraphDestroy(graph_);
-  if (meta_host_) cudaFreeHost(meta_host_);
+  for (auto& kv : graphs_) kv.second.reset();
+  if (!dry_) cudaStreamSynchronize(st_);
+  for (int k = 0; k < 2; ++k) {
+    if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
+    if (meta_ev_[k]) cudaEventDestroy(meta_ev_[k]);
+  }
   if (meta_dev_) cudaFree(meta_dev_);
   if (arena_) cudaFree(arena_);
   if (parena_) cudaFree(parena_);
@@ -483,11 +505,25 @@ void Runner::run(int max_batches) {
   }
 }
 
-void Runner::decode_step(const void* host_in, void* host_out, int* n_batches) {
+void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, int group,
+                         const std::vector<int>* members) {
   if (mode_ != 1) throw BeError(BE_ERR_STATE, "decode_step needs lockstep mode");
   if (has_running_) throw BeError(BE_ERR_STATE, "prefill still running");
-  std::vector<int> order = step_done_order_;
-  step_done_order_.clear();
+  std::vector<int> order;
+  if (members == nullptr) {
+    order = step_done_order_;
+    step_done_order_.clear();
+  } else {
+    // one micro-batch of the pipeline: its requests step, the others keep waiting
+    std::vector<char> in(reqs_.size(), 0);
+    for (int idx : *members) {
+      if (idx < 0 || idx >= (int)reqs_.size()) throw BeError(BE_ERR_INVALID, "bad request index");
+      in[idx] = 1;
+    }
+    std::vector<int> rest;
+    for (int idx : step_done_order_) (in[idx] ? order : rest).push_back(idx);
+    step_done_order_.swap(rest);
+  }
   // host rows are the live requests in request order; contiguous runs move in one copy
   std::vector<int> rows = order;
   std::sort(rows.begin(), rows.end());
@@ -537,33 +573,40 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches) {
     sig.emplace_back(plans[i].block, static_cast<int>(plans[i].toks.size()), plans[i].stride);
   }
   if (total > meta_cap_) {
-    if (meta_host_) cudaFreeHost(meta_host_);
+    ck(cudaStreamSynchronize(st_), "meta grow");
+    for (int k = 0; k < 2; ++k) {
+      if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
+      if (!meta_ev_[k]) ck(cudaEventCreateWithFlags(&meta_ev_[k], cudaEventDisableTiming), "meta ev");
+    }
     if (meta_dev_) cudaFree(meta_dev_);
     meta_cap_ = total * 2;
-    ck(cudaMallocHost(&meta_host_, meta_cap_), "meta host");
+    for (int k = 0; k < 2; ++k) ck(cudaMallocHost(&meta_host_[k], meta_cap_), "meta host");
     ck(cudaMalloc(&meta_dev_, meta_cap_), "meta dev");
-    if (graph_exec_) {
-      cudaGraphExecDestroy(graph_exec_);
-      graph_exec_ = nullptr;
-    }
-    graph_sig_.clear();
+    for (auto& kv : graphs_) kv.second.reset();  // captured graphs point into the old buffer
   }
-  ck(cudaStreamSynchronize(st_), "meta reuse");  // previous step may still read the staging
+  GraphSlot& gs = graphs_[group];
+  // the device copy of the metadata is stream-ordered after the previous step's kernels; only
+  // the host staging slot needs its earlier upload to have executed
+  const int slot = meta_slot_;
+  meta_slot_ ^= 1;
+  ck(cudaEventSynchronize(meta_ev_[slot]), "meta reuse");
+  char* stage = meta_host_[slot];
   for (size_t i = 0; i < plans.size(); ++i) {
-    std::memcpy(meta_host_ + off_tok[i], plans[i].toks.data(), plans[i].toks.size() * sizeof(be_token));
-    std::memcpy(meta_host_ + off_pt[i], plans[i].pt.data(), plans[i].pt.size() * sizeof(int32_t));
+    std::memcpy(stage + off_tok[i], plans[i].toks.data(), plans[i].toks.size() * sizeof(be_token));
+    std::memcpy(stage + off_pt[i], plans[i].pt.data(), plans[i].pt.size() * sizeof(int32_t));
   }
-  ck(cudaMemcpyAsync(meta_dev_, meta_host_, total, cudaMemcpyHostToDevice, st_), "meta h2d");
+  ck(cudaMemcpyAsync(meta_dev_, stage, total, cudaMemcpyHostToDevice, st_), "meta h2d");
+  ck(cudaEventRecord(meta_ev_[slot], st_), "meta ev record");
   auto launch_all = [&]() {
     for (size_t i = 0; i < plans.size(); ++i)
       launch(plans[i], reinterpret_cast<const be_token*>(meta_dev_ + off_tok[i]),
              reinterpret_cast<const int32_t*>(meta_dev_ + off_pt[i]));
   };
   stats.graph_replayed = 0;
-  if (use_graphs_ && sig == graph_sig_ && graph_exec_ != nullptr) {
-    ck(cudaGraphLaunch(graph_exec_, st_), "graph launch");
+  if (use_graphs_ && sig == gs.sig && gs.exec != nullptr) {
+    ck(cudaGraphLaunch(gs.exec, st_), "graph launch");
     stats.graph_replayed = 1;
-  } else if (use_graphs_ && sig == graph_sig_) {
+  } else if (use_graphs_ && sig == gs.sig) {
     // second step with this structure: capture it
     ck(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "capture begin");
     try {
@@ -574,20 +617,16 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches) {
       if (g) cudaGraphDestroy(g);
       throw;
     }
-    if (graph_) cudaGraphDestroy(graph_);
-    ck(cudaStreamEndCapture(st_, &graph_), "capture end");
-    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-    ck(cudaGraphInstantiate(&graph_exec_, graph_, 0), "graph instantiate");
-    ck(cudaGraphLaunch(graph_exec_, st_), "graph launch");
+    gs.reset();
+    ck(cudaStreamEndCapture(st_, &gs.graph), "capture end");
+    ck(cudaGraphInstantiate(&gs.exec, gs.graph, 0), "graph instantiate");
+    ck(cudaGraphLaunch(gs.exec, st_), "graph launch");
     stats.graph_replayed = 1;
   } else {
     launch_all();
-    graph_sig_ = sig;
-    if (graph_exec_) {
-      cudaGraphExecDestroy(graph_exec_);
-      graph_exec_ = nullptr;
-    }
+    gs.reset();
   }
+  gs.sig = sig;
   if (host_out != nullptr) {
     copy_rows(false, host_out);
     ck(cudaStreamSynchronize(st_), "d2h sync");
@@ -651,9 +690,20 @@ extern "C" int bh_runner_decode_step(bh_runner* h, const void* in, void* out, in
   if (h == nullptr) return BE_ERR_INVALID;
   return guard(h, [&] { h->r->decode_step(in, out, n_batches); });
 }
+extern "C" int bh_runner_decode_group(bh_runner* h, int group, const int32_t* reqs, int n,
+                                      const void* in, void* out, int* n_batches) {
+  if (h == nullptr || group < 0 || (n > 0 && reqs == nullptr)) return BE_ERR_INVALID;
+  std::vector<int> members(reqs, reqs + n);
+  return guard(h, [&] { h->r->decode_step(in, out, n_batches, group, &members); });
+}
 extern "C" int bh_runner_live_requests(const bh_runner* h) { return h ? h->r->live() : 0; }
 extern "C" int64_t bh_runner_tokens_generated(const bh_runner* h) { return h ? h->r->generated() : 0; }
 extern "C" void* bh_runner_arena(bh_runner* h) { return h ? h->r->arena() : nullptr; }
+extern "C" void* bh_runner_prefill_arena(bh_runner* h, int64_t* rows) {
+  if (h == nullptr) return nullptr;
+  if (rows) *rows = h->r->prefill_rows();
+  return h->r->prefill_arena();
+}
 extern "C" int bh_runner_trace(const bh_runner* h, bh_batch_rec* recs, int cap, int* n_out,
                                int32_t* mreq, int32_t* mstep, int32_t* mctx, int mcap, int* m_out) {
   if (h == nullptr || n_out == nullptr) return BE_ERR_INVALID;

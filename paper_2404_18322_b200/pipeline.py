@@ -1,0 +1,203 @@
+"""Multi-GPU block placement: chains placed across GPUs as pipeline stages, activations moving
+between consecutive stages by NCCL point-to-point send/recv over NVLink (the inter-block hop of
+Simulation::deliver / LinkManager::transfer, proj/core/src/scenario.cpp:282-308,
+cluster.cpp:170-192; hop payload 2*d bytes per token, costmodel.cpp:129-131).
+
+Placement (placement_stages): contiguous chain-position ranges per GPU, cut to minimise the
+most loaded stage (weights + KV bytes streamed per decode step) - consecutive blocks of a chain
+stay together, so a decode token crosses one GPU boundary per stage (under NVSwitch,
+locality = fewest hops). N micro-batches are in flight: at tick t, stage s runs micro-batch
+(t - s) mod N through its blocks, then in one grouped NCCL call sends the rows on and receives
+the next micro-batch's rows (the grouped send+recv cannot deadlock around the ring). The last
+stage feeds the first (greedy next-token input).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .workloads import Workload
+
+
+def position_costs(wl: Workload, ctx_tokens: int) -> list[float]:
+    """Bytes streamed per decode step at each chain position (all tenants' blocks there)."""
+    s = wl.shape
+    npos = max(len(c) for c in wl.chains)
+    w_bytes = s.param_bytes
+    kv_row = ctx_tokens * s.kv_bytes_per_token  # K+V read per request per block
+    rows = wl.rows_at_block()
+    cost = [0.0] * npos
+    for p in range(npos):
+        blocks = {c[p] for c in wl.chains if p < len(c)}
+        for b in blocks:
+            cost[p] += w_bytes + rows[b] * kv_row
+    return cost
+
+
+def placement_stages(costs: list[float], n: int) -> list[tuple[int, int]]:
+    """Contiguous partition of positions into n stages minimising the max stage cost (DP)."""
+    P = len(costs)
+    n = min(n, P)
+    pre = [0.0]
+    for c in costs:
+        pre.append(pre[-1] + c)
+    INF = float("inf")
+    best = [[INF] * (P + 1) for _ in range(n + 1)]
+    cut = [[0] * (P + 1) for _ in range(n + 1)]
+    best[0][0] = 0.0
+    for k in range(1, n + 1):
+        for j in range(k, P + 1):
+            for i in range(k - 1, j):
+                v = max(best[k - 1][i], pre[j] - pre[i])
+                if v < best[k][j]:
+                    best[k][j], cut[k][j] = v, i
+    ranges, j = [], P
+    for k in range(n, 0, -1):
+        i = cut[k][j]
+        ranges.append((i, j))
+        j = i
+    return ranges[::-1]
+
+
+def stage_workload(wl: Workload, rng: tuple[int, int], n_micro: int) -> Workload:
+    """The blocks of chain positions [a, b) and n_micro copies of the request mix."""
+    a, b = rng
+    names, comps, remap, chains = [], [], {}, []
+    for ch in wl.chains:
+        sub = []
+        for blk in ch[a:b]:
+            if blk not in remap:
+                remap[blk] = len(names)
+                names.append(wl.block_names[blk])
+                if wl.block_comps:
+                    comps.append(wl.block_comps[blk])
+            sub.append(remap[blk])
+        chains.append(sub)
+    n = wl.n_requests
+    return Workload(f"{wl.name}@{a}-{b}", wl.shape, names, chains,
+                    wl.req_tenant * n_micro, wl.req_prompt * n_micro, wl.req_output * n_micro,
+                    wl.max_batch_tokens, wl.seed, dict(wl.notes, stage=(a, b)),
+                    comps or None)
+
+
+class _DevRows:
+    """__cuda_array_interface__ over raw bf16 rows (viewed as int16 for NCCL transport)."""
+
+    def __init__(self, ptr: int, rows: int, cols: int):
+        self.__cuda_array_interface__ = {"shape": (rows, cols), "typestr": "<i2",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+@dataclass
+class TickStats:
+    computed: int = 0   # micro-batch steps this rank ran
+    finished: int = 0   # tokens completed by this rank as the last stage
+
+
+class PipelineStage:
+    """One rank of the block-placed pipeline (torch.distributed with the NCCL backend)."""
+
+    def __init__(self, ctx, wl: Workload, world: int, rank: int, n_micro: int | None = None,
+                 ctx_for_cost: int | None = None):
+        import torch
+        import torch.distributed as dist
+        from .runner import Runner
+        self.torch, self.dist = torch, dist
+        self.world, self.rank = world, rank
+        self.n_micro = n_micro or world
+        costs = position_costs(wl, ctx_for_cost or (wl.req_prompt[0] + wl.req_output[0] // 2))
+        self.stages = placement_stages(costs, world)
+        self.stage_costs = [sum(costs[a:b]) for a, b in self.stages]
+        self.wl = stage_workload(wl, self.stages[rank], self.n_micro)
+        self.per_mb = wl.n_requests
+        self.ctx = ctx
+        self.run = Runner(ctx, self.wl, mode=1, use_graphs=True)
+        self.stream = torch.cuda.ExternalStream(ctx.stream.value)
+        d = wl.shape.d_model
+        self.d = d
+        dptr = self.run.arena_ptr
+        self.arena = torch.as_tensor(_DevRows(dptr, self.wl.n_requests, d), device="cuda")
+        pptr, prow = self.run.prefill_arena()
+        self.parena = torch.as_tensor(_DevRows(pptr, prow, d), device="cuda")
+        self.stats = TickStats()
+
+    # ------------------------------------------------------------------ prefill
+    def prefill(self):
+        """Stage by stage: receive the prompts' hidden states, prefill, pass them on; the last
+        stage returns the first-token rows to stage 0."""
+        dist, torch = self.dist, self.torch
+        r, W = self.rank, self.world
+        with torch.cuda.stream(self.stream):
+            if W > 1 and r > 0:
+                dist.recv(self.parena, src=r - 1)
+            self.run.run()
+            if W > 1 and r < W - 1:
+                dist.send(self.parena, dst=r + 1)
+            if W > 1 and r == W - 1:
+                dist.send(self.arena, dst=0)
+            if W > 1 and r == 0:
+                dist.recv(self.arena, src=W - 1)
+        self.ctx.sync()
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------------------ decode ticks
+    def mb_rows(self, m: int):
+        return self.arena[m * self.per_mb:(m + 1) * self.per_mb]
+
+    def tick(self, t: int, total_ticks: int) -> None:
+        with self.torch.cuda.stream(self.stream):
+            run_tick(self.dist, t, total_ticks, self.rank, self.world, self.n_micro,
+                     self._compute, self.mb_rows)
+
+    def _compute(self, m: int) -> None:
+        reqs = np.arange(m * self.per_mb, (m + 1) * self.per_mb, dtype=np.int32)
+        self.run.decode_group(m, reqs)
+        self.stats.computed += 1
+        if self.rank == self.world - 1:
+            self.stats.finished += self.per_mb
+
+    def close(self):
+        self.run.close()
+
+
+def tick_plan(t: int, total_ticks: int, r: int, W: int, N: int):
+    """(compute, send, recv) micro-batch indices (or None) of stage r at tick t.
+
+    Stage r first computes at tick r (micro-batch 0), so at tick t it runs micro-batch
+    (t - r) mod N; its output goes to stage r+1 (the last stage wraps to stage 0: the next token's
+    input), and it receives the micro-batch it runs at tick t+1. Stage 0 owns every micro-batch's
+    first input (from prefill), so it only receives once the last stage has produced something.
+    """
+    comp = (t - r) % N if t >= r else None
+    if W == 1:
+        return comp, None, None
+    send = comp if comp is not None and t + 1 < total_ticks else None
+    recv = None
+    if t + 1 >= r and t + 1 < total_ticks and (r > 0 or t >= W - 1):
+        recv = (t + 1 - r) % N
+    return comp, send, recv
+
+
+def run_tick(dist, t, total_ticks, r, W, N, compute, rows) -> None:
+    """One tick: compute, then one grouped send-on / receive-next (cannot deadlock the ring)."""
+    comp, send, recv = tick_plan(t, total_ticks, r, W, N)
+    if comp is not None:
+        compute(comp)
+    ops = []
+    if send is not None:
+        ops.append(dist.P2POp(dist.isend, rows(send), (r + 1) % W))
+    if recv is not None:
+        ops.append(dist.P2POp(dist.irecv, rows(recv), (r - 1) % W))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def ticks_needed(world: int, steps: int, warmup: int) -> int:
+    return warmup + steps + world
+
+
+def tokens_per_request_needed(world: int, total_ticks: int, n_micro: int) -> int:
+    return math.ceil(total_ticks / n_micro) + 2

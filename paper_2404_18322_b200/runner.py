@@ -50,6 +50,8 @@ def _bind():
         ("bh_runner_trace", I, [P, P, I, P, P, P, P, I, P]),
         ("bh_runner_clear_trace", I, [P]),
         ("bh_runner_arena", P, [P]),
+        ("bh_runner_prefill_arena", P, [P, C.POINTER(C.c_int64)]),
+        ("bh_runner_decode_group", I, [P, I, P, I, P, P, P]),
         ("bh_runner_step_stats", I, [P, P]),
     ]:
         fn = getattr(L, name)
@@ -113,6 +115,22 @@ class Runner:
                           (host_out.ctypes.data if host_out is not None else 0))
         self._check(lib().bh_runner_decode_step(self.h, pin, pout, C.byref(n)))
         return n.value
+
+    def decode_group(self, group: int, requests, host_in=None, host_out=None) -> int:
+        """One lockstep token for a request group (pipeline micro-batch) only."""
+        req = np.ascontiguousarray(requests, np.int32)
+        n = C.c_int(0)
+        pin = C.c_void_p(host_in.data_ptr() if host_in is not None else 0)
+        pout = C.c_void_p(host_out.data_ptr() if host_out is not None else 0)
+        self._check(lib().bh_runner_decode_group(self.h, group, req.ctypes.data, req.size, pin,
+                                                 pout, C.byref(n)))
+        return n.value
+
+    def prefill_arena(self):
+        """(device pointer, rows) of the prompt hidden-state rows (all requests, in order)."""
+        rows = C.c_int64(0)
+        ptr = lib().bh_runner_prefill_arena(self.h, C.byref(rows))
+        return ptr, rows.value
 
     @property
     def live(self) -> int:

@@ -1,0 +1,86 @@
+"""Parity of the block-placed pipeline (N GPUs, NCCL P2P hops) with the one-GPU lockstep run.
+
+torchrun --nproc-per-node N scripts/pipeline_check.py [--config c2 --prompt 64 --ticks 12]
+
+Micro-batch 0 of the pipeline holds the same requests (ids 1..R) as the single-GPU workload, is
+batched identically at every block, so its rows after each pass through the last stage must equal
+the single-GPU decode step outputs bit for bit. Rank N-1 runs both and prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2404_18322_b200.device import Context  # noqa: E402
+from paper_2404_18322_b200.pipeline import PipelineStage, tokens_per_request_needed  # noqa: E402
+from paper_2404_18322_b200.runner import Runner  # noqa: E402
+from paper_2404_18322_b200.workloads import CONFIGS  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--prompt", type=int, default=64)
+    ap.add_argument("--ticks", type=int, default=12)
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    total = a.ticks
+    out = tokens_per_request_needed(world, total, world) + 1
+    wl = CONFIGS["c1"](output=out) if a.config == "c1" else \
+        CONFIGS[a.config](prompt=a.prompt, output=out)
+    ctx = Context(local)
+    st = PipelineStage(ctx, wl, world, rank)
+    snaps = []
+    last = rank == world - 1
+    base = st._compute
+
+    def compute(m):
+        base(m)
+        if last and m == 0:
+            snaps.append(st.mb_rows(0).clone())
+
+    st._compute = compute
+    st.prefill()
+    for t in range(total):
+        st.tick(t, total)
+    ctx.sync()
+    torch.cuda.synchronize()
+    dist.barrier()
+    if last:
+        ref = Runner(ctx, wl, mode=1, use_graphs=True)
+        ref.run()
+        arena = torch.as_tensor(_rows(ref.arena_ptr, wl.n_requests, wl.shape.d_model),
+                                device="cuda")
+        res = []
+        with torch.cuda.stream(st.stream):
+            for k in range(len(snaps)):
+                ref.decode_step()
+                ctx.sync()
+                same = torch.equal(arena, snaps[k])
+                diff = (arena.view(torch.bfloat16).float() -
+                        snaps[k].view(torch.bfloat16).float()).abs().max().item()
+                res.append({"pass": k + 1, "bit_exact": bool(same), "max_abs_diff": diff})
+        ref.close()
+        print(json.dumps({"pipeline_check": a.config, "world": world, "stages": st.stages,
+                          "passes": res,
+                          "ok": all(r["bit_exact"] for r in res) and len(res) > 0}), flush=True)
+    st.close()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def _rows(ptr, rows, cols):
+    from paper_2404_18322_b200.pipeline import _DevRows
+    return _DevRows(ptr, rows, cols)
+
+
+if __name__ == "__main__":
+    main()
