@@ -225,30 +225,35 @@ def kernel_rooflines(ctx, wl, peaks):
     return res
 
 
-def run_pipeline(args, world, rank, local):
-    """N > 1 with block placement: chain positions placed as pipeline stages over the GPUs,
-    N micro-batches in flight, activation hops by NCCL P2P (paper_2404_18322_b200/pipeline.py)."""
+def make_workload(args, output=None):
+    from paper_2404_18322_b200.workloads import CONFIGS
+    out = output or args.output
+    return CONFIGS[args.config](prompt=args.prompt, output=out) if args.config != "c1" \
+        else CONFIGS["c1"](output=out)
+
+
+def run_pipeline(args, world, rank, local, depth, why):
+    """N > 1 with chain positions cut into `depth` pipeline stages (world / depth replica groups
+    side by side), `depth` micro-batches in flight per group, activation hops between stages by
+    NCCL P2P over NVLink (paper_2404_18322_b200/pipeline.py)."""
     import torch
     import torch.distributed as dist
     from paper_2404_18322_b200.device import Context
     from paper_2404_18322_b200.pipeline import PipelineStage, ticks_needed, \
         tokens_per_request_needed
-    from paper_2404_18322_b200.workloads import CONFIGS
 
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    peaks, peaks_kind = load_peaks()
-    total = ticks_needed(world, args.steps, args.warmup)
-    need = tokens_per_request_needed(world, total, world) + 1
-    out = max(args.output, need)
-    wl = CONFIGS[args.config](prompt=args.prompt, output=out) if args.config != "c1" \
-        else CONFIGS["c1"](output=out)
+    total = ticks_needed(depth, args.steps, args.warmup)
+    need = tokens_per_request_needed(depth, total, depth) + 1
+    wl = make_workload(args, max(args.output, need))
     ctx = Context(local)
-    stage = PipelineStage(ctx, wl, world, rank)
+    group, st_idx = divmod(rank, depth)
+    stage = PipelineStage(ctx, wl, depth, st_idx, base_rank=group * depth)
     t0 = time.time()
     stage.prefill()
     prefill_s = time.time() - t0
-    warm = args.warmup + world  # fill the pipeline
+    warm = args.warmup + depth  # fill the pipeline
     for t in range(warm):
         stage.tick(t, total)
     ctx.sync()
@@ -271,9 +276,10 @@ def run_pipeline(args, world, rank, local):
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     ms = float(tm.item())
     fin = torch.tensor([stage.stats.finished - before], device="cuda", dtype=torch.float64)
-    dist.all_reduce(fin, op=dist.ReduceOp.SUM)  # only the last stage counts tokens
+    dist.all_reduce(fin, op=dist.ReduceOp.SUM)  # only each group's last stage counts tokens
     tokens = float(fin.item())
     stats = stage.run.step_stats()
+    hop_bytes = wl.n_requests * wl.shape.d_model * 2
     if rank == 0:
         line = {
             "metric": "block-chain decode tokens/s", "value": round(tokens / (ms / 1e3), 2),
@@ -284,15 +290,18 @@ def run_pipeline(args, world, rank, local):
             "config": {"workload": wl.name, "tenants": len(wl.chains),
                        "global_batch": wl.n_requests * world, "prompt": wl.req_prompt[0],
                        "decode": wl.req_output[0],
-                       "parallelism": f"block placement: {world} pipeline stages over chain "
-                                      f"positions {stage.stages}, {world} micro-batches of "
-                                      f"{wl.n_requests}, NCCL P2P hops",
+                       "parallelism": f"block placement: {world // depth} group(s) x {depth} "
+                                      f"pipeline stages over chain positions {stage.stages}, "
+                                      f"{depth} micro-batches of {wl.n_requests} per group, "
+                                      f"NCCL P2P hops of {hop_bytes} B",
+                       "placement": why,
                        "stage_cost_bytes": [round(c) for c in stage.stage_costs],
                        "l2": "inputs larger than L2"},
             "roofline": None, "e2e": None, "cpu_baseline": None,
             "gpu_launches": int(stats["launches"]) * args.steps, "clocks": clk,
             "prefill_s": round(prefill_s, 2),
-            "note": "one step = one pipeline tick = one micro-batch token leaving the last stage",
+            "note": "one step = one pipeline tick = one micro-batch token leaving each group's "
+                    "last stage",
         }
         print(json.dumps(line), flush=True)
     stage.close()
@@ -307,15 +316,23 @@ def run_ours(args, world, rank, local):
     from paper_2404_18322_b200.runner import Runner
     from paper_2404_18322_b200.workloads import CONFIGS
 
-    if world > 1 and args.placement == "pipeline":
-        return run_pipeline(args, world, rank, local)
+    placement = "1 GPU"
+    if world > 1:
+        from paper_2404_18322_b200.pipeline import choose_layout
+        lay = choose_layout(make_workload(args), world)
+        depth = {"pipeline": world, "replica": 1, "auto": lay["depth"]}[args.placement]
+        why = (f"{args.placement}: placement model picks depth {lay['depth']} x "
+               f"{lay['replicas']} replicas (modelled max stage bytes/step "
+               f"{world // lay['replicas'] / lay['score']:.3g}, stage HBM {lay['stage_mem']:.3g} B)")
+        if depth > 1:
+            return run_pipeline(args, world, rank, local, depth, why)
+        placement = why
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peaks_kind = load_peaks()
-    wl = CONFIGS[args.config](prompt=args.prompt, output=args.output) if args.config != "c1" \
-        else CONFIGS["c1"](output=args.output)
+    wl = make_workload(args)
     ctx = Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream.value)
     run = Runner(ctx, wl, mode=1, use_graphs=True)
@@ -432,7 +449,8 @@ def run_ours(args, world, rank, local):
                        "blocks": f"{len(wl.block_names)} blocks x {wl.shape.n_layers} layers",
                        "rows_per_block": wl.rows_at_block(), "batches_per_step": nb,
                        "l2": "inputs larger than L2 (weights+KV streamed per step)",
-                       "parallelism": f"replica per GPU x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": f"replica per GPU x{world}" if world > 1 else "1 GPU",
+                       "placement": placement},
             "roofline": roofline, "step_roofline": step_roofline, "kernels": kr,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(stats["launches"]) * args.steps,
             "graph_replayed": bool(stats["graph_replayed"]), "clocks": clk,
@@ -488,9 +506,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
-    ap.add_argument("--placement", default="pipeline", choices=["pipeline", "replica"],
-                    help="N>1: block placement as pipeline stages with NCCL P2P hops, or one "
-                         "independent replica of the workload per GPU")
+    ap.add_argument("--placement", default="auto", choices=["auto", "pipeline", "replica"],
+                    help="N>1: the placement model's choice (auto), chain positions cut into N "
+                         "pipeline stages with NCCL P2P hops, or one replica of the zoo per GPU")
     ap.add_argument("--profile", action="store_true",
                     help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
     args = ap.parse_args()

@@ -61,6 +61,44 @@ def placement_stages(costs: list[float], n: int) -> list[tuple[int, int]]:
     return ranges[::-1]
 
 
+def stage_memory(wl: Workload, rng: tuple[int, int], n_micro: int) -> float:
+    """HBM bytes a stage holds: its blocks' weights plus full-length KV of n_micro request mixes."""
+    s = wl.shape
+    a, b = rng
+    blocks = {blk for ch in wl.chains for blk in ch[a:b]}
+    kv = 0.0
+    for t, n_out, n_in in zip(wl.req_tenant, wl.req_output, wl.req_prompt):
+        nb = len(set(wl.chains[t][a:b]))
+        kv += nb * (n_in + n_out) * s.kv_bytes_per_token
+    return len(blocks) * s.param_bytes + n_micro * kv
+
+
+def choose_layout(wl: Workload, world: int, hbm_bytes: float = 0.85 * 180e9) -> dict:
+    """Block placement over `world` GPUs: pipeline depth P (chain positions cut into P stages,
+    NCCL hops between them) times R = world / P replica groups, each group serving its own
+    request mixes. Among depths whose stages fit in HBM, pick the highest modelled throughput
+    R / max_stage_cost (every GPU streams its stage's weights + KV once per token step); with
+    180 GB per GPU a 7B/13B zoo fits whole, so replication (P = 1, no hop) wins unless memory
+    forces a cut - the same trade the reference's placement makes between replicas and spread."""
+    npos = max(len(c) for c in wl.chains)
+    costs = position_costs(wl, wl.req_prompt[0] + wl.req_output[0] // 2)
+    best = None
+    for P in range(1, min(world, npos) + 1):
+        if world % P:
+            continue
+        st = placement_stages(costs, P)
+        mem = max(stage_memory(wl, r, P) for r in st)
+        if mem > hbm_bytes:
+            continue
+        score = (world // P) / max(sum(costs[a:b]) for a, b in st)
+        if best is None or score > best["score"] * (1 + 1e-9):
+            best = {"depth": P, "replicas": world // P, "stages": st, "score": score,
+                    "stage_mem": mem}
+    if best is None:
+        raise ValueError(f"{wl.name}: no placement fits {world} GPUs")
+    return best
+
+
 def stage_workload(wl: Workload, rng: tuple[int, int], n_micro: int) -> Workload:
     """The blocks of chain positions [a, b) and n_micro copies of the request mix."""
     a, b = rng
@@ -83,7 +121,8 @@ def stage_workload(wl: Workload, rng: tuple[int, int], n_micro: int) -> Workload
 
 
 class _DevRows:
-    """__cuda_array_interface__ over raw bf16 rows (viewed as int16 for NCCL transport)."""
+    """__cuda_array_interface__ over raw bf16 rows (int16 typestr: the interface has no bf16; the
+    tensor is viewed back as bfloat16 for NCCL)."""
 
     def __init__(self, ptr: int, rows: int, cols: int):
         self.__cuda_array_interface__ = {"shape": (rows, cols), "typestr": "<i2",
@@ -100,12 +139,14 @@ class PipelineStage:
     """One rank of the block-placed pipeline (torch.distributed with the NCCL backend)."""
 
     def __init__(self, ctx, wl: Workload, world: int, rank: int, n_micro: int | None = None,
-                 ctx_for_cost: int | None = None):
+                 ctx_for_cost: int | None = None, base_rank: int = 0):
+        """`world` = pipeline depth, `rank` = stage index; the group occupies global ranks
+        base_rank .. base_rank + world - 1 (replica groups side by side)."""
         import torch
         import torch.distributed as dist
         from .runner import Runner
         self.torch, self.dist = torch, dist
-        self.world, self.rank = world, rank
+        self.world, self.rank, self.base = world, rank, base_rank
         self.n_micro = n_micro or world
         costs = position_costs(wl, ctx_for_cost or (wl.req_prompt[0] + wl.req_output[0] // 2))
         self.stages = placement_stages(costs, world)
@@ -118,9 +159,10 @@ class PipelineStage:
         d = wl.shape.d_model
         self.d = d
         dptr = self.run.arena_ptr
-        self.arena = torch.as_tensor(_DevRows(dptr, self.wl.n_requests, d), device="cuda")
+        self.arena = torch.as_tensor(_DevRows(dptr, self.wl.n_requests, d),
+                                     device="cuda").view(torch.bfloat16)
         pptr, prow = self.run.prefill_arena()
-        self.parena = torch.as_tensor(_DevRows(pptr, prow, d), device="cuda")
+        self.parena = torch.as_tensor(_DevRows(pptr, prow, d), device="cuda").view(torch.bfloat16)
         self.stats = TickStats()
 
     # ------------------------------------------------------------------ prefill
@@ -129,16 +171,21 @@ class PipelineStage:
         stage returns the first-token rows to stage 0."""
         dist, torch = self.dist, self.torch
         r, W = self.rank, self.world
+
+        def p2p(op, t, peer):
+            for w in dist.batch_isend_irecv([dist.P2POp(op, t, self.base + peer)]):
+                w.wait()
+
         with torch.cuda.stream(self.stream):
             if W > 1 and r > 0:
-                dist.recv(self.parena, src=r - 1)
+                p2p(dist.irecv, self.parena, r - 1)
             self.run.run()
             if W > 1 and r < W - 1:
-                dist.send(self.parena, dst=r + 1)
+                p2p(dist.isend, self.parena, r + 1)
             if W > 1 and r == W - 1:
-                dist.send(self.arena, dst=0)
+                p2p(dist.isend, self.arena, 0)
             if W > 1 and r == 0:
-                dist.recv(self.arena, src=W - 1)
+                p2p(dist.irecv, self.arena, W - 1)
         self.ctx.sync()
         torch.cuda.synchronize()
 
@@ -149,7 +196,7 @@ class PipelineStage:
     def tick(self, t: int, total_ticks: int) -> None:
         with self.torch.cuda.stream(self.stream):
             run_tick(self.dist, t, total_ticks, self.rank, self.world, self.n_micro,
-                     self._compute, self.mb_rows)
+                     self._compute, self.mb_rows, self.base)
 
     def _compute(self, m: int) -> None:
         reqs = np.arange(m * self.per_mb, (m + 1) * self.per_mb, dtype=np.int32)
@@ -180,16 +227,17 @@ def tick_plan(t: int, total_ticks: int, r: int, W: int, N: int):
     return comp, send, recv
 
 
-def run_tick(dist, t, total_ticks, r, W, N, compute, rows) -> None:
-    """One tick: compute, then one grouped send-on / receive-next (cannot deadlock the ring)."""
+def run_tick(dist, t, total_ticks, r, W, N, compute, rows, base=0) -> None:
+    """One tick: compute, then one grouped send-on / receive-next (cannot deadlock the ring).
+    Stage s of the group is global rank base + s."""
     comp, send, recv = tick_plan(t, total_ticks, r, W, N)
     if comp is not None:
         compute(comp)
     ops = []
     if send is not None:
-        ops.append(dist.P2POp(dist.isend, rows(send), (r + 1) % W))
+        ops.append(dist.P2POp(dist.isend, rows(send), base + (r + 1) % W))
     if recv is not None:
-        ops.append(dist.P2POp(dist.irecv, rows(recv), (r - 1) % W))
+        ops.append(dist.P2POp(dist.irecv, rows(recv), base + (r - 1) % W))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()

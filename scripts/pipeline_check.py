@@ -3,8 +3,8 @@
 torchrun --nproc-per-node N scripts/pipeline_check.py [--config c2 --prompt 64 --ticks 12]
 
 Micro-batch 0 of the pipeline holds the same requests (ids 1..R) as the single-GPU workload, is
-batched identically at every block, so its rows after each pass through the last stage must equal
-the single-GPU decode step outputs bit for bit. Rank N-1 runs both and prints one JSON line.
+batched identically at every block, so its rows after each pass through the last stage must match
+the single-GPU decode step outputs (bf16 tolerance, see TOL). Rank N-1 runs both and prints one JSON line.
 """
 import argparse
 import json
@@ -22,11 +22,21 @@ from paper_2404_18322_b200.runner import Runner  # noqa: E402
 from paper_2404_18322_b200.workloads import CONFIGS  # noqa: E402
 
 
+# Prefill batches differ between the pipeline stages and the one-GPU run (different request
+# arrival order at each block instance), and a GEMM's stream-K split depends on the token count,
+# so the fp32 summation order - and the bf16 rounding of the prompt states - is not identical.
+# Decode steps are batched identically; the check is rel-L2 within bf16 drift.
+TOL = 2e-2
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--prompt", type=int, default=64)
     ap.add_argument("--ticks", type=int, default=12)
+    ap.add_argument("--exact", action="store_true",
+                    help="token budget = one prompt, so every prefill batch holds one request on "
+                         "both sides: identical GEMM shapes everywhere, outputs must be bit-exact")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -36,6 +46,8 @@ def main():
     out = tokens_per_request_needed(world, total, world) + 1
     wl = CONFIGS["c1"](output=out) if a.config == "c1" else \
         CONFIGS[a.config](prompt=a.prompt, output=out)
+    if a.exact:
+        wl.max_batch_tokens = max(wl.req_prompt)
     ctx = Context(local)
     st = PipelineStage(ctx, wl, world, rank)
     snaps = []
@@ -58,20 +70,26 @@ def main():
         ref = Runner(ctx, wl, mode=1, use_graphs=True)
         ref.run()
         arena = torch.as_tensor(_rows(ref.arena_ptr, wl.n_requests, wl.shape.d_model),
-                                device="cuda")
+                                device="cuda").view(torch.bfloat16)
         res = []
         with torch.cuda.stream(st.stream):
             for k in range(len(snaps)):
                 ref.decode_step()
                 ctx.sync()
                 same = torch.equal(arena, snaps[k])
-                diff = (arena.view(torch.bfloat16).float() -
-                        snaps[k].view(torch.bfloat16).float()).abs().max().item()
-                res.append({"pass": k + 1, "bit_exact": bool(same), "max_abs_diff": diff})
+                a32, b32 = snaps[k].float(), arena.float()
+                rel = ((a32 - b32).norm() / b32.norm()).item()
+                res.append({"pass": k + 1, "bit_exact": bool(same),
+                            "equal_frac": (snaps[k] == arena).float().mean().item(),
+                            "max_abs_diff": (a32 - b32).abs().max().item(),
+                            "max_abs_ref": b32.abs().max().item(), "rel_l2": rel})
         ref.close()
         print(json.dumps({"pipeline_check": a.config, "world": world, "stages": st.stages,
                           "passes": res,
-                          "ok": all(r["bit_exact"] for r in res) and len(res) > 0}), flush=True)
+                          "tol_rel_l2": TOL,
+                          "exact_mode": a.exact,
+                          "ok": len(res) > 0 and all(r["bit_exact"] if a.exact else
+                                                     r["rel_l2"] < TOL for r in res)}), flush=True)
     st.close()
     ctx.close()
     dist.destroy_process_group()

@@ -10,9 +10,9 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2404_18322_b200.pipeline import (placement_stages, position_costs, stage_workload,
-                                           tick_plan, run_tick, ticks_needed,
-                                           tokens_per_request_needed)
+from paper_2404_18322_b200.pipeline import (choose_layout, placement_stages, position_costs,
+                                           run_tick, stage_memory, stage_workload, tick_plan,
+                                           ticks_needed, tokens_per_request_needed)
 from paper_2404_18322_b200.workloads import CONFIGS
 
 
@@ -63,6 +63,28 @@ def test_c2_stage_workloads_cover_the_chains():
         assert sorted(blocks_seen) == sorted(wl.block_names)
 
 
+def test_layout_replicates_when_the_zoo_fits():
+    # 180 GB per GPU holds a whole 7B/13B zoo: replicas (no hop) beat any cut under weak scaling
+    for c in ("c2", "c4"):
+        wl = CONFIGS[c]()
+        for W in (1, 2, 4, 8):
+            lay = choose_layout(wl, W)
+            assert (lay["depth"], lay["replicas"]) == (1, W)
+
+
+def test_layout_cuts_the_chain_when_memory_forces_it():
+    wl = CONFIGS["c2"]()
+    whole = stage_memory(wl, (0, 8), 1)
+    lay = choose_layout(wl, 8, hbm_bytes=0.8 * whole)
+    assert lay["depth"] > 1 and lay["depth"] * lay["replicas"] == 8
+    assert lay["stage_mem"] <= 0.8 * whole
+    # every stage of the chosen cut fits, with its micro-batches' KV
+    for r in lay["stages"]:
+        assert stage_memory(wl, r, lay["depth"]) <= 0.8 * whole
+    with pytest.raises(ValueError):
+        choose_layout(wl, 8, hbm_bytes=1e9)
+
+
 @pytest.mark.parametrize("W", [1, 2, 3, 4, 8])
 def test_tick_plan_sends_match_receives(W):
     N = W
@@ -99,44 +121,48 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, W, port, total, q):
+def _worker(rank, world, W, port, total, q):
+    """W = pipeline depth; world / W groups side by side (stage s of group g = rank g*W + s)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=W)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g, s = divmod(rank, W)
     N, rows_per = W, 3
-    arena = torch.zeros(N * rows_per, 4)
+    arena = torch.full((N * rows_per, 4), 1000.0 * g)
     log = []
 
     def compute(m):
-        arena[m * rows_per:(m + 1) * rows_per] += rank + 1
-        if rank == W - 1:
-            log.append((m, float(arena[m * rows_per, 0])))
+        arena[m * rows_per:(m + 1) * rows_per] += s + 1
+        if s == W - 1:
+            log.append((m, float(arena[m * rows_per, 0]) - 1000.0 * g))
 
     for t in range(total):
-        run_tick(dist, t, total, rank, W, N, compute,
-                 lambda m: arena[m * rows_per:(m + 1) * rows_per])
+        run_tick(dist, t, total, s, W, N, compute,
+                 lambda m: arena[m * rows_per:(m + 1) * rows_per], base=g * W)
     dist.barrier()
     q.put((rank, log))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("W", [2, 3])
-def test_gloo_pipeline_ring(W):
+@pytest.mark.parametrize("world,W", [(2, 2), (3, 3), (4, 2)])
+def test_gloo_pipeline_ring(world, W):
     total = ticks_needed(W, 4, 3)
     assert tokens_per_request_needed(W, total, W) > total // W
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, W, port, total, q)) for r in range(W)]
+    ps = [ctx.Process(target=_worker, args=(r, world, W, port, total, q)) for r in range(world)]
     for p in ps:
         p.start()
-    out = dict(q.get(timeout=120) for _ in range(W))
+    out = dict(q.get(timeout=120) for _ in range(world))
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # a micro-batch's k-th pass through all W stages adds k * (1 + 2 + ... + W)
+    # a micro-batch's k-th pass through all W stages adds k * (1 + 2 + ... + W); groups never mix
     per_pass = W * (W + 1) / 2
-    seen = {}
-    for m, v in out[W - 1]:
-        seen[m] = seen.get(m, 0) + 1
-        assert v == seen[m] * per_pass, (m, v, seen[m])
-    assert len(out[W - 1]) >= total - W
+    for g in range(world // W):
+        seen = {}
+        last = out[g * W + W - 1]
+        for m, v in last:
+            seen[m] = seen.get(m, 0) + 1
+            assert v == seen[m] * per_pass, (g, m, v, seen[m])
+        assert len(last) >= total - W
