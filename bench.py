@@ -225,6 +225,83 @@ def kernel_rooflines(ctx, wl, peaks):
     return res
 
 
+def load_traffic():
+    """ncu-measured DRAM bytes per launch by kernel family (profiles/ncu_traffic.json, written
+    by scripts/ncu_traffic.py from one `ncu --set full` capture of a decode step), or {}."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def profile_step(ctx, run, wl, stream, peaks, peaks_kind):
+    """Per-launch event timing of one decode step; algorithmic bytes per launch:
+    GEMM 2(NK + MK + MN); attention = the step's K/V bytes (runner accounting) + q and o rows;
+    rms reads the fp32 residual; gather writes fp32 + bf16 rows; scatter copies bf16 rows."""
+    import torch
+    d = wl.shape.d_model
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    ctx.sync()
+    ctx.prof_enable(True)
+    e0.record(stream)
+    run.decode_step()
+    e1.record(stream)
+    recs = ctx.prof_read()
+    ctx.prof_enable(False)
+    step_ms = e0.elapsed_time(e1)
+    st = run.step_stats()
+    attn_rows = sum(r["ntok"] for r in recs if r["cls"] == "attention")
+    fam = {}
+    for r in recs:
+        c, m, n, k = r["cls"], r["ntok"], r["n"], r["k"]
+        if c.startswith("gemm"):
+            b, fl, f = 2 * (n * k + m * k + m * n), 2 * m * n * k, "gemm"
+        elif c == "attention":
+            b = st["kv_bytes"] * m / max(1, attn_rows) + 2 * 2 * m * n * k
+            fl, f = 0, "attention"
+        elif c == "rms":
+            b, fl, f = 4 * m * n, 0, "rms"
+        elif c == "gather":
+            b, fl, f = 8 * m * n, 0, "gather"
+        else:
+            b, fl, f = 4 * m * n, 0, "scatter"
+        for key in (f, c) if f == "gemm" else (f,):
+            a = fam.setdefault(key, {"launches": 0, "ms": 0.0, "bytes": 0.0, "flops": 0.0})
+            a["launches"] += 1
+            a["ms"] += r["ms"]
+            a["bytes"] += b
+            a["flops"] += fl
+    hbm = peaks["hbm_gbs"]
+    for a in fam.values():
+        a["achieved_gbs"] = round(a["bytes"] / (a["ms"] / 1e3) / 1e9, 1) if a["ms"] else None
+        a["frac"] = round(a["achieved_gbs"] / hbm, 4) if a["achieved_gbs"] else None
+        a["share_of_step"] = round(a["ms"] / step_ms, 4)
+        a["us_per_launch"] = round(1e3 * a["ms"] / a["launches"], 2)
+        a["ms"] = round(a["ms"], 4)
+    fam["_step"] = {"ms": round(step_ms, 4), "launches": len(recs),
+                    "kernel_ms": round(sum(r["ms"] for r in recs), 4),
+                    "note": "event-bracketed launches (no graph, no PDL overlap): the step here "
+                            "is slower than a graph replay; shares are what matters"}
+    top = max((k for k in fam if k in ("gemm", "attention", "rms", "gather", "scatter")),
+              key=lambda k: fam[k]["ms"])
+    a = fam[top]
+    traffic = load_traffic().get(top)
+    roofline = {"bound": "hbm", "kernel": {"gemm": "gemm_sk_kernel (all projections)",
+                                           "attention": "attn_decode_kernel"}.get(top, top),
+                "achieved": a["achieved_gbs"], "peak": hbm, "unit": "GB/s", "frac": a["frac"],
+                "peak_kind": peaks_kind,
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic_algorithmic": round(a["bytes"] / a["launches"]),
+                "traffic_source": traffic.get("source") if traffic else None,
+                "launches_per_step": a["launches"], "us_per_launch": a["us_per_launch"],
+                "share_of_step": a["share_of_step"],
+                "tflops": round(a["flops"] / (a["ms"] / 1e3) / 1e12, 1) if a["flops"] else None}
+    return {"roofline": roofline, "families": fam}
+
+
 def make_workload(args, output=None):
     from paper_2404_18322_b200.workloads import CONFIGS
     out = output or args.output
@@ -410,17 +487,13 @@ def run_ours(args, world, rank, local):
                "h2d_bytes_per_step": int(hin.numel() * 2), "d2h_bytes_per_step": int(hout.numel() * 2),
                "ms_per_step": e_ms / args.steps}
 
-    # ---- roofline of the dominant kernels, and of the whole step
-    kr = kernel_rooflines(ctx, wl, peaks) if rank == 0 and not args.no_roofline else {}
+    # ---- roofline: one more decode step with every launch bracketed by CUDA events on the
+    # runner's stream (graph replay bypassed for this step only), kernels grouped by family
+    prof = profile_step(ctx, run, wl, stream, peaks, peaks_kind) if not args.no_roofline else None
+    roofline = prof["roofline"] if prof else None
+    kr = kernel_rooflines(ctx, wl, peaks) if rank == 0 and args.isolated else {}
     hbm = peaks["hbm_gbs"]
     step_bytes = stats["weight_bytes"] + stats["kv_bytes"] + stats["act_bytes"]
-    roofline = None
-    if "attention" in kr:
-        a = kr["attention"]
-        roofline = {"bound": "hbm", "kernel": a["kernel"], "shape": a["shape"],
-                    "achieved": round(a["achieved_gbs"], 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(a["achieved_gbs"] / hbm, 4), "peak_kind": peaks_kind,
-                    "traffic": None, "us_per_launch": round(a["us"], 2)}
     step_roofline = {"bound": "hbm", "bytes_per_step": step_bytes,
                      "achieved": round(step_bytes / (ms_per_step / 1e3) / 1e9, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(step_bytes / (ms_per_step / 1e3) / 1e9 / hbm, 4),
@@ -451,7 +524,9 @@ def run_ours(args, world, rank, local):
                        "l2": "inputs larger than L2 (weights+KV streamed per step)",
                        "parallelism": f"replica per GPU x{world}" if world > 1 else "1 GPU",
                        "placement": placement},
-            "roofline": roofline, "step_roofline": step_roofline, "kernels": kr,
+            "roofline": roofline, "step_roofline": step_roofline,
+            "kernels": prof["families"] if prof else None,
+            "kernels_isolated": kr or None,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(stats["launches"]) * args.steps,
             "graph_replayed": bool(stats["graph_replayed"]), "clocks": clk,
             "prefill_s": round(prefill_s, 2),
@@ -509,6 +584,8 @@ def main():
     ap.add_argument("--placement", default="auto", choices=["auto", "pipeline", "replica"],
                     help="N>1: the placement model's choice (auto), chain positions cut into N "
                          "pipeline stages with NCCL P2P hops, or one replica of the zoo per GPU")
+    ap.add_argument("--isolated", action="store_true",
+                    help="also time the dominant kernels alone (standalone launches, > L2)")
     ap.add_argument("--profile", action="store_true",
                     help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
     args = ap.parse_args()

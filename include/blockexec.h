@@ -118,6 +118,30 @@ int be_exec_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace
 /* Kernel launches one be_exec_batch of n_tokens performs (for launch accounting). */
 int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_tokens, int pt_stride);
 
+/* Per-launch timing of exec_batch kernels: while enabled, every launch is bracketed by CUDA
+ * events on its stream (graph replay is bypassed by the runner). be_prof_read synchronises the
+ * context stream and returns (and clears) the records; with cap < n only *n_out is written. */
+enum {
+  BE_K_GATHER = 0,
+  BE_K_RMS = 1,
+  BE_K_GEMM_QKV = 2,
+  BE_K_ATTENTION = 3, /* decode/prefill attention (+ split combine); n = heads, k = head_dim */
+  BE_K_GEMM_O = 4,
+  BE_K_GEMM_GATE_UP = 5,
+  BE_K_GEMM_DOWN = 6,
+  BE_K_SCATTER = 7
+};
+typedef struct {
+  int32_t cls;  /* BE_K_* */
+  int32_t ntok; /* rows of the batch */
+  int32_t n;    /* GEMM output features (rows of W), d_model for row kernels */
+  int32_t k;    /* GEMM reduction dim */
+  float ms;     /* event-timed duration */
+} be_prof_rec;
+int be_prof_enable(be_ctx* ctx, int on);
+int be_prof_active(const be_ctx* ctx);
+int be_prof_read(be_ctx* ctx, be_prof_rec* out, int cap, int* n_out);
+
 /* K1 / K2 standalone: routing-table gather and scatter of bf16 rows. */
 int be_gather_rows(be_ctx* ctx, const void* d_arena, const int32_t* d_src, int rows, int d,
                    void* d_out, void* stream);

@@ -81,6 +81,9 @@ def lib() -> C.CDLL:
         "be_pack_weight": (I, [P, P, P, I, I, P]),
         "be_bench_gemm": (I, [P, P, I, P, P, I, I, I, I, C.POINTER(C.c_float)]),
         "be_exec_batch_launches": (I, [P, P, I, I]),
+        "be_prof_enable": (I, [P, I]),
+        "be_prof_active": (I, [P]),
+        "be_prof_read": (I, [P, P, I, P]),
         "be_attention": (I, [P, P, P, I, I, I, I, P, I, P, P, I, I, P, P]),
     }
     for name, (res, args) in sig.items():

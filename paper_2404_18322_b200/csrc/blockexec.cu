@@ -67,6 +67,15 @@ struct be_ctx {
   int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
   int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
   int gemm_deep = 1;      // GEMM ring depth: 1 deep (one CTA/SM), 0 shallow (BE_GEMM_RING)
+  // per-launch event timing of exec_batch kernels (be_prof_enable); off on the hot path
+  struct ProfRec {
+    be_prof_rec r;
+    cudaEvent_t a, b;
+  };
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;
+  size_t prof_ev_used = 0;
+  std::vector<ProfRec> prof_recs;
 };
 
 struct be_block {
@@ -235,6 +244,7 @@ extern "C" int be_ctx_destroy(be_ctx* ctx) {
   if (ctx == nullptr) return BE_ERR_INVALID;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (cudaEvent_t ev : ctx->prof_ev) cudaEventDestroy(ev);
   if (ctx->gemm_ws) cudaFree(ctx->gemm_ws);
   if (ctx->gemm_counters) cudaFree(ctx->gemm_counters);
   cudaStreamDestroy(ctx->stream);
@@ -513,6 +523,73 @@ extern "C" int be_workspace_free(be_workspace* w) {
   return BE_OK;
 }
 
+// ------------------------------------------------------------------------------ profiling
+namespace {
+
+cudaEvent_t prof_event(be_ctx* ctx) {
+  if (ctx->prof_ev_used == ctx->prof_ev.size()) {
+    cudaEvent_t ev;
+    if (cudaEventCreate(&ev) != cudaSuccess) return nullptr;
+    ctx->prof_ev.push_back(ev);
+  }
+  return ctx->prof_ev[ctx->prof_ev_used++];
+}
+
+// Brackets one launch with events on its stream when profiling is on.
+struct ProfScope {
+  be_ctx* ctx;
+  cudaStream_t st;
+  int idx = -1;
+  ProfScope(be_ctx* c, cudaStream_t s, int cls, int ntok, int N, int K) : ctx(c), st(s) {
+    if (!ctx->prof) return;
+    cudaEvent_t a = prof_event(ctx), b = prof_event(ctx);
+    if (a == nullptr || b == nullptr) return;
+    be_ctx::ProfRec rec{};
+    rec.r.cls = cls;
+    rec.r.ntok = ntok;
+    rec.r.n = N;
+    rec.r.k = K;
+    rec.a = a;
+    rec.b = b;
+    cudaEventRecord(a, st);
+    idx = (int)ctx->prof_recs.size();
+    ctx->prof_recs.push_back(rec);
+  }
+  ~ProfScope() {
+    if (idx >= 0) cudaEventRecord(ctx->prof_recs[idx].b, st);
+  }
+};
+
+}  // namespace
+
+extern "C" int be_prof_enable(be_ctx* ctx, int on) {
+  if (ctx == nullptr) return BE_ERR_INVALID;
+  ctx->prof = on != 0;
+  ctx->prof_recs.clear();
+  ctx->prof_ev_used = 0;
+  return BE_OK;
+}
+
+extern "C" int be_prof_active(const be_ctx* ctx) { return ctx != nullptr && ctx->prof ? 1 : 0; }
+
+extern "C" int be_prof_read(be_ctx* ctx, be_prof_rec* out, int cap, int* n_out) {
+  if (ctx == nullptr || n_out == nullptr || (cap > 0 && out == nullptr)) return BE_ERR_INVALID;
+  BE_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const int n = (int)ctx->prof_recs.size();
+  *n_out = n;
+  if (cap < n) return BE_OK;  // size query
+  for (int i = 0; i < n; ++i) {
+    auto& rec = ctx->prof_recs[i];
+    float ms = 0.f;
+    BE_CUDA(ctx, cudaEventElapsedTime(&ms, rec.a, rec.b));
+    out[i] = rec.r;
+    out[i].ms = ms;
+  }
+  ctx->prof_recs.clear();
+  ctx->prof_ev_used = 0;
+  return BE_OK;
+}
+
 // ------------------------------------------------------------------------------ execution
 namespace {
 
@@ -558,7 +635,10 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
   cudaError_t e;
 
   // K1: gather the members' input rows into the batch (fp32 residual + bf16 shadow)
-  e = bx::launch_gather(static_cast<const bf16*>(arena_in), tok + 0, 5, ntok, d, ws->Xb, ws->X, st);
+  {
+    ProfScope ps(ctx, st, BE_K_GATHER, ntok, d, 0);
+    e = bx::launch_gather(static_cast<const bf16*>(arena_in), tok + 0, 5, ntok, d, ws->Xb, ws->X, st);
+  }
   if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
 
   const int max_pages = pt_stride;
@@ -572,7 +652,10 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     if (kind == 'f') {
       // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
       const auto& L = blk->layers[jf++];
-      e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
+      {
+        ProfScope ps(ctx, st, BE_K_RMS, ntok, d, 0);
+        e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
+      }
       if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
       EpiParams eg{};
       eg.mode = bx::kSwiGLU;
@@ -580,20 +663,31 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
       eg.rstd = ws->rstd;
       eg.out = ws->h;
       eg.ldo = F;
-      if ((rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st)) != BE_OK) return rc;
+      {
+        ProfScope ps(ctx, st, BE_K_GEMM_GATE_UP, ntok, 2 * F, d);
+        rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st);
+      }
+      if (rc != BE_OK) return rc;
       EpiParams ed{};
       ed.mode = bx::kResid;
       ed.ntok = ntok;
       ed.xres = ws->X;
       ed.xres_b = ws->Xb;
       ed.ldr = d;
-      if ((rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st)) != BE_OK) return rc;
+      {
+        ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F);
+        rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st);
+      }
+      if (rc != BE_OK) return rc;
       continue;
     }
     const int l = ia++;
     const auto& L = blk->layers[l];
     // ---- attention component: RMSNorm (fused) -> QKV + RoPE + KV append -> paged attn -> O + residual
-    e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
+    {
+      ProfScope ps(ctx, st, BE_K_RMS, ntok, d, 0);
+      e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
+    }
     if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
     EpiParams eq{};
     eq.mode = bx::kQKV;
@@ -609,7 +703,11 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eq.d_model = d;
     eq.head_dim = hd;
     eq.rope = blk->rope;
-    if ((rc = run_gemm(ctx, ws, L.wqkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st)) != BE_OK) return rc;
+    {
+      ProfScope ps(ctx, st, BE_K_GEMM_QKV, ntok, 3 * d, d);
+      rc = run_gemm(ctx, ws, L.wqkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st);
+    }
+    if (rc != BE_OK) return rc;
 
     bx::AttnParams ap{};
     ap.q = ws->q;
@@ -628,7 +726,10 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     ap.out = ws->attn;
     ap.part = ws->attn_part;
     ap.splits = splits;
-    e = bx::launch_attention(ap, ntok, hd, st);
+    {
+      ProfScope ps(ctx, st, BE_K_ATTENTION, ntok, H, hd);
+      e = bx::launch_attention(ap, ntok, hd, st);
+    }
     if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "attention: %s", cudaGetErrorString(e));
 
     EpiParams eo{};
@@ -637,10 +738,17 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eo.xres = ws->X;
     eo.xres_b = ws->Xb;
     eo.ldr = d;
-    if ((rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st)) != BE_OK) return rc;
+    {
+      ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d);
+      rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st);
+    }
+    if (rc != BE_OK) return rc;
   }
   // K2: scatter the block outputs to their next-hop rows
-  e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st);
+  {
+    ProfScope ps(ctx, st, BE_K_SCATTER, ntok, d, 0);
+    e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st);
+  }
   if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "scatter: %s", cudaGetErrorString(e));
   return BE_OK;
 }

@@ -603,7 +603,10 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
              reinterpret_cast<const int32_t*>(meta_dev_ + off_pt[i]));
   };
   stats.graph_replayed = 0;
-  if (use_graphs_ && sig == gs.sig && gs.exec != nullptr) {
+  if (be_prof_active(ctx_)) {
+    launch_all();  // per-launch event timing: plain launches, the captured graph is kept
+    if (sig != gs.sig) gs.reset();
+  } else if (use_graphs_ && sig == gs.sig && gs.exec != nullptr) {
     ck(cudaGraphLaunch(gs.exec, st_), "graph launch");
     stats.graph_replayed = 1;
   } else if (use_graphs_ && sig == gs.sig) {

@@ -55,6 +55,15 @@ def _ptr(t) -> C.c_void_p:
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
 
 
+PROF_CLASSES = ["gather", "rms", "gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down",
+                "scatter"]
+
+
+class ProfRec(C.Structure):
+    _fields_ = [("cls", C.c_int32), ("ntok", C.c_int32), ("n", C.c_int32), ("k", C.c_int32),
+                ("ms", C.c_float)]
+
+
 class Context:
     def __init__(self, device: int = 0):
         self.device = device
@@ -74,6 +83,18 @@ class Context:
 
     def sync(self) -> None:
         check(lib().be_synchronize(self.h), self.h)
+
+    def prof_enable(self, on: bool = True) -> None:
+        """Per-launch event timing of exec_batch kernels (include/blockexec.h be_prof_*)."""
+        check(lib().be_prof_enable(self.h, 1 if on else 0), self.h)
+
+    def prof_read(self) -> list[dict]:
+        n = C.c_int(0)
+        check(lib().be_prof_read(self.h, None, 0, C.byref(n)), self.h)
+        recs = (ProfRec * max(1, n.value))()
+        check(lib().be_prof_read(self.h, C.cast(recs, C.c_void_p), n.value, C.byref(n)), self.h)
+        return [{"cls": PROF_CLASSES[r.cls], "ntok": r.ntok, "n": r.n, "k": r.k, "ms": r.ms}
+                for r in recs[:n.value]]
 
     def close(self) -> None:
         if self.h:
