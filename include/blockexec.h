@@ -123,7 +123,7 @@ int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_tokens, int p
  * context stream and returns (and clears) the records; with cap < n only *n_out is written. */
 enum {
   BE_K_GATHER = 0,
-  BE_K_RMS = 1,
+  BE_K_RMS = 1, /* reserved: the RMSNorm statistics are fused into gather / residual epilogues */
   BE_K_GEMM_QKV = 2,
   BE_K_ATTENTION = 3, /* decode/prefill attention (+ split combine); n = heads, k = head_dim */
   BE_K_GEMM_O = 4,

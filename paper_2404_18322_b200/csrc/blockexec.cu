@@ -20,9 +20,8 @@
 
 namespace bx {
 // rowops.cu
-cudaError_t launch_gather(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, float*, cudaStream_t);
+cudaError_t launch_gather(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, float*, float*, cudaStream_t);
 cudaError_t launch_scatter(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, cudaStream_t);
-cudaError_t launch_rms_stats(const float*, int, int, float, float*, cudaStream_t);
 cudaError_t launch_cosine(const __nv_bfloat16*, const __nv_bfloat16*, int, int, float, float*, int*, cudaStream_t);
 cudaError_t launch_synth_weight(__nv_bfloat16*, int, int, uint64_t, uint64_t, float, int, int, const float*, cudaStream_t);
 cudaError_t launch_synth_rows(__nv_bfloat16*, long long, uint64_t, float, cudaStream_t);
@@ -110,7 +109,7 @@ struct be_workspace {
   bf16* q = nullptr;
   bf16* attn = nullptr;
   bf16* h = nullptr;
-  float* rstd = nullptr;
+  float* ss = nullptr;  // [max_tok][d / 32] sums of squares of the residual stream (fused RMSNorm)
   float* splitws = nullptr;
   size_t splitws_elems = 0;
   int* counters = nullptr;
@@ -282,6 +281,7 @@ extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out
     return fail(ctx, BE_ERR_INVALID, "block: inconsistent shape");
   if (d->d_model % 128 != 0 || d->d_ff % 64 != 0 || (2 * d->d_ff) % 128 != 0)
     return fail(ctx, BE_ERR_INVALID, "block: d_model %% 128 and d_ff %% 64 required");
+  if (d->d_model > 8192) return fail(ctx, BE_ERR_INVALID, "block: d_model <= 8192 required");
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(ctx, BE_ERR_INVALID, "block: head_dim must be 64 or 128");
   if (d->max_pos <= 0) return fail(ctx, BE_ERR_INVALID, "block: max_pos must be positive");
@@ -475,7 +475,7 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
   ok &= cudaMalloc(&w->q, T * d * sizeof(bf16)) == cudaSuccess;
   ok &= cudaMalloc(&w->attn, T * d * sizeof(bf16)) == cudaSuccess;
   ok &= cudaMalloc(&w->h, T * dff * sizeof(bf16)) == cudaSuccess;
-  ok &= cudaMalloc(&w->rstd, T * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&w->ss, T * (d / 32) * sizeof(float)) == cudaSuccess;
   w->splitws_elems = (size_t)16 << 20;  // 64 MB of fp32 split-K partials (L2 sized)
   ok &= cudaMalloc(&w->splitws, w->splitws_elems * sizeof(float)) == cudaSuccess;
   w->n_counters = 1 << 16;
@@ -515,7 +515,7 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
 extern "C" int be_workspace_free(be_workspace* w) {
   if (w == nullptr) return BE_ERR_INVALID;
   cudaSetDevice(w->ctx->device);
-  void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->rstd, w->splitws, w->counters,
+  void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->ss, w->splitws, w->counters,
                   w->attn_part, w->d_tokens, w->d_pt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -637,7 +637,8 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
   // K1: gather the members' input rows into the batch (fp32 residual + bf16 shadow)
   {
     ProfScope ps(ctx, st, BE_K_GATHER, ntok, d, 0);
-    e = bx::launch_gather(static_cast<const bf16*>(arena_in), tok + 0, 5, ntok, d, ws->Xb, ws->X, st);
+    e = bx::launch_gather(static_cast<const bf16*>(arena_in), tok + 0, 5, ntok, d, ws->Xb, ws->X,
+                          ws->ss, st);
   }
   if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
 
@@ -652,15 +653,12 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     if (kind == 'f') {
       // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
       const auto& L = blk->layers[jf++];
-      {
-        ProfScope ps(ctx, st, BE_K_RMS, ntok, d, 0);
-        e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
-      }
-      if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
       EpiParams eg{};
       eg.mode = bx::kSwiGLU;
       eg.ntok = ntok;
-      eg.rstd = ws->rstd;
+      eg.ss_in = ws->ss;
+      eg.ss_groups = d / 32;
+      eg.norm_eps = D.norm_eps;
       eg.out = ws->h;
       eg.ldo = F;
       {
@@ -674,6 +672,8 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
       ed.xres = ws->X;
       ed.xres_b = ws->Xb;
       ed.ldr = d;
+      ed.ss_out = ws->ss;  // the next component's RMSNorm statistics
+      ed.ss_groups = d / 32;
       {
         ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F);
         rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st);
@@ -684,15 +684,12 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     const int l = ia++;
     const auto& L = blk->layers[l];
     // ---- attention component: RMSNorm (fused) -> QKV + RoPE + KV append -> paged attn -> O + residual
-    {
-      ProfScope ps(ctx, st, BE_K_RMS, ntok, d, 0);
-      e = bx::launch_rms_stats(ws->X, ntok, d, D.norm_eps, ws->rstd, st);
-    }
-    if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rms: %s", cudaGetErrorString(e));
     EpiParams eq{};
     eq.mode = bx::kQKV;
     eq.ntok = ntok;
-    eq.rstd = ws->rstd;
+    eq.ss_in = ws->ss;
+    eq.ss_groups = d / 32;
+    eq.norm_eps = D.norm_eps;
     eq.out = ws->q;
     eq.ldo = d;
     eq.tok = tok;
@@ -738,6 +735,8 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eo.xres = ws->X;
     eo.xres_b = ws->Xb;
     eo.ldr = d;
+    eo.ss_out = ws->ss;
+    eo.ss_groups = d / 32;
     {
       ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d);
       rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st);
@@ -808,8 +807,9 @@ extern "C" int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_to
                                       int pt_stride) {
   if (ctx == nullptr || blk == nullptr || n_tokens <= 0) return 0;
   const int splits = attn_splits(ctx, n_tokens, blk->desc.n_heads, pt_stride);
-  // gather + scatter; attention: rms, qkv, attention (+combine), o; ffn: rms, gate/up, down
-  return 2 + blk->n_att * (4 + (splits > 1 ? 1 : 0)) + blk->n_ffn * 3;
+  // gather + scatter; attention: qkv, attention (+combine), o; ffn: gate/up, down (the RMSNorms
+  // are fused: statistics from the residual producer, scale in the consumer's epilogue)
+  return 2 + blk->n_att * (3 + (splits > 1 ? 1 : 0)) + blk->n_ffn * 2;
 }
 
 // ------------------------------------------------------------------------------ row kernels
@@ -817,7 +817,8 @@ extern "C" int be_gather_rows(be_ctx* ctx, const void* arena, const int32_t* src
                               void* out, void* stream) {
   if (ctx == nullptr || rows < 0 || d % 8 != 0) return BE_ERR_INVALID;
   cudaError_t e = bx::launch_gather(static_cast<const bf16*>(arena), src, 1, rows, d,
-                                    static_cast<bf16*>(out), nullptr, pick_stream(ctx, stream));
+                                    static_cast<bf16*>(out), nullptr, nullptr,
+                                    pick_stream(ctx, stream));
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
 }
 

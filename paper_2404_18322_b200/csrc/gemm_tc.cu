@@ -40,35 +40,75 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // (all lanes of a warp share t0; lanes hold consecutive features). Stores are vectorised across
 // lane pairs: for token pair (2p, 2p+1) one shuffle gives the even lane features (f, f+1) of
 // token 2p and the odd lane features (f-1, f) of token 2p+1, so every store is a bf16x2 / float2.
+// rs: the chunk's 16 per-token RMSNorm scales (shared memory), nullptr = no norm.
 template <int MODE>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0, float (&v)[16]) {
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0, float (&v)[16],
+                                               const float* rs) {
   const int lane = threadIdx.x & 31;
   const bool odd = (lane & 1) != 0;
   const int nvalid = E.ntok - t0 < 16 ? E.ntok - t0 : 16;  // warp-uniform, >= 1
-  if (MODE != kQKV && E.rstd != nullptr) {
+  if (MODE != kQKV && rs != nullptr) {
     // fused RMSNorm row scale (gamma folded into the weights)
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < nvalid) v[i] *= __ldg(E.rstd + t0 + i);
+    for (int i = 0; i < 16; ++i) v[i] *= rs[i];
   }
   if constexpr (MODE == kStore || MODE == kResid) {
     const int fe = f & ~1;
+    float sq[8];  // kResid: this lane's x^2 + x'^2 of token pair p
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[2 * p] : v[2 * p + 1], 1);
       const float lo = odd ? recv : v[2 * p];
       const float hi = odd ? v[2 * p + 1] : recv;
       const int t = t0 + 2 * p + (odd ? 1 : 0);
-      if (2 * p + (odd ? 1 : 0) >= nvalid) continue;
+      const bool valid = 2 * p + (odd ? 1 : 0) < nvalid;
       if constexpr (MODE == kStore) {
-        *reinterpret_cast<uint32_t*>(E.out + (size_t)t * E.ldo + fe) = pack_bf16x2(lo, hi);
+        if (valid)
+          *reinterpret_cast<uint32_t*>(E.out + (size_t)t * E.ldo + fe) = pack_bf16x2(lo, hi);
       } else {
-        float2* px = reinterpret_cast<float2*>(E.xres + (size_t)t * E.ldr + fe);
-        float2 x = *px;
-        x.x += lo;
-        x.y += hi;
-        *px = x;
-        *reinterpret_cast<uint32_t*>(E.xres_b + (size_t)t * E.ldr + fe) = pack_bf16x2(x.x, x.y);
+        sq[p] = 0.f;
+        if (valid) {
+          float2* px = reinterpret_cast<float2*>(E.xres + (size_t)t * E.ldr + fe);
+          float2 x = *px;
+          x.x += lo;
+          x.y += hi;
+          *px = x;
+          *reinterpret_cast<uint32_t*>(E.xres_b + (size_t)t * E.ldr + fe) = pack_bf16x2(x.x, x.y);
+          sq[p] = x.x * x.x + x.y * x.y;
+        }
+      }
+    }
+    if constexpr (MODE == kResid) {
+      if (E.ss_out != nullptr) {
+        // Sum of squares per token over the warp's 32 features: token 2p + parity lives in the 16
+        // lanes of that parity. Transposed butterfly: each xor step halves the values a lane
+        // keeps (8 shuffles in all, fixed order), ending with lane bits 4..2 naming p.
+        const unsigned full = 0xffffffffu;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool up = lane & 16;
+          const float send = up ? sq[i] : sq[i + 4];
+          const float keep = up ? sq[i + 4] : sq[i];
+          sq[i] = keep + __shfl_xor_sync(full, send, 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const bool up = lane & 8;
+          const float send = up ? sq[i] : sq[i + 2];
+          const float keep = up ? sq[i + 2] : sq[i];
+          sq[i] = keep + __shfl_xor_sync(full, send, 8);
+        }
+        {
+          const bool up = lane & 4;
+          const float send = up ? sq[0] : sq[1];
+          const float keep = up ? sq[1] : sq[0];
+          sq[0] = keep + __shfl_xor_sync(full, send, 4);
+        }
+        sq[0] += __shfl_xor_sync(full, sq[0], 2);
+        const int p = ((lane >> 2) & 1) | (((lane >> 3) & 1) << 1) | (((lane >> 4) & 1) << 2);
+        const int ti = 2 * p + (odd ? 1 : 0);
+        if ((lane & 2) == 0 && ti < nvalid)
+          E.ss_out[(size_t)(t0 + ti) * E.ss_groups + (f >> 5)] = sq[0];
       }
     }
   } else if constexpr (MODE == kSwiGLU) {
@@ -93,9 +133,10 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
     const bool have = ti_l < nvalid;
     const int my_slot = have ? __ldg(E.tok + (size_t)(t0 + ti_l) * 5 + 2) : 0;
     const int my_pos = have ? __ldg(E.tok + (size_t)(t0 + ti_l) * 5 + 3) : 0;
-    const float my_rs = (have && E.rstd != nullptr) ? __ldg(E.rstd + t0 + ti_l) : 1.f;
+    if (rs != nullptr) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] *= __shfl_sync(0xffffffffu, my_rs, i);
+      for (int i = 0; i < 16; ++i) v[i] *= rs[i];
+    }
     if (sec < 2) {
       // rows are pair-interleaved per head: even = dim j, odd = dim j + hd/2 (rotate_half)
 #pragma unroll
@@ -131,6 +172,40 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
   }
 }
 
+// rs[j] = 1/sqrt(sum_g ss[n0 + j][g] / d + eps) for the BN tokens of a tile; warp q of the four
+// epilogue warps takes tokens q, q+4, ...; each lane sums groups lane, lane+32, ... then the warp
+// reduces in a fixed order (bit-reproducible).
+// All loads are issued before any reduction (one L2 round trip): a token's groups are read as
+// float4s, lane l taking float4s l and l + 32 (ss_groups <= 256, i.e. d_model <= 8192).
+template <int BN>
+__device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, float* rs) {
+  const int lane = threadIdx.x & 31;
+  const int G = E.ss_groups;
+  const int G4 = G >> 2;
+  const float inv_d = 1.0f / (float)(G * 32);
+  constexpr int J = BN / 4;  // tokens per warp
+  float s[J];
+#pragma unroll
+  for (int jj = 0; jj < J; ++jj) {
+    const int t = n0 + q + 4 * jj;
+    const float4* p = reinterpret_cast<const float4*>(E.ss_in + (size_t)t * G);
+    const bool ok = t < E.ntok;
+    const float4 a = (ok && lane < G4) ? __ldcg(p + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = (ok && lane + 32 < G4) ? __ldcg(p + lane + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s[jj] = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) s[jj] += __shfl_xor_sync(0xffffffffu, s[jj], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj)
+      rs[q + 4 * jj] = n0 + q + 4 * jj < E.ntok ? rsqrtf(s[jj] * inv_d + E.norm_eps) : 0.f;
+  }
+}
+
 struct SkRange {
   long long total;  // iterations = tiles * nkb
   int G;            // CTAs
@@ -160,7 +235,7 @@ __global__ void __launch_bounds__(192, CTAS)
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* flag = reinterpret_cast<int*>(tmem_holder + 1);
+  float* rs_smem = reinterpret_cast<float*>(tmem_holder + 4);  // [2][BN] per-token rstd
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -278,18 +353,27 @@ __global__ void __launch_bounds__(192, CTAS)
       const int f = m0 + q * 32 + lane;
       const int a = seg & 1;
       const uint32_t u = (uint32_t)(seg >> 1);
+      const bool whole = kb0 == 0 && kb1 == nkb;
+      const bool runs_epilogue = whole || (int)blockIdx.x == R.cta_of((long long)tile * nkb);
+      float* rs = nullptr;
+      if (E.ss_in != nullptr && runs_epilogue) {
+        // the norm statistics of this tile's tokens, computed under the mainloop
+        rs = rs_smem + (seg & 1) * BN;
+        tile_rstd<BN>(E, n0, q, rs);
+        named_bar_sync(2, 128);
+      }
       mbar_wait(&tfull[a], u & 1u);
       tc_fence_after();
       if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
       __syncwarp();
       const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
-      if (kb0 == 0 && kb1 == nkb) {
+      if (whole) {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           if (n0 + c0 >= E.ntok) break;
           float acc[16];
           tmem_ld16(t_lane + c0, acc);
-          epilogue_chunk<MODE>(E, f, n0 + c0, acc);
+          epilogue_chunk<MODE>(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr);
         }
       } else {
         // Partial tile. Its owner is the CTA holding the tile's first k-block (c_first): for
@@ -357,7 +441,8 @@ __global__ void __launch_bounds__(192, CTAS)
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 16) {
               if (n0 + c0 >= E.ntok) break;
-              epilogue_chunk<MODE>(E, f, n0 + c0, *reinterpret_cast<float(*)[16]>(acc + c0));
+              epilogue_chunk<MODE>(E, f, n0 + c0, *reinterpret_cast<float(*)[16]>(acc + c0),
+                                   rs ? rs + c0 : nullptr);
             }
           } else {
 #pragma unroll 1
@@ -387,7 +472,7 @@ __global__ void __launch_bounds__(192, CTAS)
                 }
               }
             }
-            epilogue_chunk<MODE>(E, f, n0 + c0, acc);
+            epilogue_chunk<MODE>(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr);
           }
           }
         }
@@ -410,7 +495,8 @@ template <int BN, int MODE>
 static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   constexpr int STAGES = gemm_stages_deep<BN>();
   constexpr int CTAS = 1;
-  constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
+                       2 * BN * 4 /*rstd*/;
   auto kern = gemm_sk_kernel<BN, STAGES, CTAS, MODE>;
   static bool configured = false;
   if (!configured) {

@@ -7,7 +7,8 @@
 //   kSwiGLU  h = silu(gate) * up  (gate/up rows interleaved)   (FFN gate/up)
 //   kQKV     RoPE(q,k) + q store + paged KV append of k, v     (attention input proj)
 // The RMSNorm of the input row is fused as a per-token scale (rstd) applied to acc; the norm
-// weight gamma is folded into W at load time. Split-K partials meet in an fp32 workspace
+// weight gamma is folded into W at load time; the per-token statistics come from the producer of
+// the residual stream (see ss_in / ss_out), so no separate norm kernel runs. Split-K partials meet in an fp32 workspace
 // (L2 resident) and the last CTA of a tile runs the epilogue.
 #pragma once
 #include <cuda.h>
@@ -20,7 +21,13 @@ enum EpiMode : int { kStore = 0, kResid = 1, kSwiGLU = 2, kQKV = 3 };
 struct EpiParams {
   int mode;
   int ntok;                // valid tokens (columns)
-  const float* rstd;       // [ntok] fused RMSNorm row scale, nullptr -> 1
+  // fused RMSNorm without a stats kernel: the producer of the residual stream (gather, or a
+  // kResid epilogue) writes per-(token, 32-feature group) sums of squares ss[t][g]; a GEMM with
+  // ss_in reduces them to rstd[t] = 1/sqrt(sum/d + eps) before its first accumulator is ready
+  const float* ss_in;      // [ntok][ss_groups] or nullptr (no norm)
+  float* ss_out;           // kResid: [ntok][ss_groups] written for the next component, or nullptr
+  int ss_groups;           // d_model / 32
+  float norm_eps;
   __nv_bfloat16* out;      // kStore/kSwiGLU/kQKV(q): [ntok][ldo]
   int ldo;
   float* xres;             // kResid: fp32 residual stream [ntok][ldr]
