@@ -258,7 +258,7 @@ def profile_step(ctx, run, wl, stream, peaks, peaks_kind):
     for r in recs:
         c, m, n, k = r["cls"], r["ntok"], r["n"], r["k"]
         if c.startswith("gemm"):
-            b, fl, f = 2 * (n * k + m * k + m * n), 2 * m * n * k, "gemm"
+            b, fl, f = r["bytes"], r["flops"], "gemm"
         elif c == "attention":
             b = st["kv_bytes"] * m / max(1, attn_rows) + 2 * 2 * m * n * k
             fl, f = 0, "attention"

@@ -137,10 +137,26 @@ typedef struct {
   int32_t n;    /* GEMM output features (rows of W), d_model for row kernels */
   int32_t k;    /* GEMM reduction dim */
   float ms;     /* event-timed duration */
+  double bytes; /* algorithmic bytes (GEMM: 2(NK + MK + MN) per GEMM); 0 = caller computes */
+  double flops; /* algorithmic flops (2 MNK per GEMM) */
 } be_prof_rec;
 int be_prof_enable(be_ctx* ctx, int on);
 int be_prof_active(const be_ctx* ctx);
 int be_prof_read(be_ctx* ctx, be_prof_rec* out, int cap, int* n_out);
+
+/* Kernel timeline inside graph replays (PDL overlap included): while enabled (cap slots), every
+ * exec_batch kernel records globaltimer ns of its first/last CTA start, first dependency release
+ * (griddepcontrol.wait return) and last CTA end into its slot. be_timeline_begin resets the
+ * window and restarts slot numbering at the next launch (graphs captured in a window keep their
+ * slots); be_timeline_read synchronises and returns the written slots in slot order. */
+typedef struct {
+  int32_t slot;
+  int32_t cls; /* BE_K_* */
+  uint64_t start_first, start_last, go_first, end_last;
+} be_timeline_rec;
+int be_timeline_enable(be_ctx* ctx, int cap);
+int be_timeline_begin(be_ctx* ctx);
+int be_timeline_read(be_ctx* ctx, be_timeline_rec* out, int cap, int* n_out);
 
 /* K1 / K2 standalone: routing-table gather and scatter of bf16 rows. */
 int be_gather_rows(be_ctx* ctx, const void* d_arena, const int32_t* d_src, int rows, int d,

@@ -84,6 +84,9 @@ def lib() -> C.CDLL:
         "be_prof_enable": (I, [P, I]),
         "be_prof_active": (I, [P]),
         "be_prof_read": (I, [P, P, I, P]),
+        "be_timeline_enable": (I, [P, I]),
+        "be_timeline_begin": (I, [P]),
+        "be_timeline_read": (I, [P, P, I, P]),
         "be_attention": (I, [P, P, P, I, I, I, I, P, I, P, P, I, I, P, P]),
     }
     for name, (res, args) in sig.items():

@@ -16,6 +16,8 @@
 #include <cstdint>
 #include <cfloat>
 
+#include "ptx.cuh"
+
 namespace bx {
 
 struct AttnParams {
@@ -35,6 +37,8 @@ struct AttnParams {
   __nv_bfloat16* out;         // [rows][H*hd]
   float* part;                // [rows][H][splits][hd + 2] partials when splits > 1
   int splits;
+  unsigned long long* tl;     // diagnostics: timeline slots of decode and combine (or nullptr)
+  int tl_cap;
 };
 
 template <int HD>
@@ -49,6 +53,10 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams P) {
   const int lane = threadIdx.x & 31;
   const int sub = lane % LPT;      // which 8-dim chunk
   const int tg = lane / LPT;       // token group inside a warp-load
+  if (threadIdx.x == 0) {
+    tl_start(P.tl, P.tl_cap);
+    tl_go(P.tl, P.tl_cap);
+  }
 
   const int ctx = P.row_ctx[(size_t)row * P.meta_stride] + P.ctx_add;
   const int npages = (ctx + 15) >> 4;
@@ -160,6 +168,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams P) {
       }
     }
   }
+  if (threadIdx.x == 0) tl_end(P.tl, P.tl_cap);
 }
 
 template <int HD>
@@ -167,6 +176,11 @@ __global__ void attn_combine_kernel(AttnParams P) {
   const int row = blockIdx.x;
   const int head = blockIdx.y;
   const int dim = threadIdx.x;
+  unsigned long long* tl = P.tl != nullptr ? P.tl + 1 : nullptr;  // the combine's own slot
+  if (dim == 0) {
+    tl_start(tl, P.tl_cap);
+    tl_go(tl, P.tl_cap);
+  }
   const float* pp = P.part + (((size_t)row * P.H + head) * P.splits) * (HD + 2);
   float M = -FLT_MAX;
   for (int s = 0; s < P.splits; ++s) M = fmaxf(M, pp[s * (HD + 2)]);
@@ -178,6 +192,7 @@ __global__ void attn_combine_kernel(AttnParams P) {
     O += pp[s * (HD + 2) + 2 + dim] * c;
   }
   P.out[(size_t)row * P.H * HD + head * HD + dim] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+  if (dim == 0) tl_end(tl, P.tl_cap);
 }
 
 cudaError_t launch_attention(const AttnParams& P, int rows, int head_dim, cudaStream_t stream) {

@@ -20,8 +20,10 @@
 
 namespace bx {
 // rowops.cu
-cudaError_t launch_gather(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, float*, float*, cudaStream_t);
-cudaError_t launch_scatter(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, cudaStream_t);
+cudaError_t launch_gather(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, float*, float*, cudaStream_t,
+                          unsigned long long*, int);
+cudaError_t launch_scatter(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, cudaStream_t,
+                           unsigned long long*, int);
 cudaError_t launch_cosine(const __nv_bfloat16*, const __nv_bfloat16*, int, int, float, float*, int*, cudaStream_t);
 cudaError_t launch_synth_weight(__nv_bfloat16*, int, int, uint64_t, uint64_t, float, int, int, const float*, cudaStream_t);
 cudaError_t launch_synth_rows(__nv_bfloat16*, long long, uint64_t, float, cudaStream_t);
@@ -45,6 +47,8 @@ struct AttnParams {
   __nv_bfloat16* out;
   float* part;
   int splits;
+  unsigned long long* tl;
+  int tl_cap;
 };
 cudaError_t launch_attention(const AttnParams&, int rows, int head_dim, cudaStream_t);
 }  // namespace bx
@@ -71,6 +75,11 @@ struct be_ctx {
     be_prof_rec r;
     cudaEvent_t a, b;
   };
+  // kernel timeline (be_timeline_*): [4][tl_cap] u64 on the device, slots in launch order
+  unsigned long long* tl = nullptr;
+  int tl_cap = 0;
+  int tl_next = 0;
+  std::vector<int> tl_cls;
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;
   size_t prof_ev_used = 0;
@@ -244,6 +253,7 @@ extern "C" int be_ctx_destroy(be_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t ev : ctx->prof_ev) cudaEventDestroy(ev);
+  if (ctx->tl) cudaFree(ctx->tl);
   if (ctx->gemm_ws) cudaFree(ctx->gemm_ws);
   if (ctx->gemm_counters) cudaFree(ctx->gemm_counters);
   cudaStreamDestroy(ctx->stream);
@@ -540,7 +550,9 @@ struct ProfScope {
   be_ctx* ctx;
   cudaStream_t st;
   int idx = -1;
-  ProfScope(be_ctx* c, cudaStream_t s, int cls, int ntok, int N, int K) : ctx(c), st(s) {
+  ProfScope(be_ctx* c, cudaStream_t s, int cls, int ntok, int N, int K, double bytes,
+            double flops)
+      : ctx(c), st(s) {
     if (!ctx->prof) return;
     cudaEvent_t a = prof_event(ctx), b = prof_event(ctx);
     if (a == nullptr || b == nullptr) return;
@@ -549,6 +561,8 @@ struct ProfScope {
     rec.r.ntok = ntok;
     rec.r.n = N;
     rec.r.k = K;
+    rec.r.bytes = bytes;
+    rec.r.flops = flops;
     rec.a = a;
     rec.b = b;
     cudaEventRecord(a, st);
@@ -560,7 +574,67 @@ struct ProfScope {
   }
 };
 
+
+
+// next timeline slot for a launch of class cls (nullptr when the timeline is off or full)
+unsigned long long* tl_slot(be_ctx* ctx, int cls) {
+  if (ctx->tl == nullptr || ctx->tl_next >= ctx->tl_cap) return nullptr;
+  const int s = ctx->tl_next++;
+  if ((int)ctx->tl_cls.size() <= s) ctx->tl_cls.resize(s + 1);
+  ctx->tl_cls[s] = cls;
+  return ctx->tl + s;
+}
+
 }  // namespace
+
+extern "C" int be_timeline_enable(be_ctx* ctx, int cap) {
+  if (ctx == nullptr || cap < 0) return BE_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  BE_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->tl) cudaFree(ctx->tl);
+  ctx->tl = nullptr;
+  ctx->tl_cap = 0;
+  ctx->tl_next = 0;
+  ctx->tl_cls.clear();
+  if (cap == 0) return BE_OK;
+  BE_CUDA(ctx, cudaMalloc(&ctx->tl, (size_t)4 * cap * sizeof(unsigned long long)));
+  ctx->tl_cap = cap;
+  return BE_OK;
+}
+
+extern "C" int be_timeline_begin(be_ctx* ctx) {
+  if (ctx == nullptr || ctx->tl == nullptr) return BE_ERR_INVALID;
+  ctx->tl_next = 0;
+  const size_t n = (size_t)ctx->tl_cap * sizeof(unsigned long long);
+  BE_CUDA(ctx, cudaMemsetAsync(ctx->tl, 0xff, n, ctx->stream));                    // min start
+  BE_CUDA(ctx, cudaMemsetAsync(ctx->tl + ctx->tl_cap, 0, n, ctx->stream));         // max start
+  BE_CUDA(ctx, cudaMemsetAsync(ctx->tl + 2 * ctx->tl_cap, 0xff, n, ctx->stream));  // min go
+  BE_CUDA(ctx, cudaMemsetAsync(ctx->tl + 3 * ctx->tl_cap, 0, n, ctx->stream));     // max end
+  return BE_OK;
+}
+
+extern "C" int be_timeline_read(be_ctx* ctx, be_timeline_rec* out, int cap, int* n_out) {
+  if (ctx == nullptr || n_out == nullptr || ctx->tl == nullptr) return BE_ERR_INVALID;
+  BE_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::vector<unsigned long long> h((size_t)4 * ctx->tl_cap);
+  BE_CUDA(ctx, cudaMemcpy(h.data(), ctx->tl, h.size() * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost));
+  int n = 0;
+  for (int s = 0; s < ctx->tl_cap && s < (int)ctx->tl_cls.size(); ++s) {
+    if (h[3 * ctx->tl_cap + s] == 0) continue;  // slot not written in this window
+    if (out != nullptr && n < cap) {
+      out[n].slot = s;
+      out[n].cls = ctx->tl_cls[s];
+      out[n].start_first = h[s];
+      out[n].start_last = h[ctx->tl_cap + s];
+      out[n].go_first = h[2 * ctx->tl_cap + s];
+      out[n].end_last = h[3 * ctx->tl_cap + s];
+    }
+    ++n;
+  }
+  *n_out = n;
+  return BE_OK;
+}
 
 extern "C" int be_prof_enable(be_ctx* ctx, int on) {
   if (ctx == nullptr) return BE_ERR_INVALID;
@@ -592,6 +666,11 @@ extern "C" int be_prof_read(be_ctx* ctx, be_prof_rec* out, int cap, int* n_out) 
 
 // ------------------------------------------------------------------------------ execution
 namespace {
+
+// algorithmic bytes of one GEMM: weights + activations in + outputs
+double gemm_bytes(int N, int K, int ntok) {
+  return 2.0 * ((double)N * K + (double)ntok * K + (double)ntok * N);
+}
 
 int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensorMap* mx, int N,
              int K, int ntok, int bn, EpiParams epi, cudaStream_t st) {
@@ -636,9 +715,9 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
 
   // K1: gather the members' input rows into the batch (fp32 residual + bf16 shadow)
   {
-    ProfScope ps(ctx, st, BE_K_GATHER, ntok, d, 0);
+    ProfScope ps(ctx, st, BE_K_GATHER, ntok, d, 0, 8.0 * ntok * d, 0);
     e = bx::launch_gather(static_cast<const bf16*>(arena_in), tok + 0, 5, ntok, d, ws->Xb, ws->X,
-                          ws->ss, st);
+                          ws->ss, st, tl_slot(ctx, BE_K_GATHER), ctx->tl_cap);
   }
   if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
 
@@ -662,7 +741,10 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
       eg.out = ws->h;
       eg.ldo = F;
       {
-        ProfScope ps(ctx, st, BE_K_GEMM_GATE_UP, ntok, 2 * F, d);
+        eg.tl = tl_slot(ctx, BE_K_GEMM_GATE_UP);
+        eg.tl_cap = ctx->tl_cap;
+        ProfScope ps(ctx, st, BE_K_GEMM_GATE_UP, ntok, 2 * F, d, gemm_bytes(2 * F, d, ntok),
+                     2.0 * (2 * F) * (d) * ntok);
         rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st);
       }
       if (rc != BE_OK) return rc;
@@ -675,7 +757,10 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
       ed.ss_out = ws->ss;  // the next component's RMSNorm statistics
       ed.ss_groups = d / 32;
       {
-        ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F);
+        ed.tl = tl_slot(ctx, BE_K_GEMM_DOWN);
+        ed.tl_cap = ctx->tl_cap;
+        ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F, gemm_bytes(d, F, ntok),
+                     2.0 * (d) * (F) * ntok);
         rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st);
       }
       if (rc != BE_OK) return rc;
@@ -701,7 +786,10 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eq.head_dim = hd;
     eq.rope = blk->rope;
     {
-      ProfScope ps(ctx, st, BE_K_GEMM_QKV, ntok, 3 * d, d);
+      eq.tl = tl_slot(ctx, BE_K_GEMM_QKV);
+        eq.tl_cap = ctx->tl_cap;
+        ProfScope ps(ctx, st, BE_K_GEMM_QKV, ntok, 3 * d, d, gemm_bytes(3 * d, d, ntok),
+                     2.0 * (3 * d) * (d) * ntok);
       rc = run_gemm(ctx, ws, L.wqkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st);
     }
     if (rc != BE_OK) return rc;
@@ -723,8 +811,11 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     ap.out = ws->attn;
     ap.part = ws->attn_part;
     ap.splits = splits;
+    ap.tl = tl_slot(ctx, BE_K_ATTENTION);
+    ap.tl_cap = ctx->tl_cap;
+    if (ap.tl != nullptr && splits > 1) tl_slot(ctx, BE_K_ATTENTION);  // combine's slot = tl + 1
     {
-      ProfScope ps(ctx, st, BE_K_ATTENTION, ntok, H, hd);
+      ProfScope ps(ctx, st, BE_K_ATTENTION, ntok, H, hd, 0, 0);
       e = bx::launch_attention(ap, ntok, hd, st);
     }
     if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "attention: %s", cudaGetErrorString(e));
@@ -738,15 +829,19 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     eo.ss_out = ws->ss;
     eo.ss_groups = d / 32;
     {
-      ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d);
+      eo.tl = tl_slot(ctx, BE_K_GEMM_O);
+        eo.tl_cap = ctx->tl_cap;
+        ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d, gemm_bytes(d, d, ntok),
+                     2.0 * (d) * (d) * ntok);
       rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st);
     }
     if (rc != BE_OK) return rc;
   }
   // K2: scatter the block outputs to their next-hop rows
   {
-    ProfScope ps(ctx, st, BE_K_SCATTER, ntok, d, 0);
-    e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st);
+    ProfScope ps(ctx, st, BE_K_SCATTER, ntok, d, 0, 4.0 * ntok * d, 0);
+    e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st,
+                           tl_slot(ctx, BE_K_SCATTER), ctx->tl_cap);
   }
   if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "scatter: %s", cudaGetErrorString(e));
   return BE_OK;
@@ -818,7 +913,7 @@ extern "C" int be_gather_rows(be_ctx* ctx, const void* arena, const int32_t* src
   if (ctx == nullptr || rows < 0 || d % 8 != 0) return BE_ERR_INVALID;
   cudaError_t e = bx::launch_gather(static_cast<const bf16*>(arena), src, 1, rows, d,
                                     static_cast<bf16*>(out), nullptr, nullptr,
-                                    pick_stream(ctx, stream));
+                                    pick_stream(ctx, stream), nullptr, 0);
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
 }
 
@@ -826,7 +921,7 @@ extern "C" int be_scatter_rows(be_ctx* ctx, const void* rows_in, const int32_t* 
                                int d, void* arena, void* stream) {
   if (ctx == nullptr || rows < 0 || d % 8 != 0) return BE_ERR_INVALID;
   cudaError_t e = bx::launch_scatter(static_cast<const bf16*>(rows_in), dst, 1, rows, d,
-                                     static_cast<bf16*>(arena), pick_stream(ctx, stream));
+                                     static_cast<bf16*>(arena), pick_stream(ctx, stream), nullptr, 0);
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "scatter: %s", cudaGetErrorString(e));
 }
 

@@ -55,6 +55,17 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
   if constexpr (MODE == kStore || MODE == kResid) {
     const int fe = f & ~1;
     float sq[8];  // kResid: this lane's x^2 + x'^2 of token pair p
+    float2 xv[8];
+    if constexpr (MODE == kResid) {
+      // all residual loads of the chunk in flight before the first store (the stores below may
+      // alias them as far as the compiler knows, which would serialise 8 L2 round trips)
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int ti = 2 * p + (odd ? 1 : 0);
+        xv[p] = ti < nvalid ? __ldcg(reinterpret_cast<const float2*>(E.xres + (size_t)(t0 + ti) * E.ldr + fe))
+                            : make_float2(0.f, 0.f);
+      }
+    }
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[2 * p] : v[2 * p + 1], 1);
@@ -68,11 +79,10 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
       } else {
         sq[p] = 0.f;
         if (valid) {
-          float2* px = reinterpret_cast<float2*>(E.xres + (size_t)t * E.ldr + fe);
-          float2 x = *px;
+          float2 x = xv[p];
           x.x += lo;
           x.y += hi;
-          *px = x;
+          *reinterpret_cast<float2*>(E.xres + (size_t)t * E.ldr + fe) = x;
           *reinterpret_cast<uint32_t*>(E.xres_b + (size_t)t * E.ldr + fe) = pack_bf16x2(x.x, x.y);
           sq[p] = x.x * x.x + x.y * x.y;
         }
@@ -244,7 +254,10 @@ __global__ void __launch_bounds__(192, CTAS)
   const long long it_begin = R.begin(blockIdx.x);
   const long long it_end = R.begin(blockIdx.x + 1);
 
-  if (threadIdx.x == 0) stamp(E, 0);
+  if (threadIdx.x == 0) {
+    stamp(E, 0);
+    tl_start(E.tl, E.tl_cap);
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_x);
     for (int s = 0; s < STAGES; ++s) {
@@ -283,6 +296,7 @@ __global__ void __launch_bounds__(192, CTAS)
       }
       pdl_wait();  // activations are produced by the previous kernel
       stamp(E, 2);
+      tl_go(E.tl, E.tl_cap);
       for (int i = 0; i < pre && load_b; ++i) {
         const long long it = it_begin + i;
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
@@ -487,7 +501,10 @@ __global__ void __launch_bounds__(192, CTAS)
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) stamp(E, 7);
+  if (threadIdx.x == 0) {
+    stamp(E, 7);
+    tl_end(E.tl, E.tl_cap);
+  }
   if (warp == 1) tmem_free<kTmemCols>(tmem_base);
 }
 

@@ -47,6 +47,8 @@ struct EpiParams {
   float* ws;               // [grid][2][BN][128] fp32 partials (first/last segment per CTA)
   int* counters;           // [tiles] arrival counters (self-resetting)
   unsigned long long* trace;  // diagnostics: [grid][8] globaltimer stamps, nullptr = off
+  unsigned long long* tl;     // diagnostics: kernel timeline slot (ptx.cuh tl_*), nullptr = off
+  int tl_cap;
   int dbg;                    // diagnostics: bit0 skip MMA, bit1 skip activation loads
 };
 

@@ -56,6 +56,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- TMA
+// Kernel timeline (diagnostics): tl = slot pointer into a [4][cap] u64 array (min CTA start,
+// max CTA start, min dependency-release, max CTA end) of globaltimer ns; nullptr = off.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_start(unsigned long long* tl, int cap) {
+  if (tl != nullptr) {
+    const unsigned long long t = gtimer();
+    atomicMin(tl, t);
+    atomicMax(tl + cap, t);
+  }
+}
+__device__ __forceinline__ void tl_go(unsigned long long* tl, int cap) {
+  if (tl != nullptr) atomicMin(tl + 2 * cap, gtimer());
+}
+__device__ __forceinline__ void tl_end(unsigned long long* tl, int cap) {
+  if (tl != nullptr) atomicMax(tl + 3 * cap, gtimer());
+}
+// L2 prefetch of a global range (no smem, no completion tracking)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
 }

@@ -19,7 +19,11 @@ namespace bx {
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ arena,
                                    const int* __restrict__ src, int src_stride, int rows, int d,
                                    __nv_bfloat16* __restrict__ xb, float* __restrict__ x,
-                                   float* __restrict__ ss) {
+                                   float* __restrict__ ss, unsigned long long* tl, int tl_cap) {
+  if (threadIdx.x == 0) {
+    tl_start(tl, tl_cap);
+    tl_go(tl, tl_cap);
+  }
   const int vec_per_row = d / 8;
   const long long total = (long long)rows * vec_per_row;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -54,12 +58,19 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ arena,
       if (live && (c & 3) == 0) ss[(size_t)r * (d / 32) + (c >> 2)] = sq;
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) tl_end(tl, tl_cap);
 }
 
 // ---------------------------------------------------------------- K2 scatter
 __global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ xb,
                                     const int* __restrict__ dst, int dst_stride, int rows, int d,
-                                    __nv_bfloat16* __restrict__ arena) {
+                                    __nv_bfloat16* __restrict__ arena, unsigned long long* tl,
+                                    int tl_cap) {
+  if (threadIdx.x == 0) {
+    tl_start(tl, tl_cap);
+    tl_go(tl, tl_cap);
+  }
   const int vec_per_row = d / 8;
   const long long total = (long long)rows * vec_per_row;
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < total;
@@ -71,6 +82,8 @@ __global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ xb,
     const uint4 val = reinterpret_cast<const uint4*>(xb + (size_t)r * d)[c];
     reinterpret_cast<uint4*>(arena + (size_t)drow * d)[c] = val;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) tl_end(tl, tl_cap);
 }
 
 // ---------------------------------------------------------------- K7 cosine
@@ -195,15 +208,19 @@ static inline int grid_for(long long work, int threads, int cap) {
 }
 
 cudaError_t launch_gather(const __nv_bfloat16* arena, const int* src, int src_stride, int rows,
-                          int d, __nv_bfloat16* xb, float* x, float* ss, cudaStream_t st) {
+                          int d, __nv_bfloat16* xb, float* x, float* ss, cudaStream_t st,
+                          unsigned long long* tl, int tl_cap) {
   if (rows <= 0) return cudaSuccess;
-  gather_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(arena, src, src_stride, rows, d, xb, x, ss);
+  gather_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(
+      arena, src, src_stride, rows, d, xb, x, ss, tl, tl_cap);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter(const __nv_bfloat16* xb, const int* dst, int dst_stride, int rows,
-                           int d, __nv_bfloat16* arena, cudaStream_t st) {
+                           int d, __nv_bfloat16* arena, cudaStream_t st, unsigned long long* tl,
+                           int tl_cap) {
   if (rows <= 0) return cudaSuccess;
-  scatter_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(xb, dst, dst_stride, rows, d, arena);
+  scatter_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(
+      xb, dst, dst_stride, rows, d, arena, tl, tl_cap);
   return cudaGetLastError();
 }
 cudaError_t launch_cosine(const __nv_bfloat16* a, const __nv_bfloat16* b, int rows, int d,

@@ -61,7 +61,12 @@ PROF_CLASSES = ["gather", "rms", "gemm_qkv", "attention", "gemm_o", "gemm_gate_u
 
 class ProfRec(C.Structure):
     _fields_ = [("cls", C.c_int32), ("ntok", C.c_int32), ("n", C.c_int32), ("k", C.c_int32),
-                ("ms", C.c_float)]
+                ("ms", C.c_float), ("bytes", C.c_double), ("flops", C.c_double)]
+
+
+class TimelineRec(C.Structure):
+    _fields_ = [("slot", C.c_int32), ("cls", C.c_int32), ("start_first", C.c_uint64),
+                ("start_last", C.c_uint64), ("go_first", C.c_uint64), ("end_last", C.c_uint64)]
 
 
 class Context:
@@ -88,13 +93,30 @@ class Context:
         """Per-launch event timing of exec_batch kernels (include/blockexec.h be_prof_*)."""
         check(lib().be_prof_enable(self.h, 1 if on else 0), self.h)
 
+    def timeline_enable(self, cap: int = 4096) -> None:
+        """Kernel timeline inside graph replays (include/blockexec.h be_timeline_*)."""
+        check(lib().be_timeline_enable(self.h, cap), self.h)
+
+    def timeline_begin(self) -> None:
+        check(lib().be_timeline_begin(self.h), self.h)
+
+    def timeline_read(self) -> list[dict]:
+        n = C.c_int(0)
+        check(lib().be_timeline_read(self.h, None, 0, C.byref(n)), self.h)
+        recs = (TimelineRec * max(1, n.value))()
+        check(lib().be_timeline_read(self.h, C.cast(recs, C.c_void_p), n.value, C.byref(n)),
+              self.h)
+        return [{"slot": r.slot, "cls": PROF_CLASSES[r.cls], "start_first": r.start_first,
+                 "start_last": r.start_last, "go_first": r.go_first, "end_last": r.end_last}
+                for r in recs[:n.value]]
+
     def prof_read(self) -> list[dict]:
         n = C.c_int(0)
         check(lib().be_prof_read(self.h, None, 0, C.byref(n)), self.h)
         recs = (ProfRec * max(1, n.value))()
         check(lib().be_prof_read(self.h, C.cast(recs, C.c_void_p), n.value, C.byref(n)), self.h)
-        return [{"cls": PROF_CLASSES[r.cls], "ntok": r.ntok, "n": r.n, "k": r.k, "ms": r.ms}
-                for r in recs[:n.value]]
+        return [{"cls": PROF_CLASSES[r.cls], "ntok": r.ntok, "n": r.n, "k": r.k, "ms": r.ms,
+                 "bytes": r.bytes, "flops": r.flops} for r in recs[:n.value]]
 
     def close(self) -> None:
         if self.h:

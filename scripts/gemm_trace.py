@@ -9,7 +9,7 @@ import torch  # noqa: E402
 from paper_2404_18322_b200 import device as dev  # noqa: E402
 
 ctx = dev.Context(0)
-shapes = [(4096, 4096, 64), (4096, 4096, 16), (22016, 4096, 64), (22016, 4096, 16)]
+shapes = [(4096, 4096, 64), (4096, 4096, 16), (12288, 4096, 64), (22016, 4096, 64), (4096, 11008, 64)]
 for N, K, M in shapes:
     w = dev.pack_weight(ctx, (torch.rand(N, K, device="cuda", dtype=torch.bfloat16) - 0.5) * 0.05)
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
