@@ -59,6 +59,10 @@ typedef struct {
    * MLP, residual). NULL = n_layers decoder layers "afaf...". Blocks split by the zoo's
    * partitioner may start or end mid-layer ("fa", "a", "f"). */
   const char* components;
+  /* Structured-pruned surrogate: when > d_ff, this block's FFN is the first
+   * d_ff channels of the FFN of a block with ffn_src channels and the same (seed, name) - the
+   * draft model of speculation (be_exec_speculative). 0 = d_ff. */
+  int ffn_src;
 } be_block_desc;
 
 /* One token row of an execution batch (decode: one per request; prefill: one per prompt token). */
@@ -114,6 +118,29 @@ int be_exec_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace
                       int n_tokens, const be_token* d_tokens, int pt_stride,
                       const int32_t* d_page_table, const void* d_arena_in, void* d_arena_out,
                       void* stream);
+
+/* One speculative decode step (§8 a14, K6 + K7). The draft block (a surrogate of verify->blk,
+ * e.g. its 50%-pruned FFN, be_block_desc.ffn_src) runs on a second stream and
+ * its output is forwarded at once to next->blk - the early forward of scenario.cpp:521-537 -
+ * while verify->blk computes the true output on the context stream. K7 then compares the
+ * draft and true rows (cos >= threshold accepts; PAPER.md:637 uses 0.95, the reference's
+ * stand-in is a Bernoulli verdict, config.hpp:60) and `next` is re-run from the true rows for
+ * the rejected ones (finish_verified, scenario.cpp:740-807), overwriting their KV slots.
+ * d_x_in / d_y_draft / d_y_true / d_z_out: device bf16 [n_tokens][d] rows; each stage's host
+ * token records index them (src_row/dst_row). verify->ws must differ from draft/next's (the
+ * two lanes run concurrently). cos_out / accept_out: host [n_tokens]. Synchronous. */
+typedef struct {
+  be_block* blk;
+  be_kv_pool* pool;
+  be_workspace* ws;
+  const be_token* tokens; /* host, n_tokens */
+  int n_pt_rows, pt_stride;
+  const int32_t* page_table; /* host */
+} be_spec_stage;
+int be_exec_speculative(be_ctx* ctx, const be_spec_stage* verify, const be_spec_stage* draft,
+                        const be_spec_stage* next, int n_tokens, const void* d_x_in,
+                        void* d_y_draft, void* d_y_true, void* d_z_out, float threshold,
+                        float* cos_out, int32_t* accept_out, int* n_accepted);
 
 /* Kernel launches one be_exec_batch of n_tokens performs (for launch accounting). */
 int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_tokens, int pt_stride);

@@ -39,6 +39,7 @@ typedef struct {
   uint64_t seed;
   const char* name;
   const char* components; /* 'a' attention / 'f' ffn per zoo component; NULL = n_layers x "af" */
+  int ffn_src;            /* > d_ff: FFN = first d_ff channels of a d_ff = ffn_src block's FFN */
 } or_block_desc; /* same layout as be_block_desc (include/blockexec.h) */
 
 typedef struct {
@@ -60,15 +61,16 @@ typedef struct {
   float* kv; /* [layer][2][max_tokens][d] */
 } or_seq;
 
+/* src_cols: logical row stride of the stream (a column prefix of a wider matrix when > cols) */
 static void fill_weight(float* w, size_t rows, size_t cols, uint64_t seed, const char* block,
-                        int layer, const char* tensor, float scale) {
+                        int layer, const char* tensor, float scale, size_t src_cols) {
   char sid[160];
   snprintf(sid, sizeof sid, "weights:%s:%d:%s", block, layer, tensor);
   const uint64_t key = or_stream_key(seed, sid);
 #pragma omp parallel for schedule(static)
   for (long long r = 0; r < (long long)rows; ++r)
     for (size_t c = 0; c < cols; ++c)
-      w[(size_t)r * cols + c] = or_bf16_round(or_synth_value(key, (uint64_t)r * cols + c, scale));
+      w[(size_t)r * cols + c] = or_bf16_round(or_synth_value(key, (uint64_t)r * src_cols + c, scale));
 }
 
 or_block* or_block_create(const or_block_desc* d) {
@@ -99,10 +101,10 @@ or_block* or_block_create(const or_block_desc* d) {
     L->wv = (float*)malloc(D * D * 4);
     L->wo = (float*)malloc(D * D * 4);
     if (!L->wq || !L->wk || !L->wv || !L->wo) return NULL;
-    fill_weight(L->wq, D, D, d->seed, b->name, l, "wq", d->init_scale);
-    fill_weight(L->wk, D, D, d->seed, b->name, l, "wk", d->init_scale);
-    fill_weight(L->wv, D, D, d->seed, b->name, l, "wv", d->init_scale);
-    fill_weight(L->wo, D, D, d->seed, b->name, l, "wo", d->init_scale);
+    fill_weight(L->wq, D, D, d->seed, b->name, l, "wq", d->init_scale, D);
+    fill_weight(L->wk, D, D, d->seed, b->name, l, "wk", d->init_scale, D);
+    fill_weight(L->wv, D, D, d->seed, b->name, l, "wv", d->init_scale, D);
+    fill_weight(L->wo, D, D, d->seed, b->name, l, "wo", d->init_scale, D);
   }
   for (int l = 0; l < b->n_ffn; ++l) {
     or_layer* L = &b->layers[l];
@@ -110,9 +112,10 @@ or_block* or_block_create(const or_block_desc* d) {
     L->wu = (float*)malloc(F * D * 4);
     L->wd = (float*)malloc(D * F * 4);
     if (!L->wg || !L->wu || !L->wd) return NULL;
-    fill_weight(L->wg, F, D, d->seed, b->name, l, "wg", d->init_scale);
-    fill_weight(L->wu, F, D, d->seed, b->name, l, "wu", d->init_scale);
-    fill_weight(L->wd, D, F, d->seed, b->name, l, "wd", d->init_scale);
+    const size_t F_src = d->ffn_src > d->d_ff ? (size_t)d->ffn_src : F;
+    fill_weight(L->wg, F, D, d->seed, b->name, l, "wg", d->init_scale, D);
+    fill_weight(L->wu, F, D, d->seed, b->name, l, "wu", d->init_scale, D);
+    fill_weight(L->wd, D, F, d->seed, b->name, l, "wd", d->init_scale, F_src);
   }
   const int half = d->head_dim / 2;
   b->rope_cos = (float*)malloc((size_t)d->max_pos * half * 4);

@@ -19,7 +19,8 @@ class OrBlockDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
                 ("head_dim", C.c_int), ("d_ff", C.c_int), ("max_pos", C.c_int),
                 ("norm_eps", C.c_float), ("rope_theta", C.c_float), ("init_scale", C.c_float),
-                ("seed", C.c_uint64), ("name", C.c_char_p), ("components", C.c_char_p)]
+                ("seed", C.c_uint64), ("name", C.c_char_p), ("components", C.c_char_p),
+                ("ffn_src", C.c_int)]
 
 
 _lib = None
@@ -70,7 +71,7 @@ class OracleBlock:
         self._cb = comps.encode()
         d = OrBlockDesc(shape.n_layers, shape.d_model, shape.n_heads, shape.head_dim, shape.d_ff,
                         shape.max_pos, shape.norm_eps, shape.rope_theta, shape.init_scale, seed,
-                        self._nb, self._cb)
+                        self._nb, self._cb, getattr(shape, "ffn_src", 0))
         self.h = lib().or_block_create(C.byref(d))
         if not self.h:
             raise ValueError("oracle: bad block shape")

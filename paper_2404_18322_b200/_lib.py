@@ -31,7 +31,8 @@ class BlockDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
                 ("head_dim", C.c_int), ("d_ff", C.c_int), ("max_pos", C.c_int),
                 ("norm_eps", C.c_float), ("rope_theta", C.c_float), ("init_scale", C.c_float),
-                ("seed", C.c_uint64), ("name", C.c_char_p), ("components", C.c_char_p)]
+                ("seed", C.c_uint64), ("name", C.c_char_p), ("components", C.c_char_p),
+                ("ffn_src", C.c_int)]
 
 
 class Token(C.Structure):
@@ -72,6 +73,7 @@ def lib() -> C.CDLL:
         "be_workspace_create": (I, [P, I, I, I, I, I, I, PP]),
         "be_workspace_free": (I, [P]),
         "be_exec_batch": (I, [P, P, P, P, I, I, P, I, I, P, P, P, P]),
+        "be_exec_speculative": (I, [P, P, P, P, I, P, P, P, P, F, P, P, P]),
         "be_exec_batch_dev": (I, [P, P, P, P, I, I, P, I, P, P, P, P]),
         "be_gather_rows": (I, [P, P, P, I, I, P, P]),
         "be_scatter_rows": (I, [P, P, P, I, I, P, P]),

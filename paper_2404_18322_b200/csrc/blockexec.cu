@@ -25,7 +25,8 @@ cudaError_t launch_gather(const __nv_bfloat16*, const int*, int, int, int, __nv_
 cudaError_t launch_scatter(const __nv_bfloat16*, const int*, int, int, int, __nv_bfloat16*, cudaStream_t,
                            unsigned long long*, int);
 cudaError_t launch_cosine(const __nv_bfloat16*, const __nv_bfloat16*, int, int, float, float*, int*, cudaStream_t);
-cudaError_t launch_synth_weight(__nv_bfloat16*, int, int, uint64_t, uint64_t, float, int, int, const float*, cudaStream_t);
+cudaError_t launch_synth_weight(__nv_bfloat16*, int, int, uint64_t, uint64_t, float, int, int, const float*, cudaStream_t,
+                                int src_cols = 0);
 cudaError_t launch_synth_rows(__nv_bfloat16*, long long, uint64_t, float, cudaStream_t);
 cudaError_t launch_pack_weight(const __nv_bfloat16*, __nv_bfloat16*, int, int, cudaStream_t);
 cudaError_t launch_rope_table(float2*, int, int, double, cudaStream_t);
@@ -80,6 +81,12 @@ struct be_ctx {
   int tl_cap = 0;
   int tl_next = 0;
   std::vector<int> tl_cls;
+  // speculation (be_exec_speculative): the draft lane's stream, fork/join events, verdict scratch
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  float* spec_cos = nullptr;
+  int* spec_accept = nullptr;
+  int spec_cap = 0;
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;
   size_t prof_ev_used = 0;
@@ -254,6 +261,11 @@ extern "C" int be_ctx_destroy(be_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t ev : ctx->prof_ev) cudaEventDestroy(ev);
   if (ctx->tl) cudaFree(ctx->tl);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->spec_cos) cudaFree(ctx->spec_cos);
+  if (ctx->spec_accept) cudaFree(ctx->spec_accept);
   if (ctx->gemm_ws) cudaFree(ctx->gemm_ws);
   if (ctx->gemm_counters) cudaFree(ctx->gemm_counters);
   cudaStreamDestroy(ctx->stream);
@@ -295,6 +307,9 @@ extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(ctx, BE_ERR_INVALID, "block: head_dim must be 64 or 128");
   if (d->max_pos <= 0) return fail(ctx, BE_ERR_INVALID, "block: max_pos must be positive");
+  if (d->ffn_src != 0 && d->ffn_src < d->d_ff)
+    return fail(ctx, BE_ERR_INVALID, "block: ffn_src must be 0 or >= d_ff");
+  const int F_src = d->ffn_src > 0 ? d->ffn_src : d->d_ff;
   cudaSetDevice(ctx->device);
   auto* b = new be_block();
   b->ctx = ctx;
@@ -345,7 +360,8 @@ extern "C" int be_block_load(be_ctx* ctx, const be_block_desc* d, be_block** out
       L.wd = cur + 2 * F * D;
       cur += ffn_elems;
       bx::launch_synth_weight(L.wgu, (int)(2 * F), (int)D, key("wg"), key("wu"), s, 2, d->head_dim, nullptr, st);
-      bx::launch_synth_weight(L.wd, (int)D, (int)F, key("wd"), 0, s, 0, d->head_dim, nullptr, st);
+      bx::launch_synth_weight(L.wd, (int)D, (int)F, key("wd"), 0, s, 0, d->head_dim, nullptr, st,
+                              F_src);
       ++jf;
     }
   }
@@ -703,7 +719,8 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
   (void)phase;
   const auto& D = blk->desc;
   const int d = D.d_model, F = D.d_ff, H = D.n_heads, hd = D.head_dim;
-  if (ws->d != d || ws->dff != F || ws->H != H)
+  // a workspace serves any block of its d_model / heads with d_ff <= its own (pruned surrogates)
+  if (ws->d != d || ws->dff < F || ws->H != H)
     return fail(ctx, BE_ERR_INVALID, "workspace shape does not match block");
   if (ntok > ws->max_tok) return fail(ctx, BE_ERR_INVALID, "batch of %d tokens > workspace %d", ntok, ws->max_tok);
   if (pool->n_layers != blk->n_att || pool->n_heads != H || pool->head_dim != hd)
@@ -739,7 +756,7 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
       eg.ss_groups = d / 32;
       eg.norm_eps = D.norm_eps;
       eg.out = ws->h;
-      eg.ldo = F;
+      eg.ldo = ws->dff;  // row stride of h (its TMA map); the down GEMM reads the first F columns
       {
         eg.tl = tl_slot(ctx, BE_K_GEMM_GATE_UP);
         eg.tl_cap = ctx->tl_cap;
@@ -896,6 +913,79 @@ extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_wo
                                  cudaMemcpyHostToDevice, st));
   return exec_dev(ctx, blk, pool, ws, phase, n_tokens, ws->d_tokens, pt_stride, ws->d_pt,
                   d_arena_in, d_arena_out, st);
+}
+
+extern "C" int be_exec_speculative(be_ctx* ctx, const be_spec_stage* verify,
+                                   const be_spec_stage* draft, const be_spec_stage* next,
+                                   int n_tokens, const void* d_x_in, void* d_y_draft,
+                                   void* d_y_true, void* d_z_out, float threshold, float* cos_out,
+                                   int32_t* accept_out, int* n_accepted) {
+  if (ctx == nullptr || verify == nullptr || draft == nullptr || next == nullptr ||
+      n_tokens <= 0 || d_x_in == nullptr || d_y_draft == nullptr || d_y_true == nullptr ||
+      d_z_out == nullptr || cos_out == nullptr || accept_out == nullptr || n_accepted == nullptr)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_speculative: bad arguments") : BE_ERR_INVALID;
+  const be_spec_stage* st3[3] = {verify, draft, next};
+  for (const be_spec_stage* g : st3)
+    if (g->blk == nullptr || g->pool == nullptr || g->ws == nullptr || g->tokens == nullptr)
+      return fail(ctx, BE_ERR_INVALID, "be_exec_speculative: incomplete stage");
+  if (verify->ws == draft->ws || verify->ws == next->ws)
+    return fail(ctx, BE_ERR_INVALID, "be_exec_speculative: the verify lane needs its own workspace");
+  const int d = verify->blk->desc.d_model;
+  if (draft->blk->desc.d_model != d || next->blk->desc.d_model != d)
+    return fail(ctx, BE_ERR_INVALID, "be_exec_speculative: blocks differ in d_model");
+  cudaSetDevice(ctx->device);
+  if (ctx->side == nullptr) {
+    BE_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    BE_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    BE_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  if (n_tokens > ctx->spec_cap) {
+    if (ctx->spec_cos) cudaFree(ctx->spec_cos);
+    if (ctx->spec_accept) cudaFree(ctx->spec_accept);
+    ctx->spec_cos = nullptr;
+    ctx->spec_accept = nullptr;
+    BE_CUDA(ctx, cudaMalloc(&ctx->spec_cos, n_tokens * sizeof(float)));
+    BE_CUDA(ctx, cudaMalloc(&ctx->spec_accept, n_tokens * sizeof(int)));
+    ctx->spec_cap = n_tokens;
+  }
+  cudaStream_t lane = ctx->stream, side = ctx->side;
+  auto run = [&](const be_spec_stage* g, const be_token* toks, int n, const void* in, void* out,
+                 cudaStream_t s) {
+    return be_exec_batch(ctx, g->blk, g->pool, g->ws, BE_PHASE_DECODE, n, toks, g->n_pt_rows,
+                         g->pt_stride, g->page_table, in, out, s);
+  };
+  int rc;
+  // K6: the draft lane (scenario.cpp:521-537) - surrogate, then the next block fed by its output
+  BE_CUDA(ctx, cudaEventRecord(ctx->ev_fork, lane));
+  BE_CUDA(ctx, cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+  if ((rc = run(draft, draft->tokens, n_tokens, d_x_in, d_y_draft, side)) != BE_OK) return rc;
+  if ((rc = run(next, next->tokens, n_tokens, d_y_draft, d_z_out, side)) != BE_OK) return rc;
+  // the verifying block on the main lane, concurrently
+  if ((rc = run(verify, verify->tokens, n_tokens, d_x_in, d_y_true, lane)) != BE_OK) return rc;
+  BE_CUDA(ctx, cudaEventRecord(ctx->ev_join, side));
+  BE_CUDA(ctx, cudaStreamWaitEvent(lane, ctx->ev_join, 0));
+  // K7 verdict: per-row cosine(draft, true) >= threshold
+  cudaError_t e = bx::launch_cosine(static_cast<const bf16*>(d_y_draft),
+                                    static_cast<const bf16*>(d_y_true), n_tokens, d, threshold,
+                                    ctx->spec_cos, ctx->spec_accept, lane);
+  if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "cosine: %s", cudaGetErrorString(e));
+  BE_CUDA(ctx, cudaMemcpyAsync(cos_out, ctx->spec_cos, n_tokens * sizeof(float),
+                               cudaMemcpyDeviceToHost, lane));
+  BE_CUDA(ctx, cudaMemcpyAsync(accept_out, ctx->spec_accept, n_tokens * sizeof(int),
+                               cudaMemcpyDeviceToHost, lane));
+  BE_CUDA(ctx, cudaStreamSynchronize(lane));
+  // rejected rows: everything computed from their draft is redone from the true rows
+  // (finish_verified, scenario.cpp:740-807); their KV slots in `next` are overwritten
+  std::vector<be_token> redo;
+  for (int i = 0; i < n_tokens; ++i)
+    if (!accept_out[i]) redo.push_back(next->tokens[i]);
+  *n_accepted = n_tokens - (int)redo.size();
+  if (!redo.empty()) {
+    if ((rc = run(next, redo.data(), (int)redo.size(), d_y_true, d_z_out, lane)) != BE_OK)
+      return rc;
+    BE_CUDA(ctx, cudaStreamSynchronize(lane));
+  }
+  return BE_OK;
 }
 
 extern "C" int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_tokens,

@@ -143,9 +143,11 @@ __device__ __forceinline__ float synth_value(uint64_t key, uint64_t i, float sca
 //   perm 1: q/k rotate_half pair interleave inside each head (phys 2j <- j, 2j+1 <- j + hd/2)
 //   perm 2: gate/up interleave (phys 2j <- gate j, 2j+1 <- up j), two keys
 // dst holds `rows` physical rows of `cols`; gamma (optional, length cols) is folded in.
+// src_cols: logical row stride of the generated stream (>= cols: a column prefix of a wider
+// matrix, the pruned FFN of a speculation surrogate)
 __global__ void synth_weight_kernel(__nv_bfloat16* __restrict__ dst, int rows, int cols,
                                     uint64_t key0, uint64_t key1, float scale, int perm,
-                                    int head_dim, const float* __restrict__ gamma) {
+                                    int head_dim, const float* __restrict__ gamma, int src_cols) {
   const long long total = (long long)rows * cols;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -160,7 +162,7 @@ __global__ void synth_weight_kernel(__nv_bfloat16* __restrict__ dst, int rows, i
       lr = pr >> 1;
       key = (pr & 1) ? key1 : key0;
     }
-    float v = synth_value(key, (uint64_t)lr * cols + c, scale);
+    float v = synth_value(key, (uint64_t)lr * src_cols + c, scale);
     v = __bfloat162float(__float2bfloat16_rn(v));  // logical bf16 weight
     if (gamma != nullptr) v *= gamma[c];
     dst[packed_index(pr, c, cols)] = __float2bfloat16_rn(v);  // GEMM-ready tile layout
@@ -231,9 +233,9 @@ cudaError_t launch_cosine(const __nv_bfloat16* a, const __nv_bfloat16* b, int ro
 }
 cudaError_t launch_synth_weight(__nv_bfloat16* dst, int rows, int cols, uint64_t key0,
                                 uint64_t key1, float scale, int perm, int head_dim,
-                                const float* gamma, cudaStream_t st) {
+                                const float* gamma, cudaStream_t st, int src_cols) {
   synth_weight_kernel<<<grid_for((long long)rows * cols, 256, 148 * 32), 256, 0, st>>>(
-      dst, rows, cols, key0, key1, scale, perm, head_dim, gamma);
+      dst, rows, cols, key0, key1, scale, perm, head_dim, gamma, src_cols > 0 ? src_cols : cols);
   return cudaGetLastError();
 }
 cudaError_t launch_pack_weight(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int cols,

@@ -6,6 +6,7 @@ sm_100a kernels of libblockexec.so.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -27,6 +28,13 @@ class BlockShape:
     rope_theta: float = 10000.0
     init_scale: float = 0.02 * 3 ** 0.5  # uniform with std 0.02
     components: str | None = None  # 'a'/'f' sequence (zoo components); None = n_layers x "af"
+    ffn_src: int = 0  # > d_ff: FFN pruned to the first d_ff channels of a d_ff = ffn_src block
+
+    def surrogate(self, keep: float = 0.5) -> "BlockShape":
+        """The speculation draft of this block: same attention, FFN structured-pruned to the
+        first keep*d_ff channels (PAPER.md:501-507 surrogate; C5 uses 50%)."""
+        f = max(64, int(self.d_ff * keep) // 64 * 64)
+        return dataclasses.replace(self, d_ff=f, ffn_src=self.ffn_src or self.d_ff)
 
     @property
     def head_dim(self) -> int:
@@ -139,7 +147,7 @@ class Block:
         self._comps_b = shape.comps.encode()
         desc = BlockDesc(shape.n_layers, shape.d_model, shape.n_heads, shape.head_dim, shape.d_ff,
                          shape.max_pos, shape.norm_eps, shape.rope_theta, shape.init_scale, seed,
-                         self._name_b, self._comps_b)
+                         self._name_b, self._comps_b, shape.ffn_src)
         h = C.c_void_p()
         check(lib().be_block_load(ctx.h, C.byref(desc), C.byref(h)), ctx.h)
         self.h = h
@@ -226,6 +234,36 @@ def exec_batch(ctx: Context, block: Block, pool: KvPool, ws: Workspace, phase: i
                               pt.shape[0], pt.shape[1], pt.ctypes.data_as(C.c_void_p),
                               _ptr(arena_in), _ptr(arena_out),
                               stream if stream is not None else C.c_void_p(0)), ctx.h)
+
+
+class SpecStage(C.Structure):
+    _fields_ = [("blk", C.c_void_p), ("pool", C.c_void_p), ("ws", C.c_void_p),
+                ("tokens", C.c_void_p), ("n_pt_rows", C.c_int), ("pt_stride", C.c_int),
+                ("page_table", C.c_void_p)]
+
+
+def exec_speculative(ctx: Context, verify, draft, nxt, x_in, y_draft, y_true, z_out,
+                     threshold: float = 0.95):
+    """One speculative decode step (include/blockexec.h be_exec_speculative). Each stage is
+    (Block, KvPool, Workspace, tokens, page_table). Returns (cos[n], accept[n], n_accepted)."""
+    keep, stages = [], []
+    for blk, pool, ws, tokens, pt in (verify, draft, nxt):
+        toks = tokens_array(tokens)
+        pt = np.ascontiguousarray(pt, dtype=np.int32)
+        keep += [toks, pt]
+        stages.append(SpecStage(blk.h.value, pool.h.value, ws.h.value,
+                                C.cast(toks, C.c_void_p).value, pt.shape[0], pt.shape[1],
+                                pt.ctypes.data))
+    n = len(verify[3])
+    cos = np.zeros(n, np.float32)
+    acc = np.zeros(n, np.int32)
+    n_acc = C.c_int(0)
+    check(lib().be_exec_speculative(ctx.h, C.byref(stages[0]), C.byref(stages[1]),
+                                    C.byref(stages[2]), n, _ptr(x_in), _ptr(y_draft),
+                                    _ptr(y_true), _ptr(z_out), threshold,
+                                    cos.ctypes.data_as(C.c_void_p),
+                                    acc.ctypes.data_as(C.c_void_p), C.byref(n_acc)), ctx.h)
+    return cos, acc, n_acc.value
 
 
 def pack_weight(ctx: Context, w):

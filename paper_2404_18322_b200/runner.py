@@ -79,7 +79,7 @@ class Runner:
         for i, nm in enumerate(self._names):
             descs[i] = BlockDesc(s.n_layers, s.d_model, s.n_heads, s.head_dim, s.d_ff, s.max_pos,
                                  s.norm_eps, s.rope_theta, s.init_scale, wl.seed, nm,
-                                 self._comps[i])
+                                 self._comps[i], s.ffn_src)
         ptr = np.zeros(len(wl.chains) + 1, np.int32)
         flat = []
         for t, ch in enumerate(wl.chains):
