@@ -401,12 +401,17 @@ __global__ void __launch_bounds__(192, CTAS)
         const int c_first = R.cta_of(tile_it0);
         const int c_last = R.cta_of(tile_it0 + nkb - 1);
         const int n_contrib = c_last - c_first + 1;
-        const size_t frow = (size_t)(q * 32 + lane) * BN;  // partial layout [feature][BN]
+        // partial layout [BN/4][128 rows] of float4 (4 consecutive tokens of one feature row): a
+        // warp instruction moves 32 consecutive rows = 512 contiguous bytes (4 L2 lines, not 32)
+        const int row = q * 32 + lane;
+        auto part4 = [&](int c) {
+          return reinterpret_cast<float4*>(E.ws + (size_t)c * BN * kBM);
+        };
         int* ctr = E.counters + tile;
         if (E.trace != nullptr && warp == 2 && lane == 0)  // diagnostics: last segment's role
           E.trace[blockIdx.x * 8 + 6] = (int)blockIdx.x == c_first ? 1000000 + n_contrib : 2000000;
         if ((int)blockIdx.x != c_first) {
-          float4* slot = reinterpret_cast<float4*>(E.ws + (size_t)blockIdx.x * BN * kBM + frow);
+          float4* slot = part4(blockIdx.x) + row;
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             if (n0 + c0 >= E.ntok) break;
@@ -414,7 +419,7 @@ __global__ void __launch_bounds__(192, CTAS)
             tmem_ld16(t_lane + c0, acc);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              __stcg(slot + (c0 >> 2) + j,
+              __stcg(slot + ((c0 >> 2) + j) * kBM,
                      make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
           }
           // the CTA barrier orders the 128 threads' stores before one release at GPU scope
@@ -438,18 +443,29 @@ __global__ void __launch_bounds__(192, CTAS)
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 16)
               tmem_ld16(t_lane + c0, *reinterpret_cast<float(*)[16]>(acc + c0));
-            for (int o = 1; o < n_contrib; ++o) {
-              const float4* p = reinterpret_cast<const float4*>(
-                  E.ws + (size_t)(c_first + o) * BN * kBM + frow);
-              float4 v[BN / 4];
+            // contributors in rounds of R with all their loads in flight (16 float4 per lane)
+            constexpr int R = BN >= 64 ? 1 : 64 / BN;
+            for (int o0 = 1; o0 < n_contrib; o0 += R) {
+              float4 v[R][BN / 4];
 #pragma unroll
-              for (int k = 0; k < BN / 4; ++k) v[k] = __ldcg(p + k);
+              for (int j = 0; j < R; ++j) {
+                if (o0 + j < n_contrib) {
+                  const float4* p = part4(c_first + o0 + j) + row;
 #pragma unroll
-              for (int k = 0; k < BN / 4; ++k) {
-                acc[4 * k] += v[k].x;
-                acc[4 * k + 1] += v[k].y;
-                acc[4 * k + 2] += v[k].z;
-                acc[4 * k + 3] += v[k].w;
+                  for (int k = 0; k < BN / 4; ++k) v[j][k] = __ldcg(p + k * kBM);
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < R; ++j) {
+                if (o0 + j < n_contrib) {
+#pragma unroll
+                  for (int k = 0; k < BN / 4; ++k) {
+                    acc[4 * k] += v[j][k].x;
+                    acc[4 * k + 1] += v[j][k].y;
+                    acc[4 * k + 2] += v[j][k].z;
+                    acc[4 * k + 3] += v[j][k].w;
+                  }
+                }
               }
             }
 #pragma unroll
@@ -469,11 +485,10 @@ __global__ void __launch_bounds__(192, CTAS)
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const int o = o0 + j;
-                const float4* p = reinterpret_cast<const float4*>(
-                                      E.ws + (size_t)(c_first + o) * BN * kBM + frow) + (c0 >> 2);
+                const float4* p = part4(c_first + (o < n_contrib ? o : 0)) + row + (c0 >> 2) * kBM;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                  v[j][k] = o < n_contrib ? __ldcg(p + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                  v[j][k] = o < n_contrib ? __ldcg(p + k * kBM) : make_float4(0.f, 0.f, 0.f, 0.f);
               }
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
