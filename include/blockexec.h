@@ -142,6 +142,17 @@ int be_exec_speculative(be_ctx* ctx, const be_spec_stage* verify, const be_spec_
                         void* d_y_draft, void* d_y_true, void* d_z_out, float threshold,
                         float* cos_out, int32_t* accept_out, int* n_accepted);
 
+/* A grouped batch: n_blocks independent batches of blocks with identical shape and component
+ * sequence (e.g. the tenants' private blocks at one chain position, which share no request)
+ * executed as one batch - one launch per kernel instead of n_blocks. Token rows
+ * [g*R, (g+1)*R) (R = n_tokens / n_blocks, one of 16/32/64) belong to blks[g] / pools[g]; a
+ * group with fewer members is padded with rows {src 0, dst -1, kv_slot -1, pos -1} (computed,
+ * never stored). Each batch's semantics are unchanged (its own weights, KV pool, page rows). */
+int be_exec_group_dev(be_ctx* ctx, int n_blocks, be_block* const* blks, be_kv_pool* const* pools,
+                      be_workspace* ws, int phase, int n_tokens, const be_token* d_tokens,
+                      int pt_stride, const int32_t* d_page_table, const void* d_arena_in,
+                      void* d_arena_out, void* stream);
+
 /* Kernel launches one be_exec_batch of n_tokens performs (for launch accounting). */
 int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_tokens, int pt_stride);
 

@@ -37,6 +37,10 @@ struct AttnParams {
   __nv_bfloat16* out;         // [rows][H*hd]
   float* part;                // [rows][H][splits][hd + 2] partials when splits > 1
   int splits;
+  // grouped batch: rows [g*grp_rows, (g+1)*grp_rows) read block g's pool pools[g]
+  int n_grp;
+  int grp_rows;
+  const __nv_bfloat16* pools[8];
   unsigned long long* tl;     // diagnostics: timeline slots of decode and combine (or nullptr)
   int tl_cap;
 };
@@ -63,6 +67,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams P) {
   const int p_begin = (int)((long long)split * npages / P.splits);
   const int p_end = (int)((long long)(split + 1) * npages / P.splits);
   const int* pt = P.page_table + (size_t)P.row_pt[(size_t)row * P.meta_stride] * P.pt_stride;
+  const __nv_bfloat16* pool = P.n_grp > 1 ? P.pools[row / P.grp_rows] : P.pool;
 
   // q chunk for this lane, prescaled so scores are in log2 units
   float q[8];
@@ -82,7 +87,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnParams P) {
   const size_t v_off = (size_t)P.H * 16 * HD;
 
   for (int p = p_begin + warp; p < p_end; p += 4) {
-    const __nv_bfloat16* kp = P.pool + (size_t)pt[p] * P.page_elems + head_off;
+    const __nv_bfloat16* kp = pool + (size_t)pt[p] * P.page_elems + head_off;
     const __nv_bfloat16* vp = kp + v_off;
     uint4 kr[NLD], vr[NLD];
 #pragma unroll

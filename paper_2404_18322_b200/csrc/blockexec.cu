@@ -48,6 +48,9 @@ struct AttnParams {
   __nv_bfloat16* out;
   float* part;
   int splits;
+  int n_grp;
+  int grp_rows;
+  const __nv_bfloat16* pools[8];
   unsigned long long* tl;
   int tl_cap;
 };
@@ -713,10 +716,14 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
   return BE_OK;
 }
 
-int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int phase,
-             int ntok, const be_token* d_tok, int pt_stride, const int32_t* d_pt,
-             const void* arena_in, void* arena_out, cudaStream_t st) {
+// One batch of one block, or a grouped batch of n_grp independent blocks of one shape whose
+// token rows sit side by side in groups of grp_rows = ntok / n_grp (one GEMM n-tile each).
+int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* pools,
+             be_workspace* ws, int phase, int ntok, const be_token* d_tok, int pt_stride,
+             const int32_t* d_pt, const void* arena_in, void* arena_out, cudaStream_t st) {
   (void)phase;
+  be_block* blk = blks[0];
+  be_kv_pool* pool = pools[0];
   const auto& D = blk->desc;
   const int d = D.d_model, F = D.d_ff, H = D.n_heads, hd = D.head_dim;
   // a workspace serves any block of its d_model / heads with d_ff <= its own (pruned surrogates)
@@ -727,7 +734,28 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     return fail(ctx, BE_ERR_INVALID, "kv pool shape does not match block");
   if (ntok == 0) return BE_OK;
   const int* tok = reinterpret_cast<const int*>(d_tok);
-  const int bn = bx::gemm_pick_bn(ntok);
+  const int grp_rows = n_grp > 1 ? ntok / n_grp : ntok;
+  const int bn = n_grp > 1 ? grp_rows : bx::gemm_pick_bn(ntok);
+  if (n_grp > 1) {
+    if (n_grp > bx::kMaxGroup || ntok % n_grp != 0 || (grp_rows != 16 && grp_rows != 32 && grp_rows != 64))
+      return fail(ctx, BE_ERR_INVALID, "grouped batch: %d blocks x %d rows unsupported", n_grp, grp_rows);
+    for (int g = 1; g < n_grp; ++g) {
+      const be_block* b = blks[g];
+      if (b->comps != blk->comps || b->desc.d_model != d || b->desc.d_ff != F ||
+          b->desc.n_heads != H || pools[g]->page_elems != pool->page_elems ||
+          pools[g]->n_layers != blk->n_att)
+        return fail(ctx, BE_ERR_INVALID, "grouped batch: blocks differ in shape");
+    }
+  }
+  // per-GEMM group tables: the weights of block g for n-tile g
+  auto group = [&](EpiParams& E, bf16* const be_block::Layer::*w, int li) {
+    E.n_grp = n_grp;
+    E.grp_rows = grp_rows;
+    for (int g = 0; g < n_grp; ++g) {
+      E.wgrp[g] = blks[g]->layers[li].*w;
+      E.kvgrp[g] = pools[g]->base;
+    }
+  };
   cudaError_t e;
 
   // K1: gather the members' input rows into the batch (fp32 residual + bf16 shadow)
@@ -748,8 +776,10 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     int rc;
     if (kind == 'f') {
       // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
+      const int li = jf;
       const auto& L = blk->layers[jf++];
       EpiParams eg{};
+      group(eg, &be_block::Layer::wgu, li);
       eg.mode = bx::kSwiGLU;
       eg.ntok = ntok;
       eg.ss_in = ws->ss;
@@ -766,6 +796,7 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
       }
       if (rc != BE_OK) return rc;
       EpiParams ed{};
+      group(ed, &be_block::Layer::wd, li);
       ed.mode = bx::kResid;
       ed.ntok = ntok;
       ed.xres = ws->X;
@@ -787,6 +818,7 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     const auto& L = blk->layers[l];
     // ---- attention component: RMSNorm (fused) -> QKV + RoPE + KV append -> paged attn -> O + residual
     EpiParams eq{};
+    group(eq, &be_block::Layer::wqkv, l);
     eq.mode = bx::kQKV;
     eq.ntok = ntok;
     eq.ss_in = ws->ss;
@@ -828,6 +860,9 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     ap.out = ws->attn;
     ap.part = ws->attn_part;
     ap.splits = splits;
+    ap.n_grp = n_grp;
+    ap.grp_rows = grp_rows;
+    for (int g = 0; g < n_grp; ++g) ap.pools[g] = pools[g]->base;
     ap.tl = tl_slot(ctx, BE_K_ATTENTION);
     ap.tl_cap = ctx->tl_cap;
     if (ap.tl != nullptr && splits > 1) tl_slot(ctx, BE_K_ATTENTION);  // combine's slot = tl + 1
@@ -838,6 +873,7 @@ int exec_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int
     if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "attention: %s", cudaGetErrorString(e));
 
     EpiParams eo{};
+    group(eo, &be_block::Layer::wo, l);
     eo.mode = bx::kResid;
     eo.ntok = ntok;
     eo.xres = ws->X;
@@ -877,8 +913,26 @@ extern "C" int be_exec_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, b
     return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_batch_dev: bad arguments") : BE_ERR_INVALID;
   if (phase != BE_PHASE_PREFILL && phase != BE_PHASE_DECODE)
     return fail(ctx, BE_ERR_INVALID, "unknown phase %d", phase);
-  return exec_dev(ctx, blk, pool, ws, phase, n_tokens, d_tokens, pt_stride, d_page_table,
+  return exec_dev(ctx, 1, &blk, &pool, ws, phase, n_tokens, d_tokens, pt_stride, d_page_table,
                   d_arena_in, d_arena_out, pick_stream(ctx, stream));
+}
+
+extern "C" int be_exec_group_dev(be_ctx* ctx, int n_blocks, be_block* const* blks,
+                                 be_kv_pool* const* pools, be_workspace* ws, int phase,
+                                 int n_tokens, const be_token* d_tokens, int pt_stride,
+                                 const int32_t* d_page_table, const void* d_arena_in,
+                                 void* d_arena_out, void* stream) {
+  if (ctx == nullptr || n_blocks < 1 || blks == nullptr || pools == nullptr || ws == nullptr ||
+      n_tokens <= 0 || d_tokens == nullptr || d_page_table == nullptr || d_arena_in == nullptr ||
+      d_arena_out == nullptr || pt_stride <= 0)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_group_dev: bad arguments") : BE_ERR_INVALID;
+  for (int g = 0; g < n_blocks; ++g)
+    if (blks[g] == nullptr || pools[g] == nullptr)
+      return fail(ctx, BE_ERR_INVALID, "be_exec_group_dev: null block or pool");
+  if (phase != BE_PHASE_PREFILL && phase != BE_PHASE_DECODE)
+    return fail(ctx, BE_ERR_INVALID, "unknown phase %d", phase);
+  return exec_dev(ctx, n_blocks, blks, pools, ws, phase, n_tokens, d_tokens, pt_stride,
+                  d_page_table, d_arena_in, d_arena_out, pick_stream(ctx, stream));
 }
 
 extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws,
@@ -911,7 +965,7 @@ extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_wo
   if (n_pt_rows > 0)
     BE_CUDA(ctx, cudaMemcpyAsync(ws->d_pt, page_table, (size_t)n_pt_rows * pt_stride * sizeof(int32_t),
                                  cudaMemcpyHostToDevice, st));
-  return exec_dev(ctx, blk, pool, ws, phase, n_tokens, ws->d_tokens, pt_stride, ws->d_pt,
+  return exec_dev(ctx, 1, &blk, &pool, ws, phase, n_tokens, ws->d_tokens, pt_stride, ws->d_pt,
                   d_arena_in, d_arena_out, st);
 }
 

@@ -154,13 +154,15 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
         const float other = __shfl_xor_sync(0xffffffffu, v[i], 1);
         const int pos = __shfl_sync(0xffffffffu, my_pos, i);
         if (i < nvalid) {
-          const float2 cs = __ldg(E.rope + (size_t)pos * (E.head_dim >> 1) + (e >> 1));
+          const int pc = pos > 0 ? pos : 0;  // padding rows of a grouped batch have pos -1
+          const float2 cs = __ldg(E.rope + (size_t)pc * (E.head_dim >> 1) + (e >> 1));
           v[i] = odd ? v[i] * cs.x + other * cs.y : v[i] * cs.x - other * cs.y;
         }
       }
     }
     const int ee = e & ~1;
     const int H = d / E.head_dim;
+    __nv_bfloat16* kvp = E.n_grp > 1 ? E.kvgrp[t0 / E.grp_rows] : E.kv_pool;
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[2 * p] : v[2 * p + 1], 1);
@@ -172,11 +174,11 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
       if (sec == 0) {
         *reinterpret_cast<uint32_t*>(E.out + (size_t)(t0 + ti) * E.ldo + (fi & ~1)) =
             pack_bf16x2(lo, hi);
-      } else {
+      } else if (slot >= 0) {  // padding rows (slot -1) own no KV
         const long long page = slot >> 4;
         const size_t idx = (size_t)(page * E.page_elems + (long long)E.layer * E.layer_elems) +
                            ((size_t)((sec - 1) * H + head) * 16 + (slot & 15)) * E.head_dim + ee;
-        *reinterpret_cast<uint32_t*>(E.kv_pool + idx) = pack_bf16x2(lo, hi);
+        *reinterpret_cast<uint32_t*>(kvp + idx) = pack_bf16x2(lo, hi);
       }
     }
   }
@@ -285,7 +287,8 @@ __global__ void __launch_bounds__(192, CTAS)
       const int pre = (int)(n_it < STAGES ? n_it : STAGES);
       auto wtile = [&](long long it) {
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
-        return wpk + ((size_t)(tile % m_tiles) * nkb + kb) * (kBM * kBK);
+        const __nv_bfloat16* wb = E.n_grp > 1 ? E.wgrp[tile / m_tiles] : wpk;  // grouped batch
+        return wb + ((size_t)(tile % m_tiles) * nkb + kb) * (kBM * kBK);
       };
       constexpr bool load_b = true;
       constexpr uint32_t stage_bytes = S::kStageBytes;

@@ -17,6 +17,7 @@
 namespace bx {
 
 enum EpiMode : int { kStore = 0, kResid = 1, kSwiGLU = 2, kQKV = 3 };
+constexpr int kMaxGroup = 8;  // blocks per grouped batch
 
 struct EpiParams {
   int mode;
@@ -47,6 +48,13 @@ struct EpiParams {
   float* ws;               // [grid][2][BN][128] fp32 partials (first/last segment per CTA)
   int* counters;           // [tiles] arrival counters (self-resetting)
   unsigned long long* trace;  // diagnostics: [grid][8] globaltimer stamps, nullptr = off
+  // grouped batch: n_grp independent blocks of one shape side by side, token rows
+  // [g*grp_rows, (g+1)*grp_rows) belonging to block g (grp_rows == BN): the GEMM of n-tile g
+  // streams wgrp[g] and the QKV epilogue appends to kvgrp[g] (n_grp <= 1: wpk / kv_pool)
+  int n_grp;
+  int grp_rows;
+  const __nv_bfloat16* wgrp[kMaxGroup];
+  __nv_bfloat16* kvgrp[kMaxGroup];
   unsigned long long* tl;     // diagnostics: kernel timeline slot (ptx.cuh tl_*), nullptr = off
   int tl_cap;
   int dbg;                    // diagnostics: bit0 skip MMA, bit1 skip activation loads

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -108,6 +109,7 @@ class Runner {
   int n_created_ = 0;
   int mode_ = 0;
   bool use_graphs_ = false;
+  bool group_ = true;  // decode: run independent same-shape batches as one grouped launch
   int max_batch_tokens_ = 4096;
   int d_ = 0;
   int max_ctx_ = 0;
@@ -134,8 +136,18 @@ class Runner {
   std::int64_t tokens_generated_ = 0;
   int batches_run_ = 0;
   // graph replay of a steady-state lockstep decode step, one per request group
+  // one launch of a decode step: a batch, or several independent same-shape batches grouped
+  struct LaunchEntry {
+    std::vector<int> plans;
+    std::vector<be_token> toks;  // grouped: concatenated, page-table rows renumbered
+    std::vector<int32_t> pt;
+    int stride = 1;
+  };
+  std::vector<LaunchEntry> group_plans(const std::vector<PlannedBatch>& plans) const;
+  void launch_entry(const std::vector<PlannedBatch>& plans, const LaunchEntry& le,
+                    const be_token* d_tok, const int32_t* d_pt);
   struct GraphSlot {
-    std::vector<std::tuple<int, int, int>> sig;  // (block, n_tokens, stride) per batch
+    std::vector<std::tuple<int, int, int>> sig;  // (block, n_tokens, stride*16+n) per launch
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
     void reset() {
@@ -164,6 +176,7 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   st_ = dry_ ? nullptr : static_cast<cudaStream_t>(be_ctx_stream(ctx));
   mode_ = w.mode;
   use_graphs_ = w.use_graphs != 0;
+  if (const char* g = std::getenv("BH_GROUP")) group_ = std::atoi(g) != 0;
   max_batch_tokens_ = w.max_batch_tokens > 0 ? w.max_batch_tokens : 4096;
   d_ = w.blocks[0].d_model;
   for (int b = 0; b < w.n_blocks; ++b) {
@@ -505,6 +518,74 @@ void Runner::run(int max_batches) {
   }
 }
 
+// Consecutive decode batches at blocks of one shape and component sequence whose members are
+// disjoint (no request is in two of them, so none consumes another's output) form one grouped
+// launch (be_exec_group_dev) - e.g. the tenants' private blocks at one chain position. Groups
+// need equal member counts of 16/32/64 (the GEMM n-tile of each block).
+std::vector<Runner::LaunchEntry> Runner::group_plans(const std::vector<PlannedBatch>& plans) const {
+  std::vector<LaunchEntry> out;
+  size_t i = 0;
+  while (i < plans.size()) {
+    LaunchEntry le;
+    le.plans.push_back(static_cast<int>(i));
+    const PlannedBatch& a = plans[i];
+    const size_t n = a.toks.size();
+    const bool groupable = group_ && a.phase == Phase::kDecode && (n == 16 || n == 32 || n == 64);
+    std::vector<int> seen;
+    for (const auto& t : a.toks) seen.push_back(t.src_row);
+    size_t j = i + 1;
+    while (groupable && j < plans.size() && le.plans.size() < 8) {
+      const PlannedBatch& b = plans[j];
+      if (b.phase != Phase::kDecode || b.toks.size() != n || comps_[b.block] != comps_[a.block] ||
+          descs_[b.block].d_ff != descs_[a.block].d_ff || b.block == a.block)
+        break;
+      bool disjoint = true;
+      for (const auto& t : b.toks)
+        if (std::find(seen.begin(), seen.end(), t.src_row) != seen.end()) disjoint = false;
+      if (!disjoint) break;
+      for (const auto& t : b.toks) seen.push_back(t.src_row);
+      le.plans.push_back(static_cast<int>(j));
+      ++j;
+    }
+    if (le.plans.size() > 1) {
+      for (int k : le.plans) le.stride = std::max(le.stride, plans[k].stride);
+      int row0 = 0;
+      for (int k : le.plans) {
+        const PlannedBatch& pb = plans[k];
+        for (be_token t : pb.toks) {
+          t.pt_row += row0;
+          le.toks.push_back(t);
+        }
+        for (int r = 0; r < pb.n_rows; ++r)
+          for (int c = 0; c < le.stride; ++c)
+            le.pt.push_back(c < pb.stride ? pb.pt[(size_t)r * pb.stride + c] : -1);
+        row0 += pb.n_rows;
+      }
+    }
+    out.push_back(std::move(le));
+    i = j;
+  }
+  return out;
+}
+
+void Runner::launch_entry(const std::vector<PlannedBatch>& plans, const LaunchEntry& le,
+                          const be_token* d_tok, const int32_t* d_pt) {
+  if (le.plans.size() == 1) {
+    launch(plans[le.plans[0]], d_tok, d_pt);
+    return;
+  }
+  be_block* blks[8];
+  be_kv_pool* pls[8];
+  for (size_t g = 0; g < le.plans.size(); ++g) {
+    blks[g] = blocks_[plans[le.plans[g]].block];
+    pls[g] = pools_[plans[le.plans[g]].block];
+  }
+  const int rc = be_exec_group_dev(ctx_, static_cast<int>(le.plans.size()), blks, pls, ws_,
+                                   BE_PHASE_DECODE, static_cast<int>(le.toks.size()), d_tok,
+                                   le.stride, d_pt, arena_, arena_, st_);
+  if (rc != BE_OK) throw BeError(rc, std::string("exec group: ") + be_last_error(ctx_));
+}
+
 void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, int group,
                          const std::vector<int>* members) {
   if (mode_ != 1) throw BeError(BE_ERR_STATE, "decode_step needs lockstep mode");
@@ -561,16 +642,37 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
   }
   if (n_batches) *n_batches = static_cast<int>(plans.size());
   if (dry_) return;
-  // metadata layout: per batch [tokens][page table], 256-byte aligned
-  std::vector<size_t> off_tok(plans.size()), off_pt(plans.size());
+  // launches: single batches, and groups of independent same-shape batches
+  const std::vector<LaunchEntry> entries = group_plans(plans);
+  auto ent_toks = [&](const LaunchEntry& le) -> const std::vector<be_token>& {
+    return le.plans.size() == 1 ? plans[le.plans[0]].toks : le.toks;
+  };
+  auto ent_pt = [&](const LaunchEntry& le) -> const std::vector<int32_t>& {
+    return le.plans.size() == 1 ? plans[le.plans[0]].pt : le.pt;
+  };
+  if (entries.size() != plans.size()) {  // launch accounting per grouped launch
+    stats.launches = 0;
+    for (const auto& le : entries) {
+      const PlannedBatch& p0 = plans[le.plans[0]];
+      stats.launches += be_exec_batch_launches(ctx_, blocks_[p0.block],
+                                               static_cast<int>(ent_toks(le).size()),
+                                               le.plans.size() == 1 ? p0.stride : le.stride);
+    }
+  }
+  // metadata layout: per launch [tokens][page table], 256-byte aligned
+  std::vector<size_t> off_tok(entries.size()), off_pt(entries.size());
   size_t total = 0;
   std::vector<std::tuple<int, int, int>> sig;
-  for (size_t i = 0; i < plans.size(); ++i) {
+  for (size_t i = 0; i < entries.size(); ++i) {
+    const auto& tk = ent_toks(entries[i]);
+    const auto& pt = ent_pt(entries[i]);
     off_tok[i] = total;
-    total += (plans[i].toks.size() * sizeof(be_token) + 255) & ~size_t(255);
+    total += (tk.size() * sizeof(be_token) + 255) & ~size_t(255);
     off_pt[i] = total;
-    total += (plans[i].pt.size() * sizeof(int32_t) + 255) & ~size_t(255);
-    sig.emplace_back(plans[i].block, static_cast<int>(plans[i].toks.size()), plans[i].stride);
+    total += (pt.size() * sizeof(int32_t) + 255) & ~size_t(255);
+    const int stride = entries[i].plans.size() == 1 ? plans[entries[i].plans[0]].stride : entries[i].stride;
+    sig.emplace_back(plans[entries[i].plans[0]].block, static_cast<int>(tk.size()),
+                     stride * 16 + static_cast<int>(entries[i].plans.size()));
   }
   if (total > meta_cap_) {
     ck(cudaStreamSynchronize(st_), "meta grow");
@@ -591,16 +693,18 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
   meta_slot_ ^= 1;
   ck(cudaEventSynchronize(meta_ev_[slot]), "meta reuse");
   char* stage = meta_host_[slot];
-  for (size_t i = 0; i < plans.size(); ++i) {
-    std::memcpy(stage + off_tok[i], plans[i].toks.data(), plans[i].toks.size() * sizeof(be_token));
-    std::memcpy(stage + off_pt[i], plans[i].pt.data(), plans[i].pt.size() * sizeof(int32_t));
+  for (size_t i = 0; i < entries.size(); ++i) {
+    const auto& tk = ent_toks(entries[i]);
+    const auto& pt = ent_pt(entries[i]);
+    std::memcpy(stage + off_tok[i], tk.data(), tk.size() * sizeof(be_token));
+    std::memcpy(stage + off_pt[i], pt.data(), pt.size() * sizeof(int32_t));
   }
   ck(cudaMemcpyAsync(meta_dev_, stage, total, cudaMemcpyHostToDevice, st_), "meta h2d");
   ck(cudaEventRecord(meta_ev_[slot], st_), "meta ev record");
   auto launch_all = [&]() {
-    for (size_t i = 0; i < plans.size(); ++i)
-      launch(plans[i], reinterpret_cast<const be_token*>(meta_dev_ + off_tok[i]),
-             reinterpret_cast<const int32_t*>(meta_dev_ + off_pt[i]));
+    for (size_t i = 0; i < entries.size(); ++i)
+      launch_entry(plans, entries[i], reinterpret_cast<const be_token*>(meta_dev_ + off_tok[i]),
+                   reinterpret_cast<const int32_t*>(meta_dev_ + off_pt[i]));
   };
   stats.graph_replayed = 0;
   if (be_prof_active(ctx_)) {

@@ -80,3 +80,32 @@ class _Rows:
     def __init__(self, ptr, rows, cols):
         self.__cuda_array_interface__ = {"shape": (rows, cols), "typestr": "<i2",
                                          "data": (ptr, False), "version": 3, "strides": None}
+
+
+def test_c2_grouped_private_blocks_match_separate_batches(ctx, monkeypatch):
+    # the 4 tenants' private blocks at a chain position run as one grouped launch
+    # (be_exec_group_dev); results equal the per-block batches within bf16 tolerance (split-K
+    # plans differ with the grouped tile count, so summation order does)
+    wl = CONFIGS["c2"](prompt=24, output=6)
+    monkeypatch.setenv("BH_GROUP", "1")
+    grouped = _decode_rows(ctx, wl, 3)
+    monkeypatch.setenv("BH_GROUP", "0")
+    separate = _decode_rows(ctx, wl, 3)
+    for g, s in zip(grouped, separate):
+        rel = np.linalg.norm(g - s) / np.linalg.norm(s)
+        assert rel <= 2e-2, rel
+        cos = (g * s).sum(1) / (np.linalg.norm(g, axis=1) * np.linalg.norm(s, axis=1))
+        assert cos.min() >= 0.999
+
+
+def test_c2_grouped_launch_count(ctx, monkeypatch):
+    wl = CONFIGS["c2"](prompt=24, output=6)
+    counts = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("BH_GROUP", flag)
+        run = Runner(ctx, wl, mode=1, use_graphs=True)
+        run.run()
+        run.decode_step()
+        counts[flag] = run.step_stats()["launches"]
+        run.close()
+    assert counts["1"] < counts["0"]
