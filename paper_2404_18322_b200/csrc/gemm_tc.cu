@@ -594,21 +594,25 @@ GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems,
   const long long tiles = (long long)m_tiles * n_tiles;
   const int nkb = K / kBK;
   const long long total = tiles * nkb;
-  // Grid. Partial tiles cost a serial fixup at the end of the kernel, so prefer whole tiles per
-  // CTA when the tile count allows, else the fewest even splits per tile that still put
-  // kMinStreamCtas CTAs on the weight stream (measured sweep, profiles/r01_gemm_sweep_gmin.log:
-  // 120 is best; ~86 CTAs do not saturate HBM through this pipeline); prefill uses every SM.
+  // Grid: every SM streams (stream-K ranges over all 148), measured best since the partial fixup
+  // became cheap (coalesced partials): all-SM stream-K beat whole tiles on 128 CTAs by 2.3% and
+  // the min-CTA knob is flat (profiles/r01_gemm_sweep_gmin.log). BE_GEMM_WHOLE=1 / BE_GEMM_GMIN
+  // restore the whole-tile preference / fewer even splits for experiments.
   static const int kMinStreamCtas = [] {
     const char* e = getenv("BE_GEMM_GMIN");
-    return e ? atoi(e) : 120;
+    return e ? atoi(e) : 148;
+  }();
+  static const bool kWholeTiles = [] {
+    const char* e = getenv("BE_GEMM_WHOLE");
+    return e ? atoi(e) != 0 : false;
   }();
   const long long sms = grid_cap > 0 && grid_cap < num_sms ? grid_cap : num_sms;
   long long g = sms;
   if (tiles >= sms) {
     const long long k = (tiles + sms - 1) / sms;  // whole tiles per CTA
-    if (tiles % k == 0 && tiles / k >= kMinStreamCtas) g = tiles / k;
+    if (kWholeTiles && tiles % k == 0 && tiles / k >= kMinStreamCtas) g = tiles / k;
   } else if (tiles >= kMinStreamCtas) {
-    g = tiles;  // one whole tile per CTA
+    if (kWholeTiles) g = tiles;  // one whole tile per CTA
   } else {
     const long long s = (kMinStreamCtas + tiles - 1) / tiles;  // even k-splits per tile
     g = tiles * s < sms ? tiles * s : sms;
