@@ -196,6 +196,13 @@ int be_timeline_enable(be_ctx* ctx, int cap);
 int be_timeline_begin(be_ctx* ctx);
 int be_timeline_read(be_ctx* ctx, be_timeline_rec* out, int cap, int* n_out);
 
+/* KV migration data path (§8 f: the P2P page copy of start_kv_migration, scenario.cpp:361-431):
+ * copies whole pages src_slots[i] of src_pool to dst_slots[i] of dst_pool (host arrays) on the
+ * destination context's stream; contiguous slot runs move as one copy. The pools may live on
+ * different GPUs (peer copy over NVLink; peer access is enabled on first use). Async. */
+int be_kv_copy_pages(be_ctx* dst_ctx, const be_kv_pool* src_pool, be_kv_pool* dst_pool,
+                     const int32_t* src_slots, const int32_t* dst_slots, int n, void* stream);
+
 /* K1 / K2 standalone: routing-table gather and scatter of bf16 rows. */
 int be_gather_rows(be_ctx* ctx, const void* d_arena, const int32_t* d_src, int rows, int d,
                    void* d_out, void* stream);

@@ -73,6 +73,12 @@ int bh_kv_share_prefix(bh_kv* k, uint64_t request, uint64_t from, const char* bl
 int bh_kv_release(bh_kv* k, uint64_t request, const char* block);
 int bh_kv_release_request(bh_kv* k, uint64_t request);
 int bh_kv_move_segment(bh_kv* k, uint64_t request, const char* block, int dst_device);
+/* Same, returning the page copies the move implies: (source slot on the old device, slot on
+ * dst_device) per page in token order - private pages move, shared ones are copied
+ * (KvStore::move_segment, kv.cpp:165-200). Feed them to be_kv_copy_pages. The bookkeeping is
+ * updated only if all copies fit in cap. */
+int bh_kv_move_segment_slots(bh_kv* k, uint64_t request, const char* block, int dst_device,
+                             int32_t* src_slots, int32_t* dst_slots, int cap, int* n_out);
 /* query: what = 0 device_of, 1 tokens, 2 pages, 3 shared_pages, 4 segment_bytes, 5 has_segment */
 int64_t bh_kv_query(const bh_kv* k, uint64_t request, const char* block, int what);
 int64_t bh_kv_bytes_saved(const bh_kv* k);

@@ -1051,6 +1051,50 @@ extern "C" int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_to
   return 2 + blk->n_att * (3 + (splits > 1 ? 1 : 0)) + blk->n_ffn * 2;
 }
 
+// ------------------------------------------------------------------------------ KV migration
+extern "C" int be_kv_copy_pages(be_ctx* dst_ctx, const be_kv_pool* src_pool, be_kv_pool* dst_pool,
+                                const int32_t* src_slots, const int32_t* dst_slots, int n,
+                                void* stream) {
+  if (dst_ctx == nullptr || src_pool == nullptr || dst_pool == nullptr || n < 0 ||
+      (n > 0 && (src_slots == nullptr || dst_slots == nullptr)))
+    return dst_ctx ? fail(dst_ctx, BE_ERR_INVALID, "be_kv_copy_pages: bad arguments") : BE_ERR_INVALID;
+  if (src_pool->page_elems != dst_pool->page_elems)
+    return fail(dst_ctx, BE_ERR_INVALID, "be_kv_copy_pages: pools differ in page layout");
+  for (int i = 0; i < n; ++i)
+    if (src_slots[i] < 0 || src_slots[i] >= src_pool->n_pages || dst_slots[i] < 0 ||
+        dst_slots[i] >= dst_pool->n_pages)
+      return fail(dst_ctx, BE_ERR_INVALID, "be_kv_copy_pages: slot %d out of range", i);
+  const int src_dev = src_pool->ctx->device, dst_dev = dst_ctx->device;
+  cudaSetDevice(dst_dev);
+  if (src_dev != dst_dev) {
+    int can = 0;
+    BE_CUDA(dst_ctx, cudaDeviceCanAccessPeer(&can, dst_dev, src_dev));
+    if (can) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(src_dev, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(dst_ctx, BE_ERR_CUDA, "peer access %d->%d: %s", dst_dev, src_dev, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  }
+  cudaStream_t st = pick_stream(dst_ctx, stream);
+  const size_t page_bytes = (size_t)src_pool->page_elems * sizeof(bf16);
+  int i = 0;
+  while (i < n) {
+    int j = i + 1;  // coalesce runs contiguous on both sides
+    while (j < n && src_slots[j] == src_slots[j - 1] + 1 && dst_slots[j] == dst_slots[j - 1] + 1) ++j;
+    const char* s = reinterpret_cast<const char*>(src_pool->base) + (size_t)src_slots[i] * page_bytes;
+    char* d = reinterpret_cast<char*>(dst_pool->base) + (size_t)dst_slots[i] * page_bytes;
+    const size_t bytes = (size_t)(j - i) * page_bytes;
+    if (src_dev == dst_dev) {
+      BE_CUDA(dst_ctx, cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, st));
+    } else {
+      BE_CUDA(dst_ctx, cudaMemcpyPeerAsync(d, dst_dev, s, src_dev, bytes, st));
+    }
+    i = j;
+  }
+  return BE_OK;
+}
+
 // ------------------------------------------------------------------------------ row kernels
 extern "C" int be_gather_rows(be_ctx* ctx, const void* arena, const int32_t* src, int rows, int d,
                               void* out, void* stream) {

@@ -178,6 +178,19 @@ int bh_kv_move_segment(bh_kv* k, uint64_t req, const char* block, int dst) {
   if (!k || !block) return BE_ERR_INVALID;
   return guard(k, [&] { k->k.move_segment(req, block, dst); });
 }
+int bh_kv_move_segment_slots(bh_kv* k, uint64_t req, const char* block, int dst,
+                             int32_t* src_slots, int32_t* dst_slots, int cap, int* n_out) {
+  if (!k || !block || !n_out || (cap > 0 && (!src_slots || !dst_slots))) return BE_ERR_INVALID;
+  return guard(k, [&] {
+    const auto copies = k->k.move_segment(req, block, dst);
+    if ((int)copies.size() > cap) throw std::invalid_argument("move_segment: slot buffer too small");
+    for (size_t i = 0; i < copies.size(); ++i) {
+      src_slots[i] = copies[i].first;
+      dst_slots[i] = copies[i].second;
+    }
+    *n_out = static_cast<int>(copies.size());
+  });
+}
 int64_t bh_kv_query(const bh_kv* k, uint64_t req, const char* block, int what) {
   if (!k || !block) return -1;
   switch (what) {

@@ -266,6 +266,17 @@ def exec_speculative(ctx: Context, verify, draft, nxt, x_in, y_draft, y_true, z_
     return cos, acc, n_acc.value
 
 
+def kv_copy_pages(ctx: Context, src_pool: "KvPool", dst_pool: "KvPool", src_slots, dst_slots,
+                  stream=None) -> None:
+    """Copy whole KV pages between pools (same GPU or peer GPUs): the data path of a KV
+    migration whose page pairs come from KvStore.move_segment_slots."""
+    s = np.ascontiguousarray(src_slots, np.int32)
+    d = np.ascontiguousarray(dst_slots, np.int32)
+    check(lib().be_kv_copy_pages(ctx.h, src_pool.h, dst_pool.h, s.ctypes.data_as(C.c_void_p),
+                                 d.ctypes.data_as(C.c_void_p), len(s),
+                                 stream if stream is not None else C.c_void_p(0)), ctx.h)
+
+
 def pack_weight(ctx: Context, w):
     """Row-major [N][K] bf16 -> packed GEMM tile layout (csrc/ptx.cuh packed_index)."""
     out = w.new_empty(w.shape)

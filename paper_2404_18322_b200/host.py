@@ -76,6 +76,8 @@ def _bind(prefix: str, L):
     if prefix == "bh_":
         sigs["kv_attach_pool"] = (I, [P, C.c_char_p, I, I])
         sigs["kv_page_slots"] = (I, [P, U64, C.c_char_p, C.POINTER(C.c_int32), I, C.POINTER(I)])
+        sigs["kv_move_segment_slots"] = (I, [P, U64, C.c_char_p, I, C.POINTER(C.c_int32),
+                                             C.POINTER(C.c_int32), I, C.POINTER(I)])
     for name, (res, args) in sigs.items():
         fn = getattr(L, prefix + name)
         fn.restype, fn.argtypes = res, args
@@ -208,6 +210,15 @@ class KvStore:
 
     def move_segment(self, request: int, block: str, dst_device: int):
         self._ck(self._f("kv_move_segment")(self.h, request, block.encode(), dst_device))
+
+    def move_segment_slots(self, request: int, block: str, dst_device: int, cap: int = 4096):
+        """move_segment plus the (source slot, destination slot) page copies it implies."""
+        src = (C.c_int32 * cap)()
+        dst = (C.c_int32 * cap)()
+        n = C.c_int(0)
+        self._ck(self._f("kv_move_segment_slots")(self.h, request, block.encode(), dst_device,
+                                                  src, dst, cap, C.byref(n)))
+        return list(src[:n.value]), list(dst[:n.value])
 
     def info(self, request: int, block: str) -> SegmentInfo:
         q = self._f("kv_query")

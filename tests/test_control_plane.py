@@ -301,6 +301,27 @@ def test_kv_page_slots_are_physical_and_unique():
         kv.append_tokens(3, "b0", 100)  # pool full (ledger over capacity)
 
 
+def test_kv_move_segment_slots_gives_page_copies():
+    """Moving a segment to another device yields one (old slot, new slot) copy per page: private
+    pages free their old slot, a shared prefix page stays for its other reader (kv.cpp move)."""
+    kv = H.KvStore()
+    kv.attach_pool("b0", 0, 8)
+    kv.attach_pool("b0", 1, 8)
+    kv.create_segment(1, "b0", 0, 64)
+    kv.append_tokens(1, "b0", 32)           # slots 0, 1
+    kv.create_segment(2, "b0", 0, 64)
+    kv.share_prefix(2, 1, "b0", 32)         # shares slots 0, 1
+    kv.append_tokens(2, "b0", 16)           # slot 2
+    assert kv.page_slots(2, "b0") == [0, 1, 2]
+    src, dst = kv.move_segment_slots(2, "b0", 1)
+    assert src == [0, 1, 2] and dst == [0, 1, 2]
+    assert kv.page_slots(2, "b0") == [0, 1, 2] and kv.info(2, "b0").device == 1
+    assert kv.page_slots(1, "b0") == [0, 1]  # the shared pages stay for request 1
+    kv.create_segment(3, "b0", 0, 64)
+    kv.append_tokens(3, "b0", 1)
+    assert kv.page_slots(3, "b0") == [2]    # request 2's private page freed slot 2 on device 0
+
+
 # ---------------------------------------------------------------- whole-simulation traces
 SIM_CASES = [
     # n_layers, dim, n_lora, first_adapted, prompts, outputs, budget

@@ -89,3 +89,37 @@ def test_block_weights_bit_exact(ctx):
         for t in ["wq", "wk", "wv", "wo", "wg", "wu", "wd"]:
             assert np.array_equal(blk.read_weight(layer, t), ob.weight(layer, t)), (layer, t)
     blk.free()
+
+
+def test_kv_copy_pages_moves_whole_pages(ctx):
+    """be_kv_copy_pages (KV migration data path): pages land byte-identical at their new slots,
+    contiguous runs coalesced, other pages untouched."""
+    shape = dev.BlockShape(n_layers=1, d_model=256, n_heads=4, d_ff=768, max_pos=64)
+    blk = dev.Block(ctx, shape, "m0", seed=2)
+    a = dev.KvPool(ctx, blk, 8)
+    b = dev.KvPool(ctx, blk, 8)
+    page_elems = shape.n_attention * 2 * shape.n_heads * 16 * shape.head_dim
+    n = 8 * page_elems
+
+    class _View:  # the pools' device memory as int16 tensors
+        def __init__(self, ptr):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2",
+                                             "data": (ptr, False), "version": 3}
+
+    ta = torch.as_tensor(_View(a.data_ptr), device="cuda")
+    tb = torch.as_tensor(_View(b.data_ptr), device="cuda")
+    ta.copy_(torch.randint(-30000, 30000, (n,), dtype=torch.int16, device="cuda"))
+    tb.zero_()
+    torch.cuda.synchronize()
+    src, dst = [2, 3, 4, 7], [5, 6, 7, 0]
+    dev.kv_copy_pages(ctx, a, b, src, dst)
+    ctx.sync()
+    pa = ta.view(8, page_elems).cpu()
+    pb = tb.view(8, page_elems).cpu()
+    for s_, d_ in zip(src, dst):
+        assert torch.equal(pa[s_], pb[d_])
+    for d_ in (1, 2, 3, 4):
+        assert not pb[d_].any()
+    a.free()
+    b.free()
+    blk.free()
