@@ -790,7 +790,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
       {
         eg.tl = tl_slot(ctx, BE_K_GEMM_GATE_UP);
         eg.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_GATE_UP, ntok, 2 * F, d, gemm_bytes(2 * F, d, ntok),
+        ProfScope ps(ctx, st, BE_K_GEMM_GATE_UP, ntok, 2 * F, d, gemm_bytes(2 * F, d, ntok) + 2.0 * (n_grp - 1) * (2 * F) * (d),
                      2.0 * (2 * F) * (d) * ntok);
         rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st);
       }
@@ -807,7 +807,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
       {
         ed.tl = tl_slot(ctx, BE_K_GEMM_DOWN);
         ed.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F, gemm_bytes(d, F, ntok),
+        ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F, gemm_bytes(d, F, ntok) + 2.0 * (n_grp - 1) * (d) * (F),
                      2.0 * (d) * (F) * ntok);
         rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st);
       }
@@ -837,7 +837,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     {
       eq.tl = tl_slot(ctx, BE_K_GEMM_QKV);
         eq.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_QKV, ntok, 3 * d, d, gemm_bytes(3 * d, d, ntok),
+        ProfScope ps(ctx, st, BE_K_GEMM_QKV, ntok, 3 * d, d, gemm_bytes(3 * d, d, ntok) + 2.0 * (n_grp - 1) * (3 * d) * (d),
                      2.0 * (3 * d) * (d) * ntok);
       rc = run_gemm(ctx, ws, L.wqkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st);
     }
@@ -884,7 +884,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     {
       eo.tl = tl_slot(ctx, BE_K_GEMM_O);
         eo.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d, gemm_bytes(d, d, ntok),
+        ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d, gemm_bytes(d, d, ntok) + 2.0 * (n_grp - 1) * (d) * (d),
                      2.0 * (d) * (d) * ntok);
       rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st);
     }
