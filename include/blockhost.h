@@ -105,6 +105,9 @@ typedef struct {
   int use_graphs;              /* capture steady-state decode steps in CUDA graphs */
   uint64_t seed;               /* synthetic prompt embeddings: stream "inputs:req<r>" */
   int dry_run;                 /* 1: control plane only (no device work; ctx may be NULL) */
+  int plan_ahead;              /* 1: bh_runner_decode_step plans step k+1 on the host while step
+                                  k runs on the device (hides host bookkeeping behind the GPU);
+                                  the request counters then run one step ahead */
 } bh_workload;
 
 typedef struct {

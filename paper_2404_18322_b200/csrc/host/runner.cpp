@@ -144,6 +144,23 @@ class Runner {
     int stride = 1;
   };
   std::vector<LaunchEntry> group_plans(const std::vector<PlannedBatch>& plans) const;
+  // one planned decode step: host bookkeeping done, metadata laid out, nothing on the device yet
+  struct StepPlan {
+    bool valid = false;
+    int group = -1;
+    std::vector<int> rows;  // live requests of the step, request order (host row order)
+    std::vector<PlannedBatch> plans;
+    std::vector<LaunchEntry> entries;
+    std::vector<size_t> off_tok, off_pt;
+    size_t total = 0;
+    std::vector<std::tuple<int, int, int>> sig;
+    bh_step_stats stats{};
+  };
+  StepPlan plan_step(int group, const std::vector<int>* members);
+  void stage_and_launch(StepPlan& sp, const void* host_in);
+  bool plan_ahead_ = false;  // plan step k+1 while step k runs (decode_step without a group)
+  StepPlan pending_;
+  void copy_host_rows(const std::vector<int>& rows, bool to_dev, void* host);
   void launch_entry(const std::vector<PlannedBatch>& plans, const LaunchEntry& le,
                     const be_token* d_tok, const int32_t* d_pt);
   struct GraphSlot {
@@ -176,6 +193,7 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   st_ = dry_ ? nullptr : static_cast<cudaStream_t>(be_ctx_stream(ctx));
   mode_ = w.mode;
   use_graphs_ = w.use_graphs != 0;
+  plan_ahead_ = w.plan_ahead != 0;
   if (const char* g = std::getenv("BH_GROUP")) group_ = std::atoi(g) != 0;
   max_batch_tokens_ = w.max_batch_tokens > 0 ? w.max_batch_tokens : 4096;
   d_ = w.blocks[0].d_model;
@@ -586,10 +604,10 @@ void Runner::launch_entry(const std::vector<PlannedBatch>& plans, const LaunchEn
   if (rc != BE_OK) throw BeError(rc, std::string("exec group: ") + be_last_error(ctx_));
 }
 
-void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, int group,
-                         const std::vector<int>* members) {
-  if (mode_ != 1) throw BeError(BE_ERR_STATE, "decode_step needs lockstep mode");
-  if (has_running_) throw BeError(BE_ERR_STATE, "prefill still running");
+Runner::StepPlan Runner::plan_step(int group, const std::vector<int>* members) {
+  StepPlan sp;
+  sp.valid = true;
+  sp.group = group;
   std::vector<int> order;
   if (members == nullptr) {
     order = step_done_order_;
@@ -605,88 +623,78 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
     for (int idx : step_done_order_) (in[idx] ? order : rest).push_back(idx);
     step_done_order_.swap(rest);
   }
-  // host rows are the live requests in request order; contiguous runs move in one copy
-  std::vector<int> rows = order;
-  std::sort(rows.begin(), rows.end());
-  const size_t row_bytes = (size_t)d_ * 2;
-  auto copy_rows = [&](bool to_dev, void* host) {
-    size_t i = 0;
-    while (i < rows.size()) {
-      size_t j = i + 1;
-      while (j < rows.size() && rows[j] == rows[j - 1] + 1) ++j;
-      char* dev = static_cast<char*>(arena_) + (size_t)rows[i] * row_bytes;
-      char* hp = static_cast<char*>(host) + i * row_bytes;
-      ck(cudaMemcpyAsync(to_dev ? (void*)dev : (void*)hp, to_dev ? (void*)hp : (void*)dev,
-                         (j - i) * row_bytes,
-                         to_dev ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st_),
-         "host rows");
-      i = j;
-    }
-  };
-  if (host_in != nullptr && !dry_) copy_rows(true, const_cast<void*>(host_in));
+  // host rows are the live requests in request order
+  sp.rows = order;
+  std::sort(sp.rows.begin(), sp.rows.end());
   for (int idx : order) dispatch(reqs_[idx]);
   // plan the whole step on the host (bookkeeping does not depend on GPU results)
-  std::vector<PlannedBatch> plans;
-  std::vector<Batch> batches;
+  const bh_step_stats saved = stats;
   stats = bh_step_stats{};
   for (;;) {
     pump();
     if (!has_running_) break;
-    plans.push_back(running_plan_);
-    batches.push_back(running_);
+    sp.plans.push_back(running_plan_);
     has_running_ = false;
     pool_.finish_batch(running_inst_, 0);
     account(running_plan_);
     ++batches_run_;
     for (const auto& m : running_.members) advance_after_step(reqs_[m.request_id - 1], m.chain_step);
   }
-  if (n_batches) *n_batches = static_cast<int>(plans.size());
-  if (dry_) return;
+  sp.stats = stats;
+  stats = saved;
+  if (dry_) return sp;
   // launches: single batches, and groups of independent same-shape batches
-  const std::vector<LaunchEntry> entries = group_plans(plans);
+  sp.entries = group_plans(sp.plans);
+  const auto& plans = sp.plans;
   auto ent_toks = [&](const LaunchEntry& le) -> const std::vector<be_token>& {
     return le.plans.size() == 1 ? plans[le.plans[0]].toks : le.toks;
   };
-  auto ent_pt = [&](const LaunchEntry& le) -> const std::vector<int32_t>& {
-    return le.plans.size() == 1 ? plans[le.plans[0]].pt : le.pt;
-  };
-  if (entries.size() != plans.size()) {  // launch accounting per grouped launch
-    stats.launches = 0;
-    for (const auto& le : entries) {
+  if (sp.entries.size() != plans.size()) {  // launch accounting per grouped launch
+    sp.stats.launches = 0;
+    for (const auto& le : sp.entries) {
       const PlannedBatch& p0 = plans[le.plans[0]];
-      stats.launches += be_exec_batch_launches(ctx_, blocks_[p0.block],
-                                               static_cast<int>(ent_toks(le).size()),
-                                               le.plans.size() == 1 ? p0.stride : le.stride);
+      sp.stats.launches += be_exec_batch_launches(ctx_, blocks_[p0.block],
+                                                  static_cast<int>(ent_toks(le).size()),
+                                                  le.plans.size() == 1 ? p0.stride : le.stride);
     }
   }
   // metadata layout: per launch [tokens][page table], 256-byte aligned
-  std::vector<size_t> off_tok(entries.size()), off_pt(entries.size());
-  size_t total = 0;
-  std::vector<std::tuple<int, int, int>> sig;
-  for (size_t i = 0; i < entries.size(); ++i) {
-    const auto& tk = ent_toks(entries[i]);
-    const auto& pt = ent_pt(entries[i]);
-    off_tok[i] = total;
-    total += (tk.size() * sizeof(be_token) + 255) & ~size_t(255);
-    off_pt[i] = total;
-    total += (pt.size() * sizeof(int32_t) + 255) & ~size_t(255);
-    const int stride = entries[i].plans.size() == 1 ? plans[entries[i].plans[0]].stride : entries[i].stride;
-    sig.emplace_back(plans[entries[i].plans[0]].block, static_cast<int>(tk.size()),
-                     stride * 16 + static_cast<int>(entries[i].plans.size()));
+  sp.off_tok.resize(sp.entries.size());
+  sp.off_pt.resize(sp.entries.size());
+  for (size_t i = 0; i < sp.entries.size(); ++i) {
+    const LaunchEntry& le = sp.entries[i];
+    const auto& tk = ent_toks(le);
+    const auto& pt = le.plans.size() == 1 ? plans[le.plans[0]].pt : le.pt;
+    sp.off_tok[i] = sp.total;
+    sp.total += (tk.size() * sizeof(be_token) + 255) & ~size_t(255);
+    sp.off_pt[i] = sp.total;
+    sp.total += (pt.size() * sizeof(int32_t) + 255) & ~size_t(255);
+    const int stride = le.plans.size() == 1 ? plans[le.plans[0]].stride : le.stride;
+    sp.sig.emplace_back(plans[le.plans[0]].block, static_cast<int>(tk.size()),
+                        stride * 16 + static_cast<int>(le.plans.size()));
   }
-  if (total > meta_cap_) {
+  return sp;
+}
+
+void Runner::stage_and_launch(StepPlan& sp, const void* host_in) {
+  const auto& plans = sp.plans;
+  const auto& entries = sp.entries;
+  const size_t row_bytes = (size_t)d_ * 2;
+  if (host_in != nullptr) copy_host_rows(sp.rows, true, const_cast<void*>(host_in));
+  if (sp.total > meta_cap_) {
     ck(cudaStreamSynchronize(st_), "meta grow");
     for (int k = 0; k < 2; ++k) {
       if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
       if (!meta_ev_[k]) ck(cudaEventCreateWithFlags(&meta_ev_[k], cudaEventDisableTiming), "meta ev");
     }
     if (meta_dev_) cudaFree(meta_dev_);
-    meta_cap_ = total * 2;
+    meta_cap_ = sp.total * 2;
     for (int k = 0; k < 2; ++k) ck(cudaMallocHost(&meta_host_[k], meta_cap_), "meta host");
     ck(cudaMalloc(&meta_dev_, meta_cap_), "meta dev");
     for (auto& kv : graphs_) kv.second.reset();  // captured graphs point into the old buffer
   }
-  GraphSlot& gs = graphs_[group];
+  (void)row_bytes;
+  GraphSlot& gs = graphs_[sp.group];
   // the device copy of the metadata is stream-ordered after the previous step's kernels; only
   // the host staging slot needs its earlier upload to have executed
   const int slot = meta_slot_;
@@ -694,26 +702,28 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
   ck(cudaEventSynchronize(meta_ev_[slot]), "meta reuse");
   char* stage = meta_host_[slot];
   for (size_t i = 0; i < entries.size(); ++i) {
-    const auto& tk = ent_toks(entries[i]);
-    const auto& pt = ent_pt(entries[i]);
-    std::memcpy(stage + off_tok[i], tk.data(), tk.size() * sizeof(be_token));
-    std::memcpy(stage + off_pt[i], pt.data(), pt.size() * sizeof(int32_t));
+    const LaunchEntry& le = entries[i];
+    const auto& tk = le.plans.size() == 1 ? plans[le.plans[0]].toks : le.toks;
+    const auto& pt = le.plans.size() == 1 ? plans[le.plans[0]].pt : le.pt;
+    std::memcpy(stage + sp.off_tok[i], tk.data(), tk.size() * sizeof(be_token));
+    std::memcpy(stage + sp.off_pt[i], pt.data(), pt.size() * sizeof(int32_t));
   }
-  ck(cudaMemcpyAsync(meta_dev_, stage, total, cudaMemcpyHostToDevice, st_), "meta h2d");
+  ck(cudaMemcpyAsync(meta_dev_, stage, sp.total, cudaMemcpyHostToDevice, st_), "meta h2d");
   ck(cudaEventRecord(meta_ev_[slot], st_), "meta ev record");
   auto launch_all = [&]() {
     for (size_t i = 0; i < entries.size(); ++i)
-      launch_entry(plans, entries[i], reinterpret_cast<const be_token*>(meta_dev_ + off_tok[i]),
-                   reinterpret_cast<const int32_t*>(meta_dev_ + off_pt[i]));
+      launch_entry(plans, entries[i], reinterpret_cast<const be_token*>(meta_dev_ + sp.off_tok[i]),
+                   reinterpret_cast<const int32_t*>(meta_dev_ + sp.off_pt[i]));
   };
+  stats = sp.stats;
   stats.graph_replayed = 0;
   if (be_prof_active(ctx_)) {
     launch_all();  // per-launch event timing: plain launches, the captured graph is kept
-    if (sig != gs.sig) gs.reset();
-  } else if (use_graphs_ && sig == gs.sig && gs.exec != nullptr) {
+    if (sp.sig != gs.sig) gs.reset();
+  } else if (use_graphs_ && sp.sig == gs.sig && gs.exec != nullptr) {
     ck(cudaGraphLaunch(gs.exec, st_), "graph launch");
     stats.graph_replayed = 1;
-  } else if (use_graphs_ && sig == gs.sig) {
+  } else if (use_graphs_ && sp.sig == gs.sig) {
     // second step with this structure: capture it
     ck(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal), "capture begin");
     try {
@@ -733,9 +743,49 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
     launch_all();
     gs.reset();
   }
-  gs.sig = sig;
+  gs.sig = sp.sig;
+}
+
+// host rows <-> arena rows of a step's live requests; contiguous runs move in one copy
+void Runner::copy_host_rows(const std::vector<int>& rows, bool to_dev, void* host) {
+  const size_t row_bytes = (size_t)d_ * 2;
+  size_t i = 0;
+  while (i < rows.size()) {
+    size_t j = i + 1;
+    while (j < rows.size() && rows[j] == rows[j - 1] + 1) ++j;
+    char* dev = static_cast<char*>(arena_) + (size_t)rows[i] * row_bytes;
+    char* hp = static_cast<char*>(host) + i * row_bytes;
+    ck(cudaMemcpyAsync(to_dev ? (void*)dev : (void*)hp, to_dev ? (void*)hp : (void*)dev,
+                       (j - i) * row_bytes, to_dev ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                       st_),
+       "host rows");
+    i = j;
+  }
+}
+
+void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, int group,
+                         const std::vector<int>* members) {
+  if (mode_ != 1) throw BeError(BE_ERR_STATE, "decode_step needs lockstep mode");
+  if (has_running_) throw BeError(BE_ERR_STATE, "prefill still running");
+  const bool whole = group < 0 && members == nullptr;
+  StepPlan sp;
+  if (pending_.valid) {
+    if (!whole) throw BeError(BE_ERR_STATE, "a planned-ahead whole step is pending");
+    sp = std::move(pending_);
+    pending_ = StepPlan{};
+  } else {
+    sp = plan_step(group, members);
+  }
+  if (n_batches) *n_batches = static_cast<int>(sp.plans.size());
+  if (dry_) {
+    stats = sp.stats;
+    return;
+  }
+  stage_and_launch(sp, host_in);
+  // plan step k+1 on the host while step k runs on the device (its inputs arrive next call)
+  if (plan_ahead_ && whole && !step_done_order_.empty()) pending_ = plan_step(-1, nullptr);
   if (host_out != nullptr) {
-    copy_rows(false, host_out);
+    copy_host_rows(sp.rows, false, host_out);
     ck(cudaStreamSynchronize(st_), "d2h sync");
   }
 }

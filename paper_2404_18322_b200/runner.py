@@ -27,7 +27,7 @@ class WorkloadC(C.Structure):
                 ("n_requests", C.c_int), ("req_tenant", C.c_void_p),
                 ("req_prompt", C.c_void_p), ("req_output", C.c_void_p),
                 ("max_batch_tokens", C.c_int), ("mode", C.c_int), ("use_graphs", C.c_int),
-                ("seed", C.c_uint64), ("dry_run", C.c_int)]
+                ("seed", C.c_uint64), ("dry_run", C.c_int), ("plan_ahead", C.c_int)]
 
 
 _bound = False
@@ -67,7 +67,7 @@ class Runner:
     """
 
     def __init__(self, ctx: Context | None, wl: Workload, mode: int = 1, use_graphs: bool = True,
-                 dry_run: bool = False):
+                 dry_run: bool = False, plan_ahead: bool = False):
         """ctx None with dry_run=True runs the control plane alone (no GPU work)."""
         _bind()
         self.ctx, self.wl = ctx, wl
@@ -92,7 +92,8 @@ class Runner:
         w = WorkloadC(len(wl.block_names), C.cast(descs, C.c_void_p), len(wl.chains),
                       k[1].ctypes.data, k[2].ctypes.data, wl.n_requests, k[3].ctypes.data,
                       k[4].ctypes.data, k[5].ctypes.data, wl.max_batch_tokens, mode,
-                      1 if use_graphs else 0, wl.seed, 1 if dry_run else 0)
+                      1 if use_graphs else 0, wl.seed, 1 if dry_run else 0,
+                      1 if plan_ahead else 0)
         h = C.c_void_p()
         rc = lib().bh_runner_create(ctx.h if ctx is not None else None, C.byref(w), C.byref(h))
         if rc != 0:

@@ -109,3 +109,22 @@ def test_c2_grouped_launch_count(ctx, monkeypatch):
         counts[flag] = run.step_stats()["launches"]
         run.close()
     assert counts["1"] < counts["0"]
+
+
+def test_c2_plan_ahead_gives_identical_rows(ctx):
+    # planning step k+1 while step k runs changes nothing computed
+    wl = CONFIGS["c2"](prompt=24, output=8)
+    d = wl.shape.d_model
+    outs = {}
+    for ahead in (False, True):
+        run = Runner(ctx, wl, mode=1, use_graphs=True, plan_ahead=ahead)
+        run.run()
+        rows = []
+        for _ in range(4):
+            h = torch.empty(64, d, dtype=torch.bfloat16)
+            run.decode_step(None, h)
+            rows.append(h.float().numpy().copy())
+        run.close()
+        outs[ahead] = rows
+    for a, b in zip(outs[False], outs[True]):
+        assert np.array_equal(a, b)
