@@ -27,6 +27,8 @@
 // Page ids and the running batch are private in the reference; the checker reads them.
 #define private public
 #include "blocksim/agent.hpp"
+#include "blocksim/config.hpp"
+#include "blocksim/costmodel.hpp"
 #include "blocksim/kv.hpp"
 #include "blocksim/metrics.hpp"
 #include "blocksim/scenario.hpp"
@@ -454,6 +456,22 @@ int rs_sim_batch(const rs_sim* h, int i, int32_t* rec, int32_t* members, int cap
     members[3 * j + 2] = std::get<2>(m[j]);
   }
   return 0;
+}
+
+// The reference's own profiles loader (config.cpp load_profiles) on a profiles.json, and its
+// CostModel::component_us lookup at (class, phase, batch, tokens): checks that measured B200
+// profiles (scripts/make_profiles.py) are accepted and read back as written.
+int rs_profile_component_us(const char* path, const char* cls, int prefill, double batch,
+                            double tokens, double* out, char* err, int err_cap) {
+  try {
+    blocksim::CostModel cm = blocksim::load_profiles(path);
+    *out = cm.component_us(cls, prefill ? blocksim::Phase::kPrefill : blocksim::Phase::kDecode,
+                           batch, tokens);
+    return 0;
+  } catch (const std::exception& e) {
+    std::snprintf(err, err_cap, "%s", e.what());
+    return 1;
+  }
 }
 
 }  // extern "C"

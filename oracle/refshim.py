@@ -124,3 +124,18 @@ def simulate(n_layers: int, dim: int, n_lora: int, first_adapted: int, prompts, 
         return blocks, kinds, chains, req_model, trace
     finally:
         L.rs_sim_free(h)
+
+
+def profile_component_us(path: str, cls: str, prefill: bool, batch: float, tokens: float) -> float:
+    """The reference's load_profiles + CostModel::component_us on a profiles.json."""
+    L = lib()
+    fn = L.rs_profile_component_us
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_double,
+                   C.POINTER(C.c_double), C.c_char_p, C.c_int]
+    out = C.c_double(0)
+    err = C.create_string_buffer(512)
+    if fn(path.encode(), cls.encode(), 1 if prefill else 0, batch, tokens, C.byref(out), err,
+          512) != 0:
+        raise ValueError(err.value.decode())
+    return out.value

@@ -384,3 +384,24 @@ def test_percentile_nearest_rank_matches_reference():
         q = rng.choice([0.5, 0.9, 0.95, 0.99, 1.0, rng.uniform(0.01, 1.0)])
         assert percentile(v, q) == R.percentile(v, q)
     assert percentile([], 0.95) == R.percentile([], 0.95) == 0.0
+
+
+def test_measured_b200_profiles_load_in_the_reference():
+    """profiles/b200_profiles.json (scripts/make_profiles.py: per-component B200 timings of this
+    repo's kernels in blocksim's schema) is accepted by the reference's own load_profiles and its
+    CostModel reads back the measured grid points."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "profiles", "b200_profiles.json")
+    prof = json.load(open(path))
+    for cls, c in prof["classes"].items():
+        for phase in ("decode", "prefill"):
+            g = c[phase]
+            for i, b in enumerate(g["batch"]):
+                for j, t in enumerate(g["tokens"]):
+                    got = R.profile_component_us(path, cls, phase == "prefill", b, t)
+                    assert got == pytest.approx(g["us"][i][j], rel=1e-12)
+    # attention cost grows with context at a fixed batch (the KV read), as the kernels do
+    dec = prof["classes"]["attention:4096"]["decode"]["us"]
+    assert dec[-1][-1] > 2 * dec[-1][0]
