@@ -55,6 +55,24 @@ struct AttnParams {
   int tl_cap;
 };
 cudaError_t launch_attention(const AttnParams&, int rows, int head_dim, cudaStream_t);
+// attention_prefill.cu
+struct PrefillAttnParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* pool;
+  long long page_elems;
+  long long layer_elems;
+  int layer;
+  const int* page_table;
+  int pt_stride;
+  const int* tok;
+  int rows;
+  int H;
+  float scale_log2;
+  __nv_bfloat16* out;
+  int* tiles;
+};
+cudaError_t launch_attention_prefill(const PrefillAttnParams&, int head_dim, int num_sms,
+                                     cudaStream_t);
 }  // namespace bx
 
 using bx::EpiParams;
@@ -74,6 +92,7 @@ struct be_ctx {
   int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
   int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
   int gemm_deep = 1;      // GEMM ring depth: 1 deep (one CTA/SM), 0 shallow (BE_GEMM_RING)
+  int prefill_tc = 1;     // tensor-core prefill attention (BE_PREFILL_TC=0: the per-row kernel)
   // per-launch event timing of exec_batch kernels (be_prof_enable); off on the hot path
   struct ProfRec {
     be_prof_rec r;
@@ -133,6 +152,7 @@ struct be_workspace {
   size_t splitws_elems = 0;
   int* counters = nullptr;
   int n_counters = 0;
+  int* prefill_tiles = nullptr;  // [max_tok + 1] query tiles of the tensor-core prefill attention
   float* attn_part = nullptr;
   size_t attn_part_elems = 0;
   be_token* d_tokens = nullptr;
@@ -253,6 +273,7 @@ extern "C" int be_ctx_create(int device, be_ctx** out) {
   ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   if (const char* g = getenv("BE_GEMM_GRID")) ctx->gemm_grid_cap = atoi(g);
   if (const char* p = getenv("BE_PDL")) ctx->use_pdl = atoi(p) != 0;
+  if (const char* p = getenv("BE_PREFILL_TC")) ctx->prefill_tc = atoi(p) != 0;
   if (const char* r = getenv("BE_GEMM_RING")) ctx->gemm_deep = strcmp(r, "shallow") != 0;
   *out = ctx;
   return BE_OK;
@@ -509,6 +530,7 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
   ok &= cudaMalloc(&w->splitws, w->splitws_elems * sizeof(float)) == cudaSuccess;
   w->n_counters = 1 << 16;
   ok &= cudaMalloc(&w->counters, w->n_counters * sizeof(int)) == cudaSuccess;
+  ok &= cudaMalloc(&w->prefill_tiles, (T + 1) * sizeof(int)) == cudaSuccess;
   const size_t part_rows = T < 1024 ? T : 1024;
   w->attn_part_elems = part_rows * H * 16 * (128 + 2);
   ok &= cudaMalloc(&w->attn_part, w->attn_part_elems * sizeof(float)) == cudaSuccess;
@@ -544,7 +566,7 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
 extern "C" int be_workspace_free(be_workspace* w) {
   if (w == nullptr) return BE_ERR_INVALID;
   cudaSetDevice(w->ctx->device);
-  void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->ss, w->splitws, w->counters,
+  void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->ss, w->splitws, w->counters, w->prefill_tiles,
                   w->attn_part, w->d_tokens, w->d_pt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -721,7 +743,6 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
 int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* pools,
              be_workspace* ws, int phase, int ntok, const be_token* d_tok, int pt_stride,
              const int32_t* d_pt, const void* arena_in, void* arena_out, cudaStream_t st) {
-  (void)phase;
   be_block* blk = blks[0];
   be_kv_pool* pool = pools[0];
   const auto& D = blk->desc;
@@ -868,7 +889,26 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     if (ap.tl != nullptr && splits > 1) tl_slot(ctx, BE_K_ATTENTION);  // combine's slot = tl + 1
     {
       ProfScope ps(ctx, st, BE_K_ATTENTION, ntok, H, hd, 0, 0);
-      e = bx::launch_attention(ap, ntok, hd, st);
+      if (phase == BE_PHASE_PREFILL && n_grp == 1 && ctx->prefill_tc) {
+        // prompt rows: query tiles share K/V tiles on tensor cores
+        bx::PrefillAttnParams pp{};
+        pp.q = ws->q;
+        pp.pool = pool->base;
+        pp.page_elems = pool->page_elems;
+        pp.layer_elems = pool->layer_elems;
+        pp.layer = l;
+        pp.page_table = d_pt;
+        pp.pt_stride = pt_stride;
+        pp.tok = tok;
+        pp.rows = ntok;
+        pp.H = H;
+        pp.scale_log2 = ap.scale_log2;
+        pp.out = ws->attn;
+        pp.tiles = ws->prefill_tiles;
+        e = bx::launch_attention_prefill(pp, hd, ctx->num_sms, st);
+      } else {
+        e = bx::launch_attention(ap, ntok, hd, st);
+      }
     }
     if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "attention: %s", cudaGetErrorString(e));
 
