@@ -91,7 +91,6 @@ struct be_ctx {
   int* gemm_counters = nullptr;
   int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
   int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
-  int gemm_deep = 1;      // GEMM ring depth: 1 deep (one CTA/SM), 0 shallow (BE_GEMM_RING)
   int prefill_tc = 1;     // tensor-core prefill attention (BE_PREFILL_TC=0: the per-row kernel)
   // per-launch event timing of exec_batch kernels (be_prof_enable); off on the hot path
   struct ProfRec {
@@ -274,7 +273,6 @@ extern "C" int be_ctx_create(int device, be_ctx** out) {
   if (const char* g = getenv("BE_GEMM_GRID")) ctx->gemm_grid_cap = atoi(g);
   if (const char* p = getenv("BE_PDL")) ctx->use_pdl = atoi(p) != 0;
   if (const char* p = getenv("BE_PREFILL_TC")) ctx->prefill_tc = atoi(p) != 0;
-  if (const char* r = getenv("BE_GEMM_RING")) ctx->gemm_deep = strcmp(r, "shallow") != 0;
   *out = ctx;
   return BE_OK;
 }
@@ -726,9 +724,7 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
   if (p.ws_needed > ws->splitws_elems || p.tiles > ws->n_counters)
     return fail(ctx, BE_ERR_INVALID, "gemm N=%d K=%d ntok=%d: stream-K workspace too small", N, K, ntok);
   L.grid = p.grid;
-  L.max_contrib = p.max_contrib;
   L.pdl = ctx->use_pdl;
-  L.deep = ctx->gemm_deep;
   epi.ws = ws->splitws;
   epi.counters = ws->counters;
   L.epi = epi;
@@ -1185,11 +1181,7 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   const int bn = bx::gemm_pick_bn(ntok);
   CUtensorMap mx;
   int rc;
-  // BE_GEMM_BREP=k: x holds k replicas of the activations, each padded to a BN multiple
-  const int brep = getenv("BE_GEMM_BREP") ? atoi(getenv("BE_GEMM_BREP")) : 1;
-  const int copy_rows = (ntok + bn - 1) / bn * bn;
-  if ((rc = make_map(ctx, &mx, x, brep > 1 ? (uint64_t)brep * copy_rows : ntok, K, bn)) != BE_OK)
-    return rc;
+  if ((rc = make_map(ctx, &mx, x, ntok, K, bn)) != BE_OK) return rc;
   const bx::GemmPlan p =
       bx::gemm_plan(N, K, ntok, bn, ctx->num_sms, (size_t)1 << 40, 1 << 16, grid_cap);
   if (p.ws_needed > ctx->gemm_ws_elems) {
@@ -1211,13 +1203,8 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.K = K;
   L.bn = bn;
   L.grid = p.grid;
-  L.max_contrib = p.max_contrib;
   L.pdl = ctx->use_pdl;
-  L.deep = ctx->gemm_deep;
   L.epi.mode = bx::kStore;
-  L.b_copies = brep > 1 ? brep : 1;
-  L.b_copy_rows = copy_rows;
-  if (const char* v = getenv("BE_GEMM_DBG")) L.epi.dbg = atoi(v);
   L.epi.ntok = ntok;
   L.epi.out = static_cast<bf16*>(out);
   L.epi.ldo = N;

@@ -232,9 +232,7 @@ template <int BN, int STAGES, int CTAS, int MODE>
 __global__ void __launch_bounds__(192, CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
-                   int max_contrib, int b_copies, int b_copy_rows, EpiParams E) {
-  // activation replica this CTA reads (spreads same-k-block reads over L2 slices)
-  const int b_row0 = (int)(blockIdx.x % b_copies) * b_copy_rows;
+                   EpiParams E) {
   using S = GemmSmem<BN>;
   constexpr uint32_t kTmemCols = tmem_cols<2 * BN>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -303,7 +301,7 @@ __global__ void __launch_bounds__(192, CTAS)
       for (int i = 0; i < pre && load_b; ++i) {
         const long long it = it_begin + i;
         const int tile = (int)(it / nkb), kb = (int)(it % nkb);
-        tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, kb * kBK, (tile / m_tiles) * BN + b_row0,
+        tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
                     kEvictLast);
       }
       for (long long i = pre; i < n_it; ++i) {
@@ -315,7 +313,7 @@ __global__ void __launch_bounds__(192, CTAS)
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         bulk_load(sA + s * S::kABytes, wtile(it), S::kABytes, &full[s], kEvictFirst);
         if (load_b)
-          tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN + b_row0,
+          tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
                       kEvictLast);
       }
       stamp(E, 3);
@@ -552,7 +550,7 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = L.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, L.w_packed, *L.map_x, L.K, m_tiles, n_tiles,
-                            L.max_contrib, L.b_copies > 0 ? L.b_copies : 1, L.b_copy_rows, L.epi);
+                            L.epi);
 }
 
 template <int MODE>
@@ -622,7 +620,6 @@ GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems,
   while (g > 1 && (size_t)g * bn * kBM > ws_elems) g /= 2;
   (void)n_counters;
   p.grid = (int)g;
-  p.max_contrib = 1;
   p.ws_needed = (size_t)g * bn * kBM;
   p.tiles = tiles;
   return p;

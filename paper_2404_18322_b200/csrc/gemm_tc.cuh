@@ -57,7 +57,6 @@ struct EpiParams {
   __nv_bfloat16* kvgrp[kMaxGroup];
   unsigned long long* tl;     // diagnostics: kernel timeline slot (ptx.cuh tl_*), nullptr = off
   int tl_cap;
-  int dbg;                    // diagnostics: bit0 skip MMA, bit1 skip activation loads
 };
 
 constexpr int kBM = 128;
@@ -70,26 +69,13 @@ struct GemmSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
 };
 
-// Ring depth. Decode shapes (BN <= 128) keep ~100 KB of stages so two CTAs fit on an SM: the
-// next GEMM of the chain (programmatic dependent launch) becomes resident beside the current
-// one and streams its first weight tiles under the current GEMM's tail. ~100 KB in flight per
-// SM is well above HBM bandwidth x unloaded latency (~45 KB/SM). Prefill tiles (BN = 256) are
-// tensor-bound and take the deep ring instead.
-template <int BN>
-__host__ __device__ constexpr int gemm_stages() {
-  if (BN >= 256) return (200 * 1024) / GemmSmem<BN>::kStageBytes;
-  int s = (100 * 1024) / GemmSmem<BN>::kStageBytes;
-  return s > 8 ? 8 : s;
-}
+// Ring depth: up to 8 stages / ~200 KB, one CTA per SM. Measured slower: deeper rings
+// (12 x 18-24 KB), ~100 KB rings with two CTAs per SM, and ~100 KB rings leaving room for the
+// next PDL-launched GEMM beside this one.
 template <int BN>
 __host__ __device__ constexpr int gemm_stages_deep() {
-  // up to 8 stages / ~200 KB; deeper rings (12 x 18-24 KB) measured slower on every shape
   const int s = (200 * 1024) / GemmSmem<BN>::kStageBytes;
   return s > 8 ? 8 : s;
-}
-template <int BN>
-__host__ __device__ constexpr int gemm_ctas_per_sm() {
-  return BN >= 256 ? 1 : 2;
 }
 
 template <int BN>
@@ -104,17 +90,12 @@ struct GemmLaunch {
   int N, K;
   int bn;                    // 16/32/64/128/256
   int grid;                  // persistent CTAs (stream-K ranges)
-  int max_contrib;           // workspace slots per tile
   int pdl;                   // launch with programmatic stream serialization
-  int deep;                  // 1: ~200 KB ring, one CTA/SM; 0: ~100 KB ring, two CTAs/SM
-  int b_copies;              // activation replicas (CTA c reads replica c % b_copies); 0/1 = one
-  int b_copy_rows;           // rows between replicas in map_x
   EpiParams epi;
 };
 
 struct GemmPlan {
   int grid;
-  int max_contrib;
   size_t ws_needed;  // fp32 elements of split-tile partials
   long long tiles;   // arrival counters needed
 };

@@ -41,16 +41,7 @@ def main():
         copies = max(2, int(3 * 126e6 // (N * K * 2)) + 1)
         ws = [dev.pack_weight(ctx, (torch.rand(N, K, device="cuda", dtype=torch.bfloat16) - 0.5) * 0.05)
               for _ in range(copies)]
-        brep = int(os.environ.get("BE_GEMM_BREP", "1"))
-        if brep > 1:
-            bn = 16 if ntok <= 16 else 32 if ntok <= 32 else 64 if ntok <= 64 else 128 if ntok <= 128 else 256
-            rows = (ntok + bn - 1) // bn * bn
-            base = torch.randn(ntok, K, device="cuda").to(torch.bfloat16)
-            x = torch.zeros(brep * rows, K, device="cuda", dtype=torch.bfloat16)
-            for r in range(brep):
-                x[r * rows:r * rows + ntok] = base
-        else:
-            x = torch.randn(ntok, K, device="cuda").to(torch.bfloat16)
+        x = torch.randn(ntok, K, device="cuda").to(torch.bfloat16)
         out = torch.empty(ntok, N, device="cuda", dtype=torch.bfloat16)
         ptrs = (C.c_void_p * copies)(*[w.data_ptr() for w in ws])
         us = C.c_float(0)
