@@ -36,7 +36,10 @@ def main():
     ap.add_argument("--ticks", type=int, default=12)
     ap.add_argument("--exact", action="store_true",
                     help="token budget = one prompt, so every prefill batch holds one request on "
-                         "both sides: identical GEMM shapes everywhere, outputs must be bit-exact")
+                         "both sides: identical GEMM shapes everywhere, outputs must be bit-exact. "
+                         "Use a prompt >= the decode batch (64): a smaller budget also splits "
+                         "decode batches, and the two runs (different chain ends per stage) can "
+                         "then group different batch sizes")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_pipeline_two_gpus_bit_exact():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29561",
-           os.path.join(ROOT, "scripts", "pipeline_check.py"), "--config", "c2", "--prompt", "32",
+           os.path.join(ROOT, "scripts", "pipeline_check.py"), "--config", "c2", "--prompt", "64",
            "--ticks", "8", "--exact"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
