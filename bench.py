@@ -344,10 +344,16 @@ def profile_step(ctx, run, wl, stream, peaks, peaks_kind):
 
 
 def make_workload(args, output=None):
+    """The BASELINE config (configs[0..3] = c1..c4) at its own prompt / decode lengths unless
+    --prompt / --output override them; `output` raises the decode length if a run needs more."""
     from paper_2404_18322_b200.workloads import CONFIGS
-    out = output or args.output
-    return CONFIGS[args.config](prompt=args.prompt, output=out) if args.config != "c1" \
-        else CONFIGS["c1"](output=out)
+    kw = {}
+    if args.prompt is not None and args.config != "c1":
+        kw["prompt"] = args.prompt
+    out = max(filter(None, [output, args.output])) if (output or args.output) else None
+    if out is not None:
+        kw["output"] = out
+    return CONFIGS[args.config](**kw)
 
 
 def run_pipeline(args, world, rank, local, depth, why):
@@ -364,7 +370,7 @@ def run_pipeline(args, world, rank, local, depth, why):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     total = ticks_needed(depth, args.steps, args.warmup)
     need = tokens_per_request_needed(depth, total, depth) + 1
-    wl = make_workload(args, max(args.output, need))
+    wl = make_workload(args, need)
     ctx = Context(local)
     group, st_idx = divmod(rank, depth)
     stage = PipelineStage(ctx, wl, depth, st_idx, base_rank=group * depth)
@@ -606,9 +612,7 @@ def run_reference(args, world, rank, local):
     is our fp32 oracle port of the block forward, with all host threads)."""
     if rank != 0:
         return
-    from paper_2404_18322_b200.workloads import CONFIGS
-    wl = CONFIGS[args.config](prompt=args.prompt, output=args.output) if args.config != "c1" \
-        else CONFIGS["c1"](output=args.output)
+    wl = make_workload(args)
     threads = os.cpu_count() or 1
     vals = []
     for i in range(args.warmup + args.steps):
@@ -637,8 +641,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
-    ap.add_argument("--prompt", type=int, default=512)
-    ap.add_argument("--output", type=int, default=128)
+    ap.add_argument("--prompt", type=int, default=None, help="default: the config's own")
+    ap.add_argument("--output", type=int, default=None, help="default: the config's own")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
@@ -653,8 +657,8 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     world, rank, local = dist_setup()
-    need = 1 + args.warmup + 2 * args.steps + 2
-    if args.output < need:
+    need = 1 + args.warmup + 2 * args.steps + 2  # value leg + e2e leg + the profiled steps
+    if make_workload(args).req_output[0] < need:
         args.output = need
     if args.impl == "reference":
         run_reference(args, world, rank, local)

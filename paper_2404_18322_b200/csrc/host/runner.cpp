@@ -547,14 +547,14 @@ std::vector<Runner::LaunchEntry> Runner::group_plans(const std::vector<PlannedBa
     LaunchEntry le;
     le.plans.push_back(static_cast<int>(i));
     const PlannedBatch& a = plans[i];
-    const size_t n = a.toks.size();
-    const bool groupable = group_ && a.phase == Phase::kDecode && (n == 16 || n == 32 || n == 64);
+    const bool groupable = group_ && a.phase == Phase::kDecode && a.toks.size() <= 64;
     std::vector<int> seen;
     for (const auto& t : a.toks) seen.push_back(t.src_row);
     size_t j = i + 1;
+    size_t rmax = a.toks.size();
     while (groupable && j < plans.size() && le.plans.size() < 8) {
       const PlannedBatch& b = plans[j];
-      if (b.phase != Phase::kDecode || b.toks.size() != n || comps_[b.block] != comps_[a.block] ||
+      if (b.phase != Phase::kDecode || b.toks.size() > 64 || comps_[b.block] != comps_[a.block] ||
           descs_[b.block].d_ff != descs_[a.block].d_ff || b.block == a.block)
         break;
       bool disjoint = true;
@@ -563,9 +563,13 @@ std::vector<Runner::LaunchEntry> Runner::group_plans(const std::vector<PlannedBa
       if (!disjoint) break;
       for (const auto& t : b.toks) seen.push_back(t.src_row);
       le.plans.push_back(static_cast<int>(j));
+      rmax = std::max(rmax, b.toks.size());
       ++j;
     }
     if (le.plans.size() > 1) {
+      // rows per block: the GEMM n-tile (16/32/64); shorter batches get padding rows that are
+      // computed but never stored (dst -1, no KV slot, empty context)
+      const size_t R = rmax <= 16 ? 16 : rmax <= 32 ? 32 : 64;
       for (int k : le.plans) le.stride = std::max(le.stride, plans[k].stride);
       int row0 = 0;
       for (int k : le.plans) {
@@ -573,6 +577,15 @@ std::vector<Runner::LaunchEntry> Runner::group_plans(const std::vector<PlannedBa
         for (be_token t : pb.toks) {
           t.pt_row += row0;
           le.toks.push_back(t);
+        }
+        for (size_t p = pb.toks.size(); p < R; ++p) {
+          be_token pad;
+          pad.src_row = pb.toks[0].src_row;
+          pad.dst_row = -1;
+          pad.kv_slot = -1;
+          pad.pos = -1;
+          pad.pt_row = row0;
+          le.toks.push_back(pad);
         }
         for (int r = 0; r < pb.n_rows; ++r)
           for (int c = 0; c < le.stride; ++c)

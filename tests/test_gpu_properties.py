@@ -82,11 +82,13 @@ class _Rows:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
-def test_c2_grouped_private_blocks_match_separate_batches(ctx, monkeypatch):
-    # the 4 tenants' private blocks at a chain position run as one grouped launch
-    # (be_exec_group_dev); results equal the per-block batches within bf16 tolerance (split-K
-    # plans differ with the grouped tile count, so summation order does)
-    wl = CONFIGS["c2"](prompt=24, output=6)
+@pytest.mark.parametrize("config", ["c2", "c3"])
+def test_grouped_private_blocks_match_separate_batches(ctx, monkeypatch, config):
+    # the tenants' private blocks at a chain position run as one grouped launch
+    # (be_exec_group_dev; C2: 4 blocks x 16 rows, C3: 8 blocks x 4 rows padded to 16); results
+    # equal the per-block batches within bf16 tolerance (split-K plans differ with the grouped
+    # tile count, so summation order does)
+    wl = CONFIGS[config](prompt=24, output=6)
     monkeypatch.setenv("BH_GROUP", "1")
     grouped = _decode_rows(ctx, wl, 3)
     monkeypatch.setenv("BH_GROUP", "0")
