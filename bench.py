@@ -41,20 +41,41 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML polled every 10 ms on
+    a thread (nvidia-smi's own 200 ms loop as the fallback), so even a ~0.25 s region holds
+    dozens of samples."""
 
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_s: float = 0.01):
         self.gpu = gpu
+        self.period = period_s
         self.proc = None
-        self.lines = []  # (arrival time, csv line)
+        self.nvml = None
+        self.samples = []  # (time, sm_mhz, max_mhz, frozenset(reasons))
         self.t = None
         self.t0 = 0.0
+        self.stop_ev = threading.Event()
 
     def start(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self.nvml = (N, h, bits, mx)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -65,45 +86,55 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        N, h, bits, mx = self.nvml
+        while not self.stop_ev.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.time(), float(sm), float(mx),
+                                     frozenset(n for n, b in bits.items() if r & b)))
+            except Exception:
+                pass
+            self.stop_ev.wait(self.period)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                self.samples.append((time.time(), float(parts[0]), float(parts[1]), frozenset(
+                    n for n, v in zip(self.NAMES, parts[3:7]) if v.lower().startswith("active"))))
+            except ValueError:
+                continue
 
     def mark(self):
         """Start of the timed region (the sampler runs from before warm-up, so samples exist)."""
         self.t0 = time.time()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
+        if self.nvml is None and self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        self.stop_ev.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
         if self.t:
             self.t.join(timeout=1)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        t0 = getattr(self, "t0", 0.0)
-        inside = [ln for ts, ln in self.lines if ts >= t0]
-        if not inside and self.lines:  # region shorter than the sampling period: nearest sample
-            inside = [self.lines[-1][1]]
-        for ln in inside:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        inside = [s for s in self.samples if s[0] >= self.t0]
+        if not inside and self.samples:  # region shorter than the sampling period: nearest sample
+            inside = [self.samples[-1]]
+        reasons = set()
+        for s in inside:
+            reasons |= s[3]
+        return {"sm_mhz": statistics.median(s[1] for s in inside) if inside else None,
+                "sm_max_mhz": max(s[2] for s in inside) if inside else None,
+                "reasons": sorted(reasons), "samples": len(inside),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_setup():
