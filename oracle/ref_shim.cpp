@@ -32,6 +32,8 @@
 #include "blocksim/kv.hpp"
 #include "blocksim/metrics.hpp"
 #include "blocksim/scenario.hpp"
+#include "blocksim/scheduler.hpp"
+#include "blocksim/cluster.hpp"
 #include "blocksim/zoo.hpp"
 #undef private
 
@@ -473,5 +475,339 @@ int rs_profile_component_us(const char* path, const char* cls, int prefill, doub
     return 1;
   }
 }
+
+
+// ---------------------------------------------------------------- scheduler decisions in flight
+// Runs a multi-device Simulation (LoRA + fully fine-tuned models with equivalence edges, memory
+// tight enough to evict, speculation / scaling / placement reviews on) and, every `every`-th
+// engine event, records the complete state the Scheduler reads plus its answers: choose_binding
+// for every live request's current step, speculation_marks, scale_decisions, placement_moves,
+// choose_device per block and preference, migration_rates, param_bytes_needed. Output is JSON;
+// tests/test_policy.py replays each snapshot into bh_policy (include/blockpolicy.h).
+struct rs_policy_trace {
+  std::string out;
+  std::string err;
+};
+
+namespace {
+nlohmann::json grid_json(const Interp2D& g) {
+  nlohmann::json v = nlohmann::json::array();
+  for (const auto& row : g.v) v.push_back(row);
+  return {{"xs", g.xs}, {"ys", g.ys}, {"v", v}};
+}
+nlohmann::json choice_json(const std::optional<BindingChoice>& c) {
+  if (!c) return nullptr;
+  return {{"block", c->block_id}, {"stitch", c->stitch_class}, {"instance", c->instance_id},
+          {"device", c->device}, {"adaptive", c->adaptive}, {"evict", c->evict_bytes},
+          {"est", {c->est.queue_us, c->est.compute_us, c->est.transfer_us, c->est.load_us}}};
+}
+}  // namespace
+
+rs_policy_trace* rs_policy_trace_run(const char* spec_json) {
+  auto* h = new rs_policy_trace();
+  try {
+    const auto spec = nlohmann::json::parse(spec_json);
+    const int n_layers = spec.value("n_layers", 4), dim = spec.value("dim", 64);
+    const int n_lora = spec.value("n_lora", 2), n_ff = spec.value("n_ff", 2);
+    const int n_servers = spec.value("n_servers", 2), per_server = spec.value("per_server", 2);
+    const std::int64_t capacity = spec.value("capacity", (std::int64_t)64 << 20);
+    const std::int64_t att_bytes = spec.value("att_bytes", (std::int64_t)4 << 20);
+    const std::int64_t ffn_bytes = spec.value("ffn_bytes", (std::int64_t)8 << 20);
+    const int every = spec.value("every", 7), max_snaps = spec.value("max_snapshots", 60);
+    std::uint64_t rng = spec.value("seed", 1);
+    auto next = [&rng]() {  // splitmix64
+      std::uint64_t z = (rng += 0x9E3779B97F4A7C15ull);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      return z ^ (z >> 31);
+    };
+    auto unif = [&next]() { return (next() >> 11) * (1.0 / 9007199254740992.0); };
+
+    Zoo zoo(0.98);
+    std::vector<ComponentDescriptor> base;
+    std::vector<LayerSignature> base_sigs;
+    for (int l = 0; l < n_layers; ++l) {
+      for (int k = 0; k < 2; ++k) {
+        ComponentDescriptor c;
+        c.id = "base." + std::string(k ? "ffn" : "att") + std::to_string(l);
+        c.kind = k ? ComponentKind::kFfn : ComponentKind::kAttention;
+        c.embed_dim = dim;
+        c.model_id = "base";
+        c.layer = l;
+        c.slot = k;
+        c.contents = {{c.id + ".w", k ? ffn_bytes : att_bytes}};
+        base.push_back(c);
+      }
+      LayerSignature s{"base", l, {}};
+      for (int i = 0; i < 8; ++i) s.probs.push_back(1.0 + i + 0.1 * l);
+      base_sigs.push_back(s);
+    }
+    zoo.add_foundation("base", base);
+    for (int v = 0; v < n_lora; ++v) {
+      const std::string m = "lora" + std::to_string(v);
+      const int first = 1 + v % std::max(1, n_layers - 1);
+      std::vector<ComponentDescriptor> comps;
+      for (int l = 0; l < n_layers; ++l) {
+        if (l >= first) {
+          ComponentDescriptor att;
+          att.id = m + ".att" + std::to_string(l);
+          att.kind = ComponentKind::kAttention;
+          att.embed_dim = dim;
+          att.model_id = m;
+          att.layer = l;
+          att.slot = 0;
+          att.attach = "fuse";
+          att.contents = {{"base.att" + std::to_string(l) + ".w", att_bytes},
+                          {m + ".delta" + std::to_string(l), att_bytes / 64}};
+          comps.push_back(att);
+        } else {
+          comps.push_back(zoo.component("base.att" + std::to_string(l)));
+        }
+        comps.push_back(zoo.component("base.ffn" + std::to_string(l)));
+      }
+      zoo.add_model_pe(m, TuningKind::kLora, "base", comps);
+    }
+    for (int v = 0; v < n_ff; ++v) {
+      const std::string m = "ft" + std::to_string(v);
+      std::vector<ComponentDescriptor> comps;
+      std::vector<LayerSignature> sigs;
+      for (int l = 0; l < n_layers; ++l) {
+        for (int k = 0; k < 2; ++k) {
+          ComponentDescriptor c;
+          c.id = m + "." + std::string(k ? "ffn" : "att") + std::to_string(l);
+          c.kind = k ? ComponentKind::kFfn : ComponentKind::kAttention;
+          c.embed_dim = dim;
+          c.model_id = m;
+          c.layer = l;
+          c.slot = k;
+          c.contents = {{c.id + ".w", k ? ffn_bytes : att_bytes}};
+          comps.push_back(c);
+        }
+        // the first (v+1) layers track the foundation (equivalent), the rest diverge
+        LayerSignature s{m, l, base_sigs[l].probs};
+        if (l > v) std::reverse(s.probs.begin(), s.probs.end());
+        sigs.push_back(s);
+      }
+      zoo.add_model_ff(m, "base", comps, sigs, base_sigs);
+    }
+
+    Cluster cl;
+    for (int s = 0; s < n_servers; ++s) cl.add_server({s, spec.value("intra_bps", 300e9)});
+    cl.set_inter_default(spec.value("inter_bps", 25e9));
+    if (n_servers >= 2) cl.set_inter_bandwidth(0, 1, spec.value("inter01_bps", 50e9));
+    for (int s = 0; s < n_servers; ++s)
+      for (int d = 0; d < per_server; ++d)
+        cl.add_device({s * per_server + d, s, d % 2 ? "slow" : "fast",
+                       capacity + (std::int64_t)(d * 3) * (1 << 20), 1e12,
+                       spec.value("load_bps", 16e9)});
+    CostModel cost;
+    cost.set_device_class("fast", 1.0);
+    cost.set_device_class("slow", 0.625);
+    auto grid = [&](double coef, bool prefill) {
+      Interp2D g;
+      g.xs = {1, 4, 16, 64};
+      g.ys = prefill ? std::vector<double>{1, 64, 512, 4096} : std::vector<double>{1, 256, 2048, 8192};
+      for (double x : g.xs) {
+        std::vector<double> row;
+        for (double y : g.ys)
+          row.push_back(coef * (prefill ? 0.5 * x * y : 20.0 + x + y / 64.0) * (0.9 + 0.2 * unif()));
+        g.v.push_back(row);
+      }
+      return g;
+    };
+    ComponentClassProfile att{grid(3.0, true), grid(4.0, false), -1};
+    ComponentClassProfile ffn{grid(5.0, true), grid(6.0, false), 0};
+    cost.add_class(CostModel::class_key(ComponentKind::kAttention, dim), att);
+    cost.add_class(CostModel::class_key(ComponentKind::kFfn, dim), ffn);
+
+    std::vector<Request> reqs;
+    const auto prompts = spec.at("prompts").get<std::vector<int>>();
+    const auto outputs = spec.at("outputs").get<std::vector<int>>();
+    const auto gaps = spec.at("gaps").get<std::vector<std::int64_t>>();
+    SimTime t = 0;
+    for (std::size_t i = 0; i < prompts.size(); ++i) {
+      Request r;
+      r.id = i + 1;
+      r.app_id = (int)i;
+      t += gaps[i];
+      r.arrival_us = t;
+      r.prompt_tokens = prompts[i];
+      r.output_tokens = outputs[i];
+      reqs.push_back(r);
+    }
+    ScenarioConfig cfg;
+    cfg.name = "policy-parity";
+    cfg.seed = spec.value("seed", 1);
+    cfg.speculation = spec.value("speculation", true);
+    cfg.spec_fraction = spec.value("spec_fraction", 0.25);
+    cfg.adaptive = spec.value("adaptive", true);
+    cfg.least_busy = spec.value("least_busy", false);
+    cfg.placement = spec.value("frag_min", false) ? PlacementPolicy::kFragMin : PlacementPolicy::kLocality;
+    cfg.scaling = spec.value("scaling", true);
+    cfg.scale_queue_us = spec.value("scale_queue_us", (std::int64_t)3000);
+    cfg.expected_tokens = spec.value("expected_tokens", 64);
+    cfg.max_batch_tokens = spec.value("max_batch_tokens", 512);
+    cfg.review_period_us = spec.value("review_period_us", (std::int64_t)5000);
+    cfg.kv_review_period_us = spec.value("kv_review_period_us", (std::int64_t)2000);
+    cfg.metrics_tick_us = us_from_s(1e6);
+
+    Simulation sim(cfg, zoo, cl, cost, reqs);
+    const Zoo& pz = sim.plan_.zoo;
+    const CostModel& cm = sim.cost_;
+    nlohmann::json st;
+    st["config"] = {{"adaptive", cfg.adaptive}, {"least_busy", cfg.least_busy},
+                    {"frag_min", cfg.placement == PlacementPolicy::kFragMin},
+                    {"speculation", cfg.speculation}, {"spec_fraction", cfg.spec_fraction},
+                    {"scale_queue_us", cfg.scale_queue_us}, {"expected_tokens", cfg.expected_tokens}};
+    const auto& sr = cm.surrogate_;
+    st["surrogate"] = {sr.attention_only, sr.ffn_only, sr.one_layer, sr.multi_layer,
+                       sr.allow_adapter_blocks};
+    for (const auto& [k, c] : cm.classes_)
+      st["classes"][k] = {{"prefill", grid_json(c.prefill)}, {"decode", grid_json(c.decode)},
+                          {"kv", c.kv_bytes_per_token}};
+    st["stitches"] = nlohmann::json::object();
+    for (const auto& [k, g] : cm.stitch_classes_) st["stitches"][k] = grid_json(g);
+    for (const auto& [k, s] : cm.device_classes_) st["device_classes"][k] = s;
+    std::set<std::string> comp_ids;
+    for (const auto& b : pz.block_ids()) {
+      const auto& bd = pz.block(b);
+      nlohmann::json cands = nlohmann::json::array();
+      auto cs = pz.candidate_instances(b);
+      for (std::size_t i = 1; i < cs.size(); ++i)
+        cands.push_back({cs[i].block_id,
+                         cs[i].stitch_id.empty() ? "" : pz.stitch(cs[i].stitch_id).cost_class,
+                         cs[i].score});
+      st["blocks"].push_back({{"id", b}, {"comps", bd.component_ids},
+                              {"dim_out", bd.embed_dim_out}, {"candidates", cands}});
+      for (const auto& c : bd.component_ids) comp_ids.insert(c);
+    }
+    for (const auto& cid : comp_ids) {
+      const auto& c = pz.component(cid);
+      nlohmann::json pieces = nlohmann::json::array();
+      for (const auto& p : c.contents) pieces.push_back({p.content_id, p.bytes});
+      st["components"].push_back({{"id", cid}, {"kind", (int)c.kind}, {"dim", c.embed_dim},
+                                  {"layer", c.layer}, {"pieces", pieces}});
+    }
+    for (const auto& mid : pz.model_ids()) st["chains"].push_back({mid, pz.model(mid).chain});
+    for (const auto& [id, s] : sim.cluster_.servers_) st["servers"].push_back({id, s.intra_bandwidth_bps});
+    st["inter_default"] = sim.cluster_.inter_default_;
+    st["inter"] = nlohmann::json::array();
+    for (const auto& [pr, b] : sim.cluster_.inter_) st["inter"].push_back({pr.first, pr.second, b});
+    for (const auto& [id, d] : sim.cluster_.devices_)
+      st["devices"].push_back({id, d.server, d.device_class, d.mem_capacity_bytes,
+                               d.mem_bandwidth_bps, d.load_bandwidth_bps});
+
+    nlohmann::json snaps = nlohmann::json::array();
+    Simulation* sp = &sim;
+    std::uint64_t n_events = 0;
+    sim.engine().set_trace_hook([&](SimTime now, std::uint64_t, EventKind) {
+      if (++n_events % (std::uint64_t)every != 0 || (int)snaps.size() >= max_snaps) return;
+      const Simulation& s = *sp;
+      nlohmann::json sn;
+      sn["now"] = now;
+      for (const auto& [id, in] : s.pool_.all())
+        sn["instances"].push_back({{"id", id}, {"block", in.block_id}, {"device", in.device},
+                                   {"ready", in.state == InstanceState::kReady},
+                                   {"ready_at", in.ready_at}, {"last_used", in.last_used},
+                                   {"created_seq", in.created_seq}, {"executing", in.executing},
+                                   {"queue_len", (int)in.queue.size()},
+                                   {"queued_cost", in.queued_cost_us},
+                                   {"queued_hwm", in.queued_cost_hwm}});
+      if (!sn.contains("instances")) sn["instances"] = nlohmann::json::array();
+      for (const auto& [dev, res] : s.pool_.residency_)
+        for (const auto& [cid, rc] : res)
+          if (rc.first > 0) sn["residency"].push_back({dev, cid, rc.first});
+      for (int dev : s.cluster_.device_ids()) {
+        using C = MemoryLedger::Category;
+        sn["ledger"].push_back({dev, s.ledger_.used(dev, C::kParams), s.ledger_.used(dev, C::kKv),
+                                s.ledger_.used(dev, C::kActivation)});
+        sn["lanes"].push_back({dev, s.pool_.lane(dev).busy_until});
+      }
+      sn["adjacency"] = nlohmann::json::array();
+      for (const auto& [pr, n] : s.sched_.adjacency_) sn["adjacency"].push_back({pr.first, pr.second, n});
+      sn["queries"] = nlohmann::json::array();
+      for (const auto& [rid, r] : s.live_) {
+        if (r.done || r.step < 0 || r.step >= (int)r.chain->size()) continue;
+        BindingQuery q;
+        q.request_id = rid;
+        q.chain_block = (*r.chain)[(std::size_t)r.step];
+        q.phase = r.phase;
+        q.tokens = r.phase == Phase::kPrefill ? r.req.prompt_tokens : 1;
+        q.context_tokens = r.context_tokens;
+        q.from_device = r.from_device;
+        q.now = now;
+        const int owner = s.kv_.device_of(rid, q.chain_block);
+        const int pages = owner >= 0 ? s.kv_.pages(rid, q.chain_block) : 0;
+        nlohmann::json qj = {{"request", rid}, {"block", q.chain_block},
+                             {"decode", q.phase == Phase::kDecode}, {"tokens", q.tokens},
+                             {"context", q.context_tokens}, {"from", q.from_device},
+                             {"kv_owner", owner}, {"kv_pages", pages}};
+        try {
+          qj["choice"] = choice_json(s.sched_.choose_binding(q));
+        } catch (const std::exception& e) {
+          qj["error"] = e.what();
+        }
+        sn["queries"].push_back(qj);
+      }
+      // synthetic steps for every block: a fresh prefill at chain entry and a decode hop from
+      // device 1 (no cache yet) - these reach the new-instance / eviction paths
+      std::uint64_t fresh = 1000000;
+      for (const auto& b : s.plan_.zoo.block_ids()) {
+        for (int k = 0; k < 2; ++k) {
+          BindingQuery q;
+          q.request_id = ++fresh;
+          q.chain_block = b;
+          q.phase = k ? Phase::kDecode : Phase::kPrefill;
+          q.tokens = k ? 1 : 96;
+          q.context_tokens = k ? 300 : 96;
+          q.from_device = k ? 1 : -1;
+          q.now = now;
+          nlohmann::json qj = {{"request", q.request_id}, {"block", b}, {"decode", k == 1},
+                               {"tokens", q.tokens}, {"context", q.context_tokens},
+                               {"from", q.from_device}, {"kv_owner", -1}, {"kv_pages", 0}};
+          try {
+            qj["choice"] = choice_json(s.sched_.choose_binding(q));
+          } catch (const std::exception& e) {
+            qj["error"] = e.what();
+          }
+          sn["queries"].push_back(qj);
+        }
+      }
+      sn["marks"] = s.sched_.speculation_marks();
+      sn["scale"] = nlohmann::json::array();
+      for (const auto& d : s.sched_.scale_decisions(now)) sn["scale"].push_back({d.instance_id, d.device});
+      sn["moves"] = nlohmann::json::array();
+      for (const auto& m : s.sched_.placement_moves()) sn["moves"].push_back({m.instance_id, m.dst_device});
+      for (const auto& b : s.plan_.zoo.block_ids()) {
+        for (int pref = 0; pref < 3; ++pref) {
+          sn["devices"].push_back({b, pref, std::vector<int>{},
+                                   s.sched_.choose_device(b, (DevicePreference)pref, {})});
+          sn["devices"].push_back({b, pref, std::vector<int>{0},
+                                   s.sched_.choose_device(b, (DevicePreference)pref, {0})});
+        }
+        for (int dev : s.cluster_.device_ids())
+          sn["need"].push_back({b, dev, s.pool_.param_bytes_needed(b, dev)});
+        const auto ids = s.cluster_.device_ids();
+        for (std::size_t a = 0; a < ids.size(); ++a)
+          for (std::size_t c = 0; c < ids.size(); ++c)
+            if (a != c) {
+              auto [rec, cp] = s.sched_.migration_rates(b, ids[a], ids[c]);
+              sn["rates"].push_back({b, ids[a], ids[c], rec, cp});
+            }
+      }
+      snaps.push_back(std::move(sn));
+    });
+    auto rep = sim.run();
+    nlohmann::json out = {{"static", st}, {"snapshots", snaps}, {"events", n_events},
+                          {"completed", rep.value("completed", nlohmann::json())}};
+    h->out = out.dump();
+  } catch (const std::exception& e) {
+    h->err = e.what();
+  }
+  return h;
+}
+const char* rs_policy_trace_json(const rs_policy_trace* h) { return h->out.c_str(); }
+const char* rs_policy_trace_error(const rs_policy_trace* h) { return h->err.c_str(); }
+void rs_policy_trace_free(rs_policy_trace* h) { delete h; }
 
 }  // extern "C"

@@ -139,3 +139,28 @@ def profile_component_us(path: str, cls: str, prefill: bool, batch: float, token
           512) != 0:
         raise ValueError(err.value.decode())
     return out.value
+
+
+def policy_trace(spec: dict) -> dict:
+    """Runs the reference Simulation described by `spec` (see rs_policy_trace_run in
+    oracle/ref_shim.cpp) and returns its static description plus the Scheduler's decisions at
+    snapshots taken while it runs."""
+    import json
+    L = lib()
+    if not getattr(L, "_policy_bound", False):
+        L.rs_policy_trace_run.restype = C.c_void_p
+        L.rs_policy_trace_run.argtypes = [C.c_char_p]
+        for n in ("rs_policy_trace_json", "rs_policy_trace_error"):
+            getattr(L, n).restype = C.c_char_p
+            getattr(L, n).argtypes = [C.c_void_p]
+        L.rs_policy_trace_free.restype = None
+        L.rs_policy_trace_free.argtypes = [C.c_void_p]
+        L._policy_bound = True
+    h = L.rs_policy_trace_run(json.dumps(spec).encode())
+    try:
+        err = L.rs_policy_trace_error(h).decode()
+        if err:
+            raise RuntimeError(err)
+        return json.loads(L.rs_policy_trace_json(h).decode())
+    finally:
+        L.rs_policy_trace_free(h)

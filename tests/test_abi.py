@@ -13,7 +13,7 @@ LIB = os.path.join(ROOT, "paper_2404_18322_b200", "libblockexec.so")
 
 def declared_functions():
     names = set()
-    for h in ("blockexec.h", "blockhost.h"):
+    for h in ("blockexec.h", "blockhost.h", "blockpolicy.h"):
         text = open(os.path.join(ROOT, "include", h)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         for m in re.finditer(r"\b((?:be|bh)_[a-z0-9_]+)\s*\(", text):
@@ -25,7 +25,8 @@ def test_header_declares_the_abi():
     names = declared_functions()
     assert {"be_exec_batch", "be_exec_batch_dev", "be_cosine", "be_gather_rows",
             "be_scatter_rows", "bh_pool_pop_batch", "bh_kv_append_tokens",
-            "bh_runner_decode_step"} <= names
+            "bh_runner_decode_step", "bh_policy_choose_binding", "bh_policy_speculation_marks",
+            "bh_policy_choose_device", "bh_policy_placement_moves"} <= names
     assert len(names) > 50
 
 
