@@ -489,6 +489,9 @@ def run_ours(args, world, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peaks_kind = load_peaks()
     wl = make_workload(args)
+    if world > 1:
+        wl, routing = routed_share(wl, world, rank)
+        placement += f"; {routing}"
     ctx = Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream.value)
     # plan_ahead: the host bookkeeping of step k+1 runs while step k is on the GPU (it matters
@@ -635,6 +638,22 @@ def run_ours(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def routed_share(wl, world, rank):
+    """Replica placement: the global stream is `world` copies of the config's requests; each
+    request binds to a replica through bh_policy_choose_binding (the reference's estimate rule,
+    priced by the measured B200 profiles) and stays there for decode (KV owner). Returns this
+    rank's share as a workload, plus a note for the JSON line."""
+    import dataclasses
+    from paper_2404_18322_b200.pipeline import route_requests
+    dev = route_requests(wl, world, copies=world)
+    mine = [g // world for g, d in enumerate(dev) if d == rank]
+    share = dataclasses.replace(wl, req_tenant=[wl.req_tenant[i] for i in mine],
+                                req_prompt=[wl.req_prompt[i] for i in mine],
+                                req_output=[wl.req_output[i] for i in mine])
+    counts = [dev.count(r) for r in range(world)]
+    return share, f"requests routed by bh_policy choose_binding: {counts} per replica"
 
 
 def run_reference(args, world, rank, local):

@@ -99,6 +99,94 @@ def choose_layout(wl: Workload, world: int, hbm_bytes: float = 0.85 * 180e9) -> 
     return best
 
 
+def _profile_classes(path: str | None):
+    import json
+    import os
+    if path is None:
+        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "profiles", "b200_profiles.json")
+    if not os.path.exists(path):
+        return {}
+    return json.load(open(path))["classes"]
+
+
+def routing_policy(wl: Workload, n_devices: int, profiles: str | None = None,
+                   hbm_bytes: int = 180 * 10**9):
+    """A bh_policy (include/blockpolicy.h) describing replica placement of `wl`: every block on
+    each of n_devices GPUs of one NVLink server, priced by the measured B200 cost profiles
+    (profiles/b200_profiles.json, scripts/make_profiles.py; §8(f) rank 2). Classes the profile
+    file lacks are priced by streamed bytes at the measured copy peak."""
+    from .policy import Policy
+    s = wl.shape
+    d = s.d_model
+    prof = _profile_classes(profiles)
+    pol = Policy(adaptive=False, speculation=False)
+    att_bytes, ffn_bytes = 2 * 4 * d * d, 2 * 3 * d * s.d_ff
+    for kind, wbytes, kv in (("attention", att_bytes, 4 * d), ("ffn", ffn_bytes, 0)):
+        key = f"{kind}:{d}"
+        if key in prof:
+            c = prof[key]
+            grids = [{"xs": c[p]["batch"], "ys": c[p]["tokens"], "v": c[p]["us"]}
+                     for p in ("prefill", "decode")]
+            kv = c.get("kv_bytes_per_token", kv)
+        else:  # bytes model: weights once + K/V of batch x tokens, at 6.37 TB/s
+            xs, ys = [1, 8, 64], [1, 256, 4096]
+            us = [[(wbytes + b * t * kv) / 6.37e12 * 1e6 for t in ys] for b in xs]
+            grids = [{"xs": xs, "ys": ys, "v": us}] * 2
+        pol.add_cost_class(key, grids[0], grids[1], kv)
+    pol.set_device_class("b200", 1.0)
+    for bi, name in enumerate(wl.block_names):
+        comps = []
+        for ci, k in enumerate(wl.block_comps[bi] if wl.block_comps else s.comps):
+            cid = f"{name}.c{ci}"
+            pol.add_component(cid, "attention" if k == "a" else "ffn", d, ci // 2,
+                              [(cid + ".w", att_bytes if k == "a" else ffn_bytes)])
+            comps.append(cid)
+        pol.add_block(name, comps, d)
+    for t, ch in enumerate(wl.chains):
+        pol.add_chain(f"tenant{t}", [wl.block_names[b] for b in ch])
+    pol.add_server(0, 900e9)  # NVLink 5 per direction
+    for dev in range(n_devices):
+        pol.add_device(dev, 0, "b200", hbm_bytes, 7.7e12, 55e9)
+    seq = 0
+    for dev in range(n_devices):
+        for name in wl.block_names:
+            seq += 1
+            pol.put_instance(f"r{dev}.{name}", name, dev, ready=True, created_seq=seq)
+        pol.set_ledger(dev, s.param_bytes * len(wl.block_names))
+    return pol
+
+
+def route_requests(wl: Workload, n_devices: int, copies: int = 1,
+                   profiles: str | None = None) -> list[int]:
+    """Routes `copies` x the workload's requests (request i of copy c is global request
+    i * copies + c) over n_devices replicas with the reference's binding rule
+    (bh_policy_choose_binding = Scheduler::choose_binding, scheduler.cpp:80-160): each prefill
+    binds to the lowest (queue + compute + transfer + load) estimate, ties to the lower device;
+    the chosen instance's queue grows by the step's standalone cost (InstancePool::enqueue,
+    agent.cpp:132-137). Decode steps then stick to the device holding the request's KV, so the
+    prefill choice is the request's replica. Returns the device per global request."""
+    pol = routing_policy(wl, n_devices, profiles)
+    queued = {}
+    out = []
+    for i in range(wl.n_requests):
+        blk = wl.block_names[wl.chains[wl.req_tenant[i]][0]]
+        for c in range(copies):
+            ch = pol.choose_binding(i * copies + c, blk, False, wl.req_prompt[i],
+                                    wl.req_prompt[i], -1, 0)
+            if ch is None:
+                raise ValueError(f"no feasible replica for block {blk}")
+            iid = ch["instance"]
+            queued[iid] = queued.get(iid, 0.0) + ch["est"][1]
+            pol.put_instance(iid, blk, ch["device"], ready=True,
+                             created_seq=1 + ch["device"] * len(wl.block_names)
+                             + wl.block_names.index(blk),
+                             queue_len=1, queued_cost_us=queued[iid],
+                             queued_cost_hwm=queued[iid])
+            out.append(ch["device"])
+    return out
+
+
 def stage_workload(wl: Workload, rng: tuple[int, int], n_micro: int) -> Workload:
     """The blocks of chain positions [a, b) and n_micro copies of the request mix."""
     a, b = rng

@@ -139,3 +139,41 @@ def test_policy_errors_mirror_reference():
     with pytest.raises(ValueError):
         pol.add_cost_class("attention:8", {"xs": [2, 1], "ys": [1], "v": [[1], [2]]},
                            {"xs": [1], "ys": [1], "v": [[1]]})
+
+
+def test_replica_routing_balances_copies():
+    """bench.py's replica placement: world copies of a config's requests routed by
+    choose_binding land one copy per replica (equal queued cost after every group of identical
+    requests; ties to the lower device), so each GPU serves the config's own mix."""
+    from paper_2404_18322_b200.pipeline import route_requests
+    from paper_2404_18322_b200.workloads import CONFIGS
+    for cfg, n in (("c2", 4), ("c3", 2), ("c1", 8)):
+        wl = CONFIGS[cfg]()
+        dev = route_requests(wl, n, copies=n)
+        assert len(dev) == n * wl.n_requests
+        for i in range(wl.n_requests):
+            assert sorted(dev[i * n:(i + 1) * n]) == list(range(n))
+
+
+def test_routing_prices_with_measured_profiles():
+    """The router's compute estimate for a 7B block is the measured B200 profile (profiles/
+    b200_profiles.json) summed over the block's components, read through the reference's own
+    bilinear rule (bit-exact vs the reference's CostModel in test_control_plane)."""
+    import json
+    import os
+    from paper_2404_18322_b200.pipeline import routing_policy
+    from paper_2404_18322_b200.workloads import CONFIGS
+    wl = CONFIGS["c2"]()
+    pol = routing_policy(wl, 2)
+    blk = wl.block_names[0]
+    ch = pol.choose_binding(1, blk, False, 512, 512)
+    prof = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "profiles",
+                                       "b200_profiles.json")))["classes"]
+
+    def lookup(c, b, t):
+        g = prof[c]["prefill"]
+        return g["us"][g["batch"].index(b)][g["tokens"].index(t)]
+    n_layers = wl.shape.n_layers
+    want = n_layers * (lookup("attention:4096", 1, 512) + lookup("ffn:4096", 1, 512))
+    assert abs(ch["est"][1] - want) <= 1e-9 * want
+    assert ch["device"] == 0 and ch["est"][0] == 0.0
