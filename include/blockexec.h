@@ -203,6 +203,19 @@ int be_timeline_read(be_ctx* ctx, be_timeline_rec* out, int cap, int* n_out);
 int be_kv_copy_pages(be_ctx* dst_ctx, const be_kv_pool* src_pool, be_kv_pool* dst_pool,
                      const int32_t* src_slots, const int32_t* dst_slots, int n, void* stream);
 
+/* KV migration with overlapped recompute / copy (the plan is
+ * plan_migration, kv.cpp:16-58, bh_plan_migration; the move is start_kv_migration,
+ * scenario.cpp:361-431). A segment's n_pages pages (src_slots -> dst_slots, token order, from
+ * bh_kv_move_segment_slots) move to dst_pool: the first n_recompute pages are rebuilt on the
+ * destination by a chunked prefill of `blk` over the head tokens' block-input rows
+ * (d_head_rows, head_tokens rows, (n_recompute-1)*16 < head_tokens <= n_recompute*16), while the
+ * other pages are copied from src_pool (peer GPU over NVLink, or the same GPU) on a side stream;
+ * the call's stream waits for both. `blk`, dst_pool and ws belong to ctx. Async. */
+int be_kv_migrate(be_ctx* ctx, be_block* blk, const be_kv_pool* src_pool, be_kv_pool* dst_pool,
+                  be_workspace* ws, const int32_t* src_slots, const int32_t* dst_slots,
+                  int n_pages, int n_recompute, int head_tokens, const void* d_head_rows,
+                  void* stream);
+
 /* K1 / K2 standalone: routing-table gather and scatter of bf16 rows. */
 int be_gather_rows(be_ctx* ctx, const void* d_arena, const int32_t* d_src, int rows, int d,
                    void* d_out, void* stream);

@@ -741,6 +741,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
              const int32_t* d_pt, const void* arena_in, void* arena_out, cudaStream_t st) {
   be_block* blk = blks[0];
   be_kv_pool* pool = pools[0];
+  cudaSetDevice(ctx->device);  // several contexts (GPUs) may share one host thread
   const auto& D = blk->desc;
   const int d = D.d_model, F = D.d_ff, H = D.n_heads, hd = D.head_dim;
   // a workspace serves any block of its d_model / heads with d_ff <= its own (pruned surrogates)
@@ -994,6 +995,7 @@ extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_wo
   for (int64_t i = 0; i < (int64_t)n_pt_rows * pt_stride; ++i)
     if (page_table[i] < -1 || page_table[i] >= pool->n_pages)
       return fail(ctx, BE_ERR_INVALID, "page table entry %lld out of range", (long long)i);
+  cudaSetDevice(ctx->device);
   cudaStream_t st = pick_stream(ctx, stream);
   if (n_tokens > 0)
     BE_CUDA(ctx, cudaMemcpyAsync(ws->d_tokens, tokens, n_tokens * sizeof(be_token),
@@ -1127,6 +1129,56 @@ extern "C" int be_kv_copy_pages(be_ctx* dst_ctx, const be_kv_pool* src_pool, be_
       BE_CUDA(dst_ctx, cudaMemcpyPeerAsync(d, dst_dev, s, src_dev, bytes, st));
     }
     i = j;
+  }
+  return BE_OK;
+}
+
+extern "C" int be_kv_migrate(be_ctx* ctx, be_block* blk, const be_kv_pool* src_pool,
+                             be_kv_pool* dst_pool, be_workspace* ws, const int32_t* src_slots,
+                             const int32_t* dst_slots, int n_pages, int n_recompute,
+                             int head_tokens, const void* d_head_rows, void* stream) {
+  if (ctx == nullptr || blk == nullptr || src_pool == nullptr || dst_pool == nullptr ||
+      ws == nullptr || n_pages < 0 || n_recompute < 0 || n_recompute > n_pages ||
+      (n_pages > 0 && (src_slots == nullptr || dst_slots == nullptr)))
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_kv_migrate: bad arguments") : BE_ERR_INVALID;
+  if (n_recompute > 0 && (d_head_rows == nullptr || head_tokens <= (n_recompute - 1) * 16 ||
+                          head_tokens > n_recompute * 16))
+    return fail(ctx, BE_ERR_INVALID,
+                "be_kv_migrate: %d recompute pages need %d..%d head tokens (got %d)",
+                n_recompute, (n_recompute - 1) * 16 + 1, n_recompute * 16, head_tokens);
+  if (dst_pool->ctx != ctx || blk->ctx != ctx)
+    return fail(ctx, BE_ERR_INVALID, "be_kv_migrate: block and destination pool must be on ctx");
+  cudaSetDevice(ctx->device);
+  if (ctx->side == nullptr) {
+    BE_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    BE_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    BE_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  cudaStream_t st = pick_stream(ctx, stream);
+  const int n_copy = n_pages - n_recompute;
+  int rc;
+  // tail pages: copy engine (peer copy over NVLink when the pools are on different GPUs), on the
+  // side stream so it overlaps the recompute
+  if (n_copy > 0) {
+    BE_CUDA(ctx, cudaEventRecord(ctx->ev_fork, st));
+    BE_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    if ((rc = be_kv_copy_pages(ctx, src_pool, dst_pool, src_slots + n_recompute,
+                               dst_slots + n_recompute, n_copy, ctx->side)) != BE_OK)
+      return rc;
+  }
+  // head pages: chunked prefill of the head tokens through the block on the destination, K/V
+  // appended straight into the destination pages (outputs discarded: dst_row -1)
+  if (n_recompute > 0) {
+    std::vector<be_token> toks(head_tokens);
+    for (int t = 0; t < head_tokens; ++t)
+      toks[t] = be_token{t, -1, dst_slots[t >> 4] * 16 + (t & 15), t, 0};
+    if ((rc = be_exec_batch(ctx, blk, dst_pool, ws, BE_PHASE_PREFILL, head_tokens, toks.data(),
+                            1, n_recompute, dst_slots, d_head_rows, nullptr, st)) != BE_OK)
+      return rc;
+  }
+  if (n_copy > 0) {
+    BE_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+    BE_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ev_join, 0));
   }
   return BE_OK;
 }

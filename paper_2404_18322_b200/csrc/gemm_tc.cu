@@ -531,11 +531,13 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
                        2 * BN * 4 /*rstd*/;
   auto kern = gemm_sk_kernel<BN, STAGES, CTAS, MODE>;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;  // per device: the attribute is device state
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> dev & 1ull)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured |= 1ull << dev;
   }
   const int m_tiles = L.N / kBM;
   const int n_tiles = (L.epi.ntok + BN - 1) / BN;

@@ -277,6 +277,23 @@ def kv_copy_pages(ctx: Context, src_pool: "KvPool", dst_pool: "KvPool", src_slot
                                  stream if stream is not None else C.c_void_p(0)), ctx.h)
 
 
+def kv_migrate(ctx: Context, blk: "Block", src_pool: "KvPool", dst_pool: "KvPool",
+               ws: "Workspace", src_slots, dst_slots, n_recompute: int = 0, head_rows=None,
+               head_tokens: int | None = None, stream=None) -> None:
+    """KV migration with overlapped recompute / copy (be_kv_migrate): the first n_recompute
+    pages are rebuilt on the destination by a chunked prefill of `blk` over `head_rows` (the
+    head tokens' block-input rows, bf16 [head_tokens][d] on ctx's GPU); the rest are copied
+    from src_pool on a side stream. n_recompute comes from plan_migration (policy.py)."""
+    s = np.ascontiguousarray(src_slots, np.int32)
+    d = np.ascontiguousarray(dst_slots, np.int32)
+    if head_tokens is None:
+        head_tokens = head_rows.shape[0] if head_rows is not None else 0
+    check(lib().be_kv_migrate(ctx.h, blk.h, src_pool.h, dst_pool.h, ws.h,
+                              s.ctypes.data_as(C.c_void_p), d.ctypes.data_as(C.c_void_p),
+                              len(s), n_recompute, head_tokens, _ptr(head_rows),
+                              stream if stream is not None else C.c_void_p(0)), ctx.h)
+
+
 def pack_weight(ctx: Context, w):
     """Row-major [N][K] bf16 -> packed GEMM tile layout (csrc/ptx.cuh packed_index)."""
     out = w.new_empty(w.shape)
