@@ -617,7 +617,7 @@ def run_ours(args, world, rank, local):
             "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, "
             "synthetic prompt embeddings; greedy feedback of the last hidden state)",
-            "config": {"workload": wl.name, "model": "Llama-2-7B-shaped" if args.config in ("c2", "c3")
+            "config": {"workload": wl.name, "model": "Llama-2-7B-shaped" if args.config in ("c2", "c3", "c5")
                        else wl.name, "tenants": len(wl.chains), "global_batch": n_live * world,
                        "prompt": wl.req_prompt[0], "decode": wl.req_output[0],
                        "blocks": f"{len(wl.block_names)} blocks x {wl.shape.n_layers} layers",
@@ -690,7 +690,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--prompt", type=int, default=None, help="default: the config's own")
     ap.add_argument("--output", type=int, default=None, help="default: the config's own")
     ap.add_argument("--no-e2e", action="store_true")

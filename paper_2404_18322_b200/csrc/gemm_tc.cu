@@ -579,10 +579,16 @@ cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream) {
 }
 
 int gemm_pick_bn(int ntok) {
+  // BE_GEMM_BN256_MIN: smallest batch that takes 256-token tiles (4-stage ring) instead of
+  // 128-token ones (6 stages); experiments only
+  static const int kBn256Min = [] {
+    const char* e = getenv("BE_GEMM_BN256_MIN");
+    return e ? atoi(e) : 129;
+  }();
   if (ntok <= 16) return 16;
   if (ntok <= 32) return 32;
   if (ntok <= 64) return 64;
-  if (ntok <= 128) return 128;
+  if (ntok <= 128 || ntok < kBn256Min) return 128;
   return 256;
 }
 

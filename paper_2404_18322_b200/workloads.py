@@ -93,4 +93,15 @@ def c4_llama13b(prompt: int = 512, output: int = 128) -> Workload:
     return shared_prefix_zoo("c4-llama13b-4tenant", shape, npos, 8, 4, 16, prompt, output)
 
 
-CONFIGS = {"c1": c1_tiny, "c2": c2_llama7b, "c3": c3_llama7b_16tenant, "c4": c4_llama13b}
+def c5_llama7b_8tenant(prompt: int = 512, output: int = 128) -> Workload:
+    """configs[4]: the speculative-execution case - batch 256 over 8 tenants (32 requests each),
+    7B shape, blocks 0-5 shared, 6-7 private. Its cosine equivalence check at batch 256 is
+    tests/test_gpu_speculation.py::test_speculative_stage_at_c5_scale; the decode step of the
+    workload runs like the others (bench.py --config c5); 8 B200 = one replica per GPU."""
+    shape, npos = llama_blocks(32, 4, 4096, 32, 11008, prompt + output + 16)
+    return shared_prefix_zoo("c5-llama7b-8tenant", shape, npos, 6, 8, 32, prompt, output,
+                             max_batch_tokens=8192)
+
+
+CONFIGS = {"c1": c1_tiny, "c2": c2_llama7b, "c3": c3_llama7b_16tenant, "c4": c4_llama13b,
+           "c5": c5_llama7b_8tenant}

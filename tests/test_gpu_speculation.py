@@ -100,3 +100,72 @@ def test_speculative_step_matches_oracle(ctx, threshold):
         gpu[k].free()
     ws_main.free()
     ws_side.free()
+
+
+def test_speculative_stage_at_c5_scale(ctx):
+    """configs[4] (C5): the cosine equivalence check at batch 256 over 8 tenants on 7B-shaped
+    4-layer blocks (verify = a shared block, draft = its 50%-FFN surrogate, next = the following
+    shared block). Size-independent properties instead of the CPU oracle:
+      * the verify lane's rows equal a plain be_exec_batch of the block bit for bit;
+      * K7's cosine equals an fp32 torch cosine of the draft/true rows; accept = cos >= thr;
+      * the next block's rows equal next(draft) for accepted rows and next(true) for rejected
+        ones (a plain run on the selected inputs; other batch composition, so within bf16
+        rounding)."""
+    from paper_2404_18322_b200.workloads import c5_llama7b_8tenant
+    wl = c5_llama7b_8tenant()
+    shape = dev.BlockShape(n_layers=4, d_model=4096, n_heads=32, d_ff=11008, max_pos=128)
+    n, prompt, d = len(wl.req_tenant), 64, shape.d_model
+    assert n == 256 and len(wl.chains) == 8
+    pages = (prompt + 1 + 15) // 16
+    pt = np.arange(n * pages, dtype=np.int32).reshape(n, pages)
+    names = {"verify": ("b3", shape), "draft": ("b3", shape.surrogate(0.5)),
+             "next": ("b4", shape)}
+    gpu, pools = {}, {}
+    for k, (nm, sh) in names.items():
+        gpu[k] = dev.Block(ctx, sh, nm, seed=9)
+        pools[k] = dev.KvPool(ctx, gpu[k], n * pages)
+    ws_main = dev.Workspace(ctx, shape, max_tokens=8192, max_rows=n, max_pages=pages)
+    ws_side = dev.Workspace(ctx, shape, max_tokens=n, max_rows=n, max_pages=pages)
+    g = torch.Generator().manual_seed(5)
+    for k in names:  # prompt KV for every lane, in 32-request prefill batches
+        for r0 in range(0, n, 32):
+            xp = torch.randn(32 * prompt, d, generator=g).to(torch.bfloat16).cuda()
+            toks = [(i * prompt + p, i * prompt + p, int(pt[r0 + i, p // 16]) * 16 + p % 16, p,
+                     r0 + i) for i in range(32) for p in range(prompt)]
+            dev.exec_batch(ctx, gpu[k], pools[k], ws_main, dev.PHASE_PREFILL, toks, pt, xp,
+                           torch.empty_like(xp))
+    ctx.sync()
+    x = torch.randn(n, d, generator=g).to(torch.bfloat16).cuda()
+    dtoks = [(r, r, int(pt[r, prompt // 16]) * 16 + prompt % 16, prompt, r) for r in range(n)]
+    st = {k: (gpu[k], pools[k], ws_main if k == "verify" else ws_side, dtoks, pt) for k in names}
+    y_draft, y_true, z = (torch.zeros(n, d, dtype=torch.bfloat16, device="cuda")
+                          for _ in range(3))
+    cos0, _, _ = dev.exec_speculative(ctx, st["verify"], st["draft"], st["next"], x, y_draft,
+                                      y_true, z, 0.95)
+    thr = float(np.median(cos0))  # a threshold that splits the batch
+    cos, acc, n_acc = dev.exec_speculative(ctx, st["verify"], st["draft"], st["next"], x,
+                                           y_draft, y_true, z, thr)
+    assert 0 < n_acc < n
+    yd, yt = y_draft.float(), y_true.float()
+    cos_t = (yd * yt).sum(1) / (yd.norm(dim=1) * yt.norm(dim=1))
+    np.testing.assert_allclose(cos, cos_t.cpu().numpy(), atol=1e-5)
+    assert np.array_equal(acc, (cos >= thr).astype(np.int32)) and n_acc == int(acc.sum())
+    y_plain = torch.empty_like(x)
+    dev.exec_batch(ctx, gpu["verify"], pools["verify"], ws_main, dev.PHASE_DECODE, dtoks, pt, x,
+                   y_plain)
+    ctx.sync()
+    assert torch.equal(y_plain, y_true)
+    a = torch.from_numpy(acc).cuda().bool()[:, None]
+    z_in = torch.where(a, y_draft, y_true)
+    z_plain = torch.empty_like(x)
+    dev.exec_batch(ctx, gpu["next"], pools["next"], ws_main, dev.PHASE_DECODE, dtoks, pt, z_in,
+                   z_plain)
+    ctx.sync()
+    assert rel_l2(f32(z), f32(z_plain)) <= 1e-2
+    zc = torch.nn.functional.cosine_similarity(z.float(), z_plain.float(), dim=1)
+    assert float(zc.min()) >= 0.999
+    for k in names:
+        pools[k].free()
+        gpu[k].free()
+    ws_main.free()
+    ws_side.free()
