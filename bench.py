@@ -617,8 +617,9 @@ def run_ours(args, world, rank, local):
             "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, "
             "synthetic prompt embeddings; greedy feedback of the last hidden state)",
-            "config": {"workload": wl.name, "model": "Llama-2-7B-shaped" if args.config in ("c2", "c3", "c5")
-                       else wl.name, "tenants": len(wl.chains), "global_batch": n_live * world,
+            "config": {"workload": wl.name, "model": {"c2": "Llama-2-7B-shaped", "c3": "Llama-2-7B-shaped",
+                                 "c4": "Llama-2-13B-shaped",
+                                 "c5": "Llama-2-7B-shaped"}.get(args.config, wl.name), "tenants": len(wl.chains), "global_batch": n_live * world,
                        "prompt": wl.req_prompt[0], "decode": wl.req_output[0],
                        "blocks": f"{len(wl.block_names)} blocks x {wl.shape.n_layers} layers",
                        "rows_per_block": wl.rows_at_block(), "batches_per_step": nb,
