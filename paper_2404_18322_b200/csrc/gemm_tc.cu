@@ -283,38 +283,49 @@ __global__ void __launch_bounds__(192, CTAS)
       // ---------------- producer: packed weight tiles by bulk copy, activations by TMA
       const long long n_it = it_end - it_begin;
       const int pre = (int)(n_it < STAGES ? n_it : STAGES);
-      auto wtile = [&](long long it) {
-        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
-        const __nv_bfloat16* wb = E.n_grp > 1 ? E.wgrp[tile / m_tiles] : wpk;  // grouped batch
-        return wb + ((size_t)(tile % m_tiles) * nkb + kb) * (kBM * kBK);
+      // (tile, k-block) cursors advanced incrementally: no 64-bit division per load
+      struct Cur {
+        int tile, kb, m, n;
       };
-      constexpr bool load_b = true;
+      const int tile0 = (int)(it_begin / nkb);
+      Cur cw{tile0, (int)(it_begin - (long long)tile0 * nkb), tile0 % m_tiles, tile0 / m_tiles};
+      Cur cb = cw;
+      auto step = [&](Cur& c) {
+        if (++c.kb == nkb) {
+          c.kb = 0;
+          ++c.tile;
+          if (++c.m == m_tiles) {
+            c.m = 0;
+            ++c.n;
+          }
+        }
+      };
+      auto wtile = [&](const Cur& c) {
+        const __nv_bfloat16* wb = E.n_grp > 1 ? E.wgrp[c.n] : wpk;  // grouped batch
+        return wb + ((size_t)c.m * nkb + c.kb) * (kBM * kBK);
+      };
       constexpr uint32_t stage_bytes = S::kStageBytes;
       // weights first: nothing upstream writes them, so they stream under the previous kernel
-      for (int i = 0; i < pre; ++i) {
+      for (int i = 0; i < pre; ++i, step(cw)) {
         mbar_arrive_expect_tx(&full[i], stage_bytes);
-        bulk_load(sA + i * S::kABytes, wtile(it_begin + i), S::kABytes, &full[i], kEvictFirst);
+        bulk_load(sA + i * S::kABytes, wtile(cw), S::kABytes, &full[i], kEvictFirst);
       }
       pdl_wait();  // activations are produced by the previous kernel
       stamp(E, 2);
       tl_go(E.tl, E.tl_cap);
-      for (int i = 0; i < pre && load_b; ++i) {
-        const long long it = it_begin + i;
-        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
-        tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
-                    kEvictLast);
-      }
-      for (long long i = pre; i < n_it; ++i) {
-        const int s = (int)(i % STAGES);
-        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+      for (int i = 0; i < pre; ++i, step(cb))
+        tma_load_2d(&map_x, &full[i], sB + i * S::kBBytes, cb.kb * kBK, cb.n * BN, kEvictLast);
+      int s = pre % STAGES;
+      uint32_t ph = (uint32_t)(pre / STAGES) & 1u;
+      for (long long i = pre; i < n_it; ++i, step(cw)) {
         mbar_wait(&empty[s], ph ^ 1u);
-        const long long it = it_begin + i;
-        const int tile = (int)(it / nkb), kb = (int)(it % nkb);
         mbar_arrive_expect_tx(&full[s], stage_bytes);
-        bulk_load(sA + s * S::kABytes, wtile(it), S::kABytes, &full[s], kEvictFirst);
-        if (load_b)
-          tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, kb * kBK, (tile / m_tiles) * BN,
-                      kEvictLast);
+        bulk_load(sA + s * S::kABytes, wtile(cw), S::kABytes, &full[s], kEvictFirst);
+        tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, cw.kb * kBK, cw.n * BN, kEvictLast);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
       stamp(E, 3);
     }
