@@ -333,10 +333,11 @@ __global__ void __launch_bounds__(192, CTAS)
   } else if (warp == 1) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc_bf16(kBM, BN);
-    long long i = 0;  // ring position
+    int s = 0;  // ring slot and its phase, advanced incrementally
+    uint32_t ph = 0;
     int seg = 0;
+    int kb0 = (int)(it_begin % nkb);
     for (long long it = it_begin; it < it_end; ++seg) {
-      const int kb0 = (int)(it % nkb);
       const long long left = it_end - it;
       const int kb1 = (int)((nkb - kb0) < left ? nkb : kb0 + left);
       const int a = seg & 1;
@@ -344,9 +345,8 @@ __global__ void __launch_bounds__(192, CTAS)
       mbar_wait(&tempty[a], (u & 1u) ^ 1u);
       tc_fence_after();
       const uint32_t tacc = tmem_base + (uint32_t)(a * BN);
-      for (int kb = kb0; kb < kb1; ++kb, ++i) {
-        const int s = (int)(i % STAGES);
-        mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(sA + s * S::kABytes);
@@ -360,8 +360,13 @@ __global__ void __launch_bounds__(192, CTAS)
           if (kb == kb1 - 1) umma_commit(&tfull[a]);
         }
         __syncwarp();
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
       it += kb1 - kb0;
+      kb0 = 0;  // later segments start at a tile's first k-block
     }
   } else {
     // ---------------- epilogue warps 2..5

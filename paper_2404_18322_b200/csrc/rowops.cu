@@ -24,17 +24,18 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ arena,
     tl_start(tl, tl_cap);
     tl_go(tl, tl_cap);
   }
-  const int vec_per_row = d / 8;
-  const long long total = (long long)rows * vec_per_row;
-  const long long stride = (long long)gridDim.x * blockDim.x;
+  // 32-bit index math (rows * d / 8 < 2^31, checked by the launcher): no 64-bit division
+  const unsigned vec_per_row = (unsigned)d / 8u;
+  const unsigned total = (unsigned)rows * vec_per_row;
+  const unsigned stride = gridDim.x * blockDim.x;
   // every thread runs the same trip count so the group shuffles below see full warps
-  const long long trips = (total + stride - 1) / stride;
-  const long long v0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  for (long long k = 0; k < trips; ++k) {
-    const long long v = v0 + k * stride;
+  const unsigned trips = (total + stride - 1) / stride;
+  const unsigned v0 = blockIdx.x * blockDim.x + threadIdx.x;
+  for (unsigned k = 0; k < trips; ++k) {
+    const unsigned v = v0 + k * stride;
     const bool live = v < total;
     const int r = live ? (int)(v / vec_per_row) : 0;
-    const int c = live ? (int)(v - (long long)r * vec_per_row) : 0;
+    const int c = live ? (int)(v - (unsigned)r * vec_per_row) : 0;
     float sq = 0.f;
     if (live) {
       const uint4 val = __ldg(reinterpret_cast<const uint4*>(arena + (size_t)src[(size_t)r * src_stride] * d) + c);
@@ -71,12 +72,11 @@ __global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ xb,
     tl_start(tl, tl_cap);
     tl_go(tl, tl_cap);
   }
-  const int vec_per_row = d / 8;
-  const long long total = (long long)rows * vec_per_row;
-  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < total;
-       v += (long long)gridDim.x * blockDim.x) {
+  const unsigned vec_per_row = (unsigned)d / 8u;
+  const unsigned total = (unsigned)rows * vec_per_row;
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < total; v += gridDim.x * blockDim.x) {
     const int r = (int)(v / vec_per_row);
-    const int c = (int)(v - (long long)r * vec_per_row);
+    const int c = (int)(v - (unsigned)r * vec_per_row);
     const int drow = dst[(size_t)r * dst_stride];
     if (drow < 0) continue;  // token output not needed downstream
     const uint4 val = reinterpret_cast<const uint4*>(xb + (size_t)r * d)[c];
@@ -213,6 +213,7 @@ cudaError_t launch_gather(const __nv_bfloat16* arena, const int* src, int src_st
                           int d, __nv_bfloat16* xb, float* x, float* ss, cudaStream_t st,
                           unsigned long long* tl, int tl_cap) {
   if (rows <= 0) return cudaSuccess;
+  if ((long long)rows * d / 8 >= (1ll << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   gather_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(
       arena, src, src_stride, rows, d, xb, x, ss, tl, tl_cap);
   return cudaGetLastError();
@@ -221,6 +222,7 @@ cudaError_t launch_scatter(const __nv_bfloat16* xb, const int* dst, int dst_stri
                            int d, __nv_bfloat16* arena, cudaStream_t st, unsigned long long* tl,
                            int tl_cap) {
   if (rows <= 0) return cudaSuccess;
+  if ((long long)rows * d / 8 >= (1ll << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   scatter_rows_kernel<<<grid_for((long long)rows * d / 8, 256, 148 * 16), 256, 0, st>>>(
       xb, dst, dst_stride, rows, d, arena, tl, tl_cap);
   return cudaGetLastError();
