@@ -221,10 +221,17 @@ __device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, flo
 struct SkRange {
   long long total;  // iterations = tiles * nkb
   int G;            // CTAs
-  __device__ __forceinline__ long long begin(int c) const { return (long long)c * total / G; }
+  // 32-bit arithmetic when total * G fits (every shape here): a 64-bit division is a long
+  // emulated sequence on the epilogue's critical path
+  __device__ __forceinline__ bool narrow() const { return total * G < (1ll << 32); }
+  __device__ __forceinline__ long long begin(int c) const {
+    return narrow() ? (long long)((unsigned)c * (unsigned)total / (unsigned)G)
+                    : (long long)c * total / G;
+  }
   // CTA whose range holds iteration it
   __device__ __forceinline__ int cta_of(long long it) const {
-    return (int)(((it + 1) * G - 1) / total);
+    return narrow() ? (int)(((unsigned)(it + 1) * (unsigned)G - 1u) / (unsigned)total)
+                    : (int)(((it + 1) * G - 1) / total);
   }
 };
 
@@ -374,8 +381,8 @@ __global__ void __launch_bounds__(192, CTAS)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int seg = 0;
     for (long long it = it_begin; it < it_end; ++seg) {
-      const int tile = (int)(it / nkb);
-      const int kb0 = (int)(it % nkb);
+      const int tile = (int)((unsigned)it / (unsigned)nkb);  // it < 2^31
+      const int kb0 = (int)it - tile * nkb;
       const long long left = it_end - it;
       const int kb1 = (int)((nkb - kb0) < left ? nkb : kb0 + left);
       it += kb1 - kb0;
