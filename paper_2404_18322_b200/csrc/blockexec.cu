@@ -790,8 +790,20 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     return fail(ctx, BE_ERR_INVALID, "attention partial buffer too small");
 
   int ia = 0, jf = 0;
+  const int n_comp = (int)blk->comps.size();
+  int ci = -1;
+  // the block's last GEMM writes the next-hop rows itself (kResidOut: K2 fused in its epilogue)
+  auto finish = [&](EpiParams& e) {
+    if (ci != n_comp - 1) return;
+    e.mode = bx::kResidOut;
+    e.out = static_cast<bf16*>(arena_out);
+    e.ldo = d;
+    e.tok = tok;
+    e.ss_out = nullptr;
+  };
   for (char kind : blk->comps) {
     int rc;
+    ++ci;
     if (kind == 'f') {
       // ---- ffn component: RMSNorm (fused) -> gate/up + SwiGLU -> down + residual
       const int li = jf;
@@ -822,6 +834,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
       ed.ldr = d;
       ed.ss_out = ws->ss;  // the next component's RMSNorm statistics
       ed.ss_groups = d / 32;
+      finish(ed);
       {
         ed.tl = tl_slot(ctx, BE_K_GEMM_DOWN);
         ed.tl_cap = ctx->tl_cap;
@@ -918,6 +931,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     eo.ldr = d;
     eo.ss_out = ws->ss;
     eo.ss_groups = d / 32;
+    finish(eo);
     {
       eo.tl = tl_slot(ctx, BE_K_GEMM_O);
         eo.tl_cap = ctx->tl_cap;
@@ -927,13 +941,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     }
     if (rc != BE_OK) return rc;
   }
-  // K2: scatter the block outputs to their next-hop rows
-  {
-    ProfScope ps(ctx, st, BE_K_SCATTER, ntok, d, 0, 4.0 * ntok * d, 0);
-    e = bx::launch_scatter(ws->Xb, tok + 1, 5, ntok, d, static_cast<bf16*>(arena_out), st,
-                           tl_slot(ctx, BE_K_SCATTER), ctx->tl_cap);
-  }
-  if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "scatter: %s", cudaGetErrorString(e));
+  // K2 (the scatter to the next-hop rows) ran inside the last GEMM's epilogue (kResidOut)
   return BE_OK;
 }
 
@@ -1084,9 +1092,10 @@ extern "C" int be_exec_batch_launches(be_ctx* ctx, const be_block* blk, int n_to
                                       int pt_stride) {
   if (ctx == nullptr || blk == nullptr || n_tokens <= 0) return 0;
   const int splits = attn_splits(ctx, n_tokens, blk->desc.n_heads, pt_stride);
-  // gather + scatter; attention: qkv, attention (+combine), o; ffn: gate/up, down (the RMSNorms
-  // are fused: statistics from the residual producer, scale in the consumer's epilogue)
-  return 2 + blk->n_att * (3 + (splits > 1 ? 1 : 0)) + blk->n_ffn * 2;
+  // gather; attention: qkv, attention (+combine), o; ffn: gate/up, down (the RMSNorms are fused:
+  // statistics from the residual producer, scale in the consumer's epilogue; the scatter is fused
+  // into the last GEMM's epilogue)
+  return 1 + blk->n_att * (3 + (splits > 1 ? 1 : 0)) + blk->n_ffn * 2;
 }
 
 // ------------------------------------------------------------------------------ KV migration

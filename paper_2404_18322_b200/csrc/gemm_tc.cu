@@ -52,11 +52,11 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] *= rs[i];
   }
-  if constexpr (MODE == kStore || MODE == kResid) {
+  if constexpr (MODE == kStore || MODE == kResid || MODE == kResidOut) {
     const int fe = f & ~1;
     float sq[8];  // kResid: this lane's x^2 + x'^2 of token pair p
     float2 xv[8];
-    if constexpr (MODE == kResid) {
+    if constexpr (MODE == kResid || MODE == kResidOut) {
       // all residual loads of the chunk in flight before the first store (the stores below may
       // alias them as far as the compiler knows, which would serialise 8 L2 round trips)
 #pragma unroll
@@ -76,6 +76,11 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
       if constexpr (MODE == kStore) {
         if (valid)
           *reinterpret_cast<uint32_t*>(E.out + (size_t)t * E.ldo + fe) = pack_bf16x2(lo, hi);
+      } else if constexpr (MODE == kResidOut) {
+        const int drow = valid ? __ldg(E.tok + (size_t)t * 5 + 1) : -1;  // be_token.dst_row
+        if (drow >= 0)
+          *reinterpret_cast<uint32_t*>(E.out + (size_t)drow * E.ldo + fe) =
+              pack_bf16x2(xv[p].x + lo, xv[p].y + hi);
       } else {
         sq[p] = 0.f;
         if (valid) {
@@ -597,6 +602,7 @@ cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream) {
     case kResid: return launch_mode<kResid>(L, stream);
     case kSwiGLU: return launch_mode<kSwiGLU>(L, stream);
     case kQKV: return launch_mode<kQKV>(L, stream);
+    case kResidOut: return launch_mode<kResidOut>(L, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -16,7 +16,9 @@
 
 namespace bx {
 
-enum EpiMode : int { kStore = 0, kResid = 1, kSwiGLU = 2, kQKV = 3 };
+// kResidOut: the block's last GEMM - residual add, then K2 (the scatter) fused: the bf16 row of
+// token t goes straight to out[tok[t].dst_row] (dst_row < 0: not stored); no fp32 / stats copy
+enum EpiMode : int { kStore = 0, kResid = 1, kSwiGLU = 2, kQKV = 3, kResidOut = 4 };
 constexpr int kMaxGroup = 8;  // blocks per grouped batch
 
 struct EpiParams {
