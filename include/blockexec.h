@@ -203,6 +203,34 @@ int be_timeline_read(be_ctx* ctx, be_timeline_rec* out, int cap, int* n_out);
 int be_kv_copy_pages(be_ctx* dst_ctx, const be_kv_pool* src_pool, be_kv_pool* dst_pool,
                      const int32_t* src_slots, const int32_t* dst_slots, int n, void* stream);
 
+/* LoRA adapters on a block's attention components (multi-tenant adapter
+ * deltas by segmented GEMM). A fused-attention LoRA variant (the reference's attach "fuse",
+ * gen_configs.py lora_components; its own block in the zoo, with the base weights as shared
+ * content) runs as the BASE block plus a rank-16 delta per attention projection:
+ * W'_x = W_x + B_x A_x for x in q, k, v, o. Synthetic factors: stream "lora:<name>:<l>:<t>"
+ * (t in aq ak av ao: [16][d], scale_a; bq bk bv bo: [d][16], scale_b), splitmix counter mode as
+ * the weights. One launch serves tokens of up to BE_MAX_LORA adapters (lora_idx per token, -1 =
+ * the base block): the base GEMM streams the shared weights once, a shrink kernel forms
+ * u = A x per token and the GEMM epilogue adds B u before RoPE / the residual add. */
+#define BE_LORA_RANK 16
+#define BE_MAX_LORA 8
+typedef struct be_lora be_lora;
+int be_lora_load(be_ctx* ctx, const be_block* base, const char* name, uint64_t seed,
+                 float scale_a, float scale_b, be_lora** out);
+int be_lora_free(be_lora* lora);
+/* be_exec_batch with adapters: lora_idx (host, n_tokens) picks loras[idx] per token. */
+int be_exec_lora_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int phase,
+                       int n_tokens, const be_token* tokens, int n_pt_rows, int pt_stride,
+                       const int32_t* page_table, int n_lora, const be_lora* const* loras,
+                       const int32_t* lora_idx, const void* d_arena_in, void* d_arena_out,
+                       void* stream);
+/* Same with every per-token array already on the device (graph-capturable). */
+int be_exec_lora_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws,
+                           int phase, int n_tokens, const be_token* d_tokens, int pt_stride,
+                           const int32_t* d_page_table, int n_lora, const be_lora* const* loras,
+                           const int32_t* d_lora_idx, const void* d_arena_in, void* d_arena_out,
+                           void* stream);
+
 /* KV migration with overlapped recompute / copy (the plan is
  * plan_migration, kv.cpp:16-58, bh_plan_migration; the move is start_kv_migration,
  * scenario.cpp:361-431). A segment's n_pages pages (src_slots -> dst_slots, token order, from

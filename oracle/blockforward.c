@@ -155,6 +155,18 @@ const float* or_block_weight(const or_block* b, int layer, const char* t) {
   return NULL;
 }
 
+/* W[layer][tensor] += delta (logical [rows][cols] fp32): a LoRA adapter's B A folded into the
+ * restated weights (the GPU keeps B and A apart; be_exec_lora_batch). */
+int or_block_add_delta(or_block* b, int layer, const char* t, const float* delta) {
+  float* w = (float*)or_block_weight(b, layer, t);
+  if (!w || !delta) return 1;
+  const size_t D = b->desc.d_model, F = b->desc.d_ff;
+  size_t n = D * D;
+  if (!strcmp(t, "wg") || !strcmp(t, "wu") || !strcmp(t, "wd")) n = D * F;
+  for (size_t i = 0; i < n; ++i) w[i] += delta[i];
+  return 0;
+}
+
 or_seq* or_seq_create(const or_block* b, int max_tokens) {
   or_seq* s = (or_seq*)calloc(1, sizeof(or_seq));
   s->n_layers = b->n_att; /* K/V planes: one per attention component */

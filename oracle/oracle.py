@@ -39,6 +39,8 @@ def lib():
         L.or_block_free.argtypes = [P]
         L.or_block_weight.restype = C.POINTER(C.c_float)
         L.or_block_weight.argtypes = [P, C.c_int, C.c_char_p]
+        L.or_block_add_delta.restype = C.c_int
+        L.or_block_add_delta.argtypes = [P, C.c_int, C.c_char_p, P]
         L.or_seq_create.restype = P
         L.or_seq_create.argtypes = [P, C.c_int]
         L.or_seq_free.argtypes = [P]
@@ -84,6 +86,22 @@ class OracleBlock:
                       "wd": (s.d_model, s.d_ff)}[tensor]
         ptr = lib().or_block_weight(self.h, layer, tensor.encode())
         return np.ctypeslib.as_array(ptr, shape=(rows, cols)).copy()
+
+    def add_lora(self, name: str, seed: int, scale_a: float, scale_b: float, rank: int = 16):
+        """Folds a LoRA adapter into the restated weights: W_x += B_x A_x for x in q, k, v, o of
+        every attention layer, the factors being the synthetic streams be_lora_load generates
+        ("lora:<name>:<l>:<t>", include/blockexec.h)."""
+        s = self.shape
+        d = s.d_model
+        n_att = (getattr(s, "comps", None) or "af" * s.n_layers).count("a")
+        for layer in range(n_att):
+            for x in "qkvo":
+                a = synth(rank * d, seed, f"lora:{name}:{layer}:a{x}", scale_a).reshape(rank, d)
+                b = synth(d * rank, seed, f"lora:{name}:{layer}:b{x}", scale_b).reshape(d, rank)
+                delta = np.ascontiguousarray(b.astype(np.float64) @ a.astype(np.float64),
+                                             np.float32)
+                if lib().or_block_add_delta(self.h, layer, f"w{x}".encode(), _p(delta)) != 0:
+                    raise ValueError("oracle: add_delta failed")
 
     def new_seq(self, max_tokens: int) -> "OracleSeq":
         return OracleSeq(self, max_tokens)

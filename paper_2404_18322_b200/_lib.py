@@ -76,6 +76,10 @@ def lib() -> C.CDLL:
         "be_exec_speculative": (I, [P, P, P, P, I, P, P, P, P, F, P, P, P]),
         "be_kv_copy_pages": (I, [P, P, P, P, P, I, P]),
         "be_kv_migrate": (I, [P, P, P, P, P, P, P, I, I, I, P, P]),
+        "be_lora_load": (I, [P, P, C.c_char_p, U64, F, F, PP]),
+        "be_lora_free": (I, [P]),
+        "be_exec_lora_batch": (I, [P, P, P, P, I, I, P, I, I, P, I, P, P, P, P, P]),
+        "be_exec_lora_batch_dev": (I, [P, P, P, P, I, I, P, I, P, I, P, P, P, P, P]),
         "be_exec_batch_dev": (I, [P, P, P, P, I, I, P, I, P, P, P, P]),
         "be_gather_rows": (I, [P, P, P, I, I, P, P]),
         "be_scatter_rows": (I, [P, P, P, I, I, P, P]),

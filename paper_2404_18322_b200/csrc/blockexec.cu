@@ -30,6 +30,9 @@ cudaError_t launch_synth_weight(__nv_bfloat16*, int, int, uint64_t, uint64_t, fl
 cudaError_t launch_synth_rows(__nv_bfloat16*, long long, uint64_t, float, cudaStream_t);
 cudaError_t launch_pack_weight(const __nv_bfloat16*, __nv_bfloat16*, int, int, cudaStream_t);
 cudaError_t launch_rope_table(float2*, int, int, double, cudaStream_t);
+cudaError_t launch_synth_plain(__nv_bfloat16*, int, int, uint64_t, float, int, int, cudaStream_t);
+cudaError_t launch_lora_shrink(const __nv_bfloat16*, int, int, const float*, int, float,
+                               const LoraTable&, int, const int*, float*, int, cudaStream_t);
 // attention.cu
 struct AttnParams {
   const __nv_bfloat16* q;
@@ -138,6 +141,19 @@ struct be_kv_pool {
   int n_layers = 0, n_heads = 0, head_dim = 0;
 };
 
+// LoRA adapter of a block's attention components: per attention layer
+// A_qkv [3r][d] (q, k, v stacked), B_qkv [3d][r] (rows in the fused QKV GEMM's physical order),
+// A_o [r][d], B_o [d][r]; plain row-major bf16, r = kLoraRank
+struct be_lora {
+  be_ctx* ctx = nullptr;
+  int d = 0, n_att = 0;
+  bf16* slab = nullptr;
+  struct Layer {
+    bf16 *aqkv, *bqkv, *ao, *bo;
+  };
+  std::vector<Layer> layers;
+};
+
 struct be_workspace {
   be_ctx* ctx = nullptr;
   int d = 0, dff = 0, H = 0, max_tok = 0, max_rows = 0, max_pages = 0;
@@ -147,6 +163,8 @@ struct be_workspace {
   bf16* attn = nullptr;
   bf16* h = nullptr;
   float* ss = nullptr;  // [max_tok][d / 32] sums of squares of the residual stream (fused RMSNorm)
+  float* lora_u = nullptr;  // [max_tok][3 * kLoraRank] LoRA shrink outputs
+  int32_t* d_lora_idx = nullptr;  // [max_tok] adapter per token (be_exec_lora_batch staging)
   float* splitws = nullptr;
   size_t splitws_elems = 0;
   int* counters = nullptr;
@@ -524,6 +542,8 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
   ok &= cudaMalloc(&w->attn, T * d * sizeof(bf16)) == cudaSuccess;
   ok &= cudaMalloc(&w->h, T * dff * sizeof(bf16)) == cudaSuccess;
   ok &= cudaMalloc(&w->ss, T * (d / 32) * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&w->lora_u, T * 3 * bx::kLoraRank * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&w->d_lora_idx, T * sizeof(int32_t)) == cudaSuccess;
   w->splitws_elems = (size_t)16 << 20;  // 64 MB of fp32 split-K partials (L2 sized)
   ok &= cudaMalloc(&w->splitws, w->splitws_elems * sizeof(float)) == cudaSuccess;
   w->n_counters = 1 << 16;
@@ -565,7 +585,7 @@ extern "C" int be_workspace_free(be_workspace* w) {
   if (w == nullptr) return BE_ERR_INVALID;
   cudaSetDevice(w->ctx->device);
   void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->ss, w->splitws, w->counters, w->prefill_tiles,
-                  w->attn_part, w->d_tokens, w->d_pt};
+                  w->attn_part, w->d_tokens, w->d_pt, w->lora_u, w->d_lora_idx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete w;
@@ -736,9 +756,17 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
 
 // One batch of one block, or a grouped batch of n_grp independent blocks of one shape whose
 // token rows sit side by side in groups of grp_rows = ntok / n_grp (one GEMM n-tile each).
+// Adapters of one launch: token t uses loras[idx[t]] (idx on the device, -1 = base block only)
+struct LoraSet {
+  int n = 0;
+  const be_lora* const* loras = nullptr;
+  const int32_t* idx = nullptr;
+};
+
 int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* pools,
              be_workspace* ws, int phase, int ntok, const be_token* d_tok, int pt_stride,
-             const int32_t* d_pt, const void* arena_in, void* arena_out, cudaStream_t st) {
+             const int32_t* d_pt, const void* arena_in, void* arena_out, cudaStream_t st,
+             const LoraSet* lora = nullptr) {
   be_block* blk = blks[0];
   be_kv_pool* pool = pools[0];
   cudaSetDevice(ctx->device);  // several contexts (GPUs) may share one host thread
@@ -865,6 +893,23 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     eq.d_model = d;
     eq.head_dim = hd;
     eq.rope = blk->rope;
+    if (lora != nullptr) {
+      // segmented LoRA: u = rstd * A_qkv x per token (its adapter), delta added in the epilogue
+      bx::LoraTable ta{}, tb{};
+      for (int a = 0; a < lora->n; ++a) {
+        ta.p[a] = lora->loras[a]->layers[l].aqkv;
+        tb.p[a] = lora->loras[a]->layers[l].bqkv;
+      }
+      e = bx::launch_lora_shrink(ws->Xb, d, d, ws->ss, d / 32, D.norm_eps, ta, 3 * bx::kLoraRank,
+                                 lora->idx, ws->lora_u, ntok, st);
+      if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "lora shrink: %s", cudaGetErrorString(e));
+      eq.mode = bx::kQKVLora;
+      eq.lora_u = ws->lora_u;
+      eq.lora_ustride = 3 * bx::kLoraRank;
+      eq.lora_seg = d;
+      eq.lora_idx = lora->idx;
+      eq.lora_b = tb;
+    }
     {
       eq.tl = tl_slot(ctx, BE_K_GEMM_QKV);
         eq.tl_cap = ctx->tl_cap;
@@ -932,6 +977,22 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     eo.ss_out = ws->ss;
     eo.ss_groups = d / 32;
     finish(eo);
+    if (lora != nullptr) {
+      bx::LoraTable ta{}, tb{};
+      for (int a = 0; a < lora->n; ++a) {
+        ta.p[a] = lora->loras[a]->layers[l].ao;
+        tb.p[a] = lora->loras[a]->layers[l].bo;
+      }
+      e = bx::launch_lora_shrink(ws->attn, d, d, nullptr, d / 32, 0.f, ta, bx::kLoraRank,
+                                 lora->idx, ws->lora_u, ntok, st);
+      if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "lora shrink: %s", cudaGetErrorString(e));
+      eo.mode = eo.mode == bx::kResidOut ? bx::kResidOutLora : bx::kResidLora;
+      eo.lora_u = ws->lora_u;
+      eo.lora_ustride = bx::kLoraRank;
+      eo.lora_seg = d;
+      eo.lora_idx = lora->idx;
+      eo.lora_b = tb;
+    }
     {
       eo.tl = tl_slot(ctx, BE_K_GEMM_O);
         eo.tl_cap = ctx->tl_cap;
@@ -980,10 +1041,27 @@ extern "C" int be_exec_group_dev(be_ctx* ctx, int n_blocks, be_block* const* blk
                   d_page_table, d_arena_in, d_arena_out, pick_stream(ctx, stream));
 }
 
+namespace {
+int exec_batch_host(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int phase,
+                    int n_tokens, const be_token* tokens, int n_pt_rows, int pt_stride,
+                    const int32_t* page_table, const void* d_arena_in, void* d_arena_out,
+                    cudaStream_t stream, const LoraSet* lora);
+}  // namespace
+
 extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws,
                              int phase, int n_tokens, const be_token* tokens, int n_pt_rows,
                              int pt_stride, const int32_t* page_table, const void* d_arena_in,
                              void* d_arena_out, void* stream) {
+  return exec_batch_host(ctx, blk, pool, ws, phase, n_tokens, tokens, n_pt_rows, pt_stride,
+                         page_table, d_arena_in, d_arena_out,
+                         ctx ? pick_stream(ctx, stream) : nullptr, nullptr);
+}
+
+namespace {
+int exec_batch_host(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws, int phase,
+                    int n_tokens, const be_token* tokens, int n_pt_rows, int pt_stride,
+                    const int32_t* page_table, const void* d_arena_in, void* d_arena_out,
+                    cudaStream_t stream, const LoraSet* lora) {
   if (ctx == nullptr || blk == nullptr || pool == nullptr || ws == nullptr || n_tokens < 0 ||
       (n_tokens > 0 && tokens == nullptr) || pt_stride <= 0 || n_pt_rows < 0)
     return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_batch: bad arguments") : BE_ERR_INVALID;
@@ -1004,7 +1082,7 @@ extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_wo
     if (page_table[i] < -1 || page_table[i] >= pool->n_pages)
       return fail(ctx, BE_ERR_INVALID, "page table entry %lld out of range", (long long)i);
   cudaSetDevice(ctx->device);
-  cudaStream_t st = pick_stream(ctx, stream);
+  cudaStream_t st = stream;
   if (n_tokens > 0)
     BE_CUDA(ctx, cudaMemcpyAsync(ws->d_tokens, tokens, n_tokens * sizeof(be_token),
                                  cudaMemcpyHostToDevice, st));
@@ -1012,7 +1090,116 @@ extern "C" int be_exec_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_wo
     BE_CUDA(ctx, cudaMemcpyAsync(ws->d_pt, page_table, (size_t)n_pt_rows * pt_stride * sizeof(int32_t),
                                  cudaMemcpyHostToDevice, st));
   return exec_dev(ctx, 1, &blk, &pool, ws, phase, n_tokens, ws->d_tokens, pt_stride, ws->d_pt,
-                  d_arena_in, d_arena_out, st);
+                  d_arena_in, d_arena_out, st, lora);
+}
+}  // namespace
+
+// ------------------------------------------------------------------------------ LoRA adapters
+extern "C" int be_lora_load(be_ctx* ctx, const be_block* base, const char* name, uint64_t seed,
+                            float scale_a, float scale_b, be_lora** out) {
+  if (ctx == nullptr || base == nullptr || name == nullptr || out == nullptr)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_lora_load: bad arguments") : BE_ERR_INVALID;
+  if (base->n_att == 0) return fail(ctx, BE_ERR_INVALID, "be_lora_load: block has no attention");
+  cudaSetDevice(ctx->device);
+  constexpr int r = bx::kLoraRank;
+  const size_t D = base->desc.d_model;
+  const size_t per_layer = 3 * r * D + 3 * D * r + r * D + D * r;
+  auto* L = new be_lora();
+  L->ctx = ctx;
+  L->d = (int)D;
+  L->n_att = base->n_att;
+  if (cudaMalloc(&L->slab, per_layer * L->n_att * sizeof(bf16)) != cudaSuccess) {
+    delete L;
+    return fail(ctx, BE_ERR_NOMEM, "be_lora_load: allocation failed");
+  }
+  cudaStream_t st = ctx->stream;
+  const int hd = base->desc.head_dim;
+  bf16* cur = L->slab;
+  for (int l = 0; l < L->n_att; ++l) {
+    be_lora::Layer Y{cur, cur + 3 * r * D, cur + 6 * r * D, cur + 7 * r * D};
+    cur += per_layer;
+    auto key = [&](const char* t) {
+      return stream_key(seed, std::string("lora:") + name + ":" + std::to_string(l) + ":" + t);
+    };
+    // A rows: logical order; B rows: the GEMM's physical row order (q/k pair interleave)
+    bx::launch_synth_plain(Y.aqkv, r, (int)D, key("aq"), scale_a, 0, hd, st);
+    bx::launch_synth_plain(Y.aqkv + r * D, r, (int)D, key("ak"), scale_a, 0, hd, st);
+    bx::launch_synth_plain(Y.aqkv + 2 * r * D, r, (int)D, key("av"), scale_a, 0, hd, st);
+    bx::launch_synth_plain(Y.bqkv, (int)D, r, key("bq"), scale_b, 1, hd, st);
+    bx::launch_synth_plain(Y.bqkv + D * r, (int)D, r, key("bk"), scale_b, 1, hd, st);
+    bx::launch_synth_plain(Y.bqkv + 2 * D * r, (int)D, r, key("bv"), scale_b, 0, hd, st);
+    bx::launch_synth_plain(Y.ao, r, (int)D, key("ao"), scale_a, 0, hd, st);
+    bx::launch_synth_plain(Y.bo, (int)D, r, key("bo"), scale_b, 0, hd, st);
+    L->layers.push_back(Y);
+  }
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cudaFree(L->slab);
+    delete L;
+    return fail(ctx, BE_ERR_CUDA, "be_lora_load: %s", cudaGetErrorString(e));
+  }
+  *out = L;
+  return BE_OK;
+}
+
+extern "C" int be_lora_free(be_lora* l) {
+  if (l == nullptr) return BE_ERR_INVALID;
+  cudaSetDevice(l->ctx->device);
+  if (l->slab) cudaFree(l->slab);
+  delete l;
+  return BE_OK;
+}
+
+namespace {
+int check_loras(be_ctx* ctx, const be_block* blk, int n_lora, const be_lora* const* loras) {
+  if (n_lora < 1 || n_lora > bx::kMaxLora || loras == nullptr)
+    return fail(ctx, BE_ERR_INVALID, "lora batch: 1..%d adapters", bx::kMaxLora);
+  for (int a = 0; a < n_lora; ++a)
+    if (loras[a] == nullptr || loras[a]->d != blk->desc.d_model || loras[a]->n_att != blk->n_att)
+      return fail(ctx, BE_ERR_INVALID, "lora batch: adapter %d does not fit the block", a);
+  return BE_OK;
+}
+}  // namespace
+
+extern "C" int be_exec_lora_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool,
+                                      be_workspace* ws, int phase, int n_tokens,
+                                      const be_token* d_tokens, int pt_stride,
+                                      const int32_t* d_page_table, int n_lora,
+                                      const be_lora* const* loras, const int32_t* d_lora_idx,
+                                      const void* d_arena_in, void* d_arena_out, void* stream) {
+  if (ctx == nullptr || blk == nullptr || pool == nullptr || ws == nullptr || n_tokens <= 0 ||
+      d_tokens == nullptr || d_page_table == nullptr || d_lora_idx == nullptr ||
+      d_arena_in == nullptr || pt_stride <= 0 || n_tokens > ws->max_tok)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_lora_batch_dev: bad arguments") : BE_ERR_INVALID;
+  int rc = check_loras(ctx, blk, n_lora, loras);
+  if (rc != BE_OK) return rc;
+  LoraSet set{n_lora, loras, d_lora_idx};
+  return exec_dev(ctx, 1, &blk, &pool, ws, phase, n_tokens, d_tokens, pt_stride, d_page_table,
+                  d_arena_in, d_arena_out, pick_stream(ctx, stream), &set);
+}
+
+extern "C" int be_exec_lora_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws,
+                                  int phase, int n_tokens, const be_token* tokens, int n_pt_rows,
+                                  int pt_stride, const int32_t* page_table, int n_lora,
+                                  const be_lora* const* loras, const int32_t* lora_idx,
+                                  const void* d_arena_in, void* d_arena_out, void* stream) {
+  if (ctx == nullptr || blk == nullptr || n_tokens <= 0 || lora_idx == nullptr)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_lora_batch: bad arguments") : BE_ERR_INVALID;
+  int rc = check_loras(ctx, blk, n_lora, loras);
+  if (rc != BE_OK) return rc;
+  for (int t = 0; t < n_tokens; ++t)
+    if (lora_idx[t] < -1 || lora_idx[t] >= n_lora)
+      return fail(ctx, BE_ERR_INVALID, "token %d: adapter index %d out of range", t, lora_idx[t]);
+  if (n_tokens > ws->max_tok)
+    return fail(ctx, BE_ERR_INVALID, "batch of %d tokens > workspace %d", n_tokens, ws->max_tok);
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = pick_stream(ctx, stream);
+  BE_CUDA(ctx, cudaMemcpyAsync(ws->d_lora_idx, lora_idx, n_tokens * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, st));
+  // the token / page-table validation and staging of be_exec_batch, then the adapter launch
+  LoraSet set{n_lora, loras, ws->d_lora_idx};
+  return exec_batch_host(ctx, blk, pool, ws, phase, n_tokens, tokens, n_pt_rows, pt_stride,
+                         page_table, d_arena_in, d_arena_out, st, &set);
 }
 
 extern "C" int be_exec_speculative(be_ctx* ctx, const be_spec_stage* verify,

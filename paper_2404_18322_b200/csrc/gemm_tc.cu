@@ -41,22 +41,56 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // lane pairs: for token pair (2p, 2p+1) one shuffle gives the even lane features (f, f+1) of
 // token 2p and the odd lane features (f-1, f) of token 2p+1, so every store is a bf16x2 / float2.
 // rs: the chunk's 16 per-token RMSNorm scales (shared memory), nullptr = no norm.
+// LoRA delta of feature row f for the chunk's tokens: v[i] += <B_a[f][0..r), u[t][seg*r ..)>.
+// B rows are 32 bytes (r = 16 bf16), u slices are broadcast loads shared by the warp.
+__device__ __forceinline__ void lora_add(const EpiParams& E, int f, int t0, int nvalid,
+                                         float (&v)[16]) {
+  const int seg = f / E.lora_seg;
+#pragma unroll 1
+  for (int i = 0; i < nvalid; ++i) {
+    const int a = __ldg(E.lora_idx + t0 + i);  // warp-uniform
+    if (a < 0) continue;
+    const uint4* b = reinterpret_cast<const uint4*>(E.lora_b.p[a] + (size_t)f * kLoraRank);
+    const float4* u = reinterpret_cast<const float4*>(E.lora_u + (size_t)(t0 + i) * E.lora_ustride +
+                                                      seg * kLoraRank);
+    float acc = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4 bw = __ldg(b + h);
+      const __nv_bfloat162* bb = reinterpret_cast<const __nv_bfloat162*>(&bw);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float4 uu = __ldg(u + 2 * h + q);
+        const float2 b0 = __bfloat1622float2(bb[2 * q]), b1 = __bfloat1622float2(bb[2 * q + 1]);
+        acc += b0.x * uu.x + b0.y * uu.y + b1.x * uu.z + b1.y * uu.w;
+      }
+    }
+    v[i] += acc;
+  }
+}
+
 template <int MODE>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0, float (&v)[16],
                                                const float* rs) {
+  // the adapter modes run their base epilogue after adding the LoRA delta
+  constexpr int BASE = MODE == kQKVLora ? kQKV
+                       : MODE == kResidLora ? kResid
+                       : MODE == kResidOutLora ? kResidOut : MODE;
+  constexpr bool kLora = MODE >= kQKVLora;
   const int lane = threadIdx.x & 31;
   const bool odd = (lane & 1) != 0;
   const int nvalid = E.ntok - t0 < 16 ? E.ntok - t0 : 16;  // warp-uniform, >= 1
-  if (MODE != kQKV && rs != nullptr) {
+  if (BASE != kQKV && rs != nullptr) {
     // fused RMSNorm row scale (gamma folded into the weights)
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] *= rs[i];
   }
-  if constexpr (MODE == kStore || MODE == kResid || MODE == kResidOut) {
+  if constexpr (kLora && BASE != kQKV) lora_add(E, f, t0, nvalid, v);
+  if constexpr (BASE == kStore || BASE == kResid || BASE == kResidOut) {
     const int fe = f & ~1;
     float sq[8];  // kResid: this lane's x^2 + x'^2 of token pair p
     float2 xv[8];
-    if constexpr (MODE == kResid || MODE == kResidOut) {
+    if constexpr (BASE == kResid || BASE == kResidOut) {
       // all residual loads of the chunk in flight before the first store (the stores below may
       // alias them as far as the compiler knows, which would serialise 8 L2 round trips)
 #pragma unroll
@@ -73,10 +107,10 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
       const float hi = odd ? v[2 * p + 1] : recv;
       const int t = t0 + 2 * p + (odd ? 1 : 0);
       const bool valid = 2 * p + (odd ? 1 : 0) < nvalid;
-      if constexpr (MODE == kStore) {
+      if constexpr (BASE == kStore) {
         if (valid)
           *reinterpret_cast<uint32_t*>(E.out + (size_t)t * E.ldo + fe) = pack_bf16x2(lo, hi);
-      } else if constexpr (MODE == kResidOut) {
+      } else if constexpr (BASE == kResidOut) {
         const int drow = valid ? __ldg(E.tok + (size_t)t * 5 + 1) : -1;  // be_token.dst_row
         if (drow >= 0)
           *reinterpret_cast<uint32_t*>(E.out + (size_t)drow * E.ldo + fe) =
@@ -93,7 +127,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
         }
       }
     }
-    if constexpr (MODE == kResid) {
+    if constexpr (BASE == kResid) {
       if (E.ss_out != nullptr) {
         // Sum of squares per token over the warp's 32 features: token 2p + parity lives in the 16
         // lanes of that parity. Transposed butterfly: each xor step halves the values a lane
@@ -126,7 +160,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
           E.ss_out[(size_t)(t0 + ti) * E.ss_groups + (f >> 5)] = sq[0];
       }
     }
-  } else if constexpr (MODE == kSwiGLU) {
+  } else if constexpr (BASE == kSwiGLU) {
     // even lane holds gate_j, odd lane holds up_j (rows interleaved at load time)
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
@@ -152,6 +186,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] *= rs[i];
     }
+    if constexpr (kLora) lora_add(E, f, t0, nvalid, v);
     if (sec < 2) {
       // rows are pair-interleaved per head: even = dim j, odd = dim j + hd/2 (rotate_half)
 #pragma unroll
@@ -603,6 +638,9 @@ cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream) {
     case kSwiGLU: return launch_mode<kSwiGLU>(L, stream);
     case kQKV: return launch_mode<kQKV>(L, stream);
     case kResidOut: return launch_mode<kResidOut>(L, stream);
+    case kQKVLora: return launch_mode<kQKVLora>(L, stream);
+    case kResidLora: return launch_mode<kResidLora>(L, stream);
+    case kResidOutLora: return launch_mode<kResidOutLora>(L, stream);
     default: return cudaErrorInvalidValue;
   }
 }

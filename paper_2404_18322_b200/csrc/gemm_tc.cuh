@@ -18,8 +18,19 @@ namespace bx {
 
 // kResidOut: the block's last GEMM - residual add, then K2 (the scatter) fused: the bf16 row of
 // token t goes straight to out[tok[t].dst_row] (dst_row < 0: not stored); no fp32 / stats copy
-enum EpiMode : int { kStore = 0, kResid = 1, kSwiGLU = 2, kQKV = 3, kResidOut = 4 };
+// k*Lora: the same epilogues plus a per-token low-rank adapter delta added to the (normalised)
+// accumulator before anything else: v[t][f] += <B_{a(t)}[f], u[t][seg(f)]> (segmented LoRA: the
+// tokens of one launch may belong to different adapters; u from lora_shrink_kernel)
+enum EpiMode : int {
+  kStore = 0, kResid = 1, kSwiGLU = 2, kQKV = 3, kResidOut = 4,
+  kQKVLora = 5, kResidLora = 6, kResidOutLora = 7
+};
 constexpr int kMaxGroup = 8;  // blocks per grouped batch
+constexpr int kLoraRank = 16;  // LoRA rank r of every adapter
+constexpr int kMaxLora = 8;    // adapters per launch
+struct LoraTable {
+  const __nv_bfloat16* p[kMaxLora];
+};
 
 struct EpiParams {
   int mode;
@@ -59,6 +70,13 @@ struct EpiParams {
   __nv_bfloat16* kvgrp[kMaxGroup];
   unsigned long long* tl;     // diagnostics: kernel timeline slot (ptx.cuh tl_*), nullptr = off
   int tl_cap;
+  // k*Lora modes: u [ntok][ustride] fp32, adapter per token (-1: none), B_a [N][kLoraRank] bf16
+  // rows in the GEMM's physical row order; segment f / lora_seg picks u's r-slice (q / k / v)
+  const float* lora_u;
+  int lora_ustride;
+  int lora_seg;
+  const int* lora_idx;
+  LoraTable lora_b;
 };
 
 constexpr int kBM = 128;

@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "ptx.cuh"
+#include "gemm_tc.cuh"
 
 namespace bx {
 
@@ -169,6 +170,68 @@ __global__ void synth_weight_kernel(__nv_bfloat16* __restrict__ dst, int rows, i
   }
 }
 
+// LoRA adapter factors in plain row-major layout: rows of the logical stream, perm 1 = the q/k
+// rotate_half pair interleave of the GEMM rows they feed (same row map as synth_weight_kernel)
+__global__ void synth_plain_kernel(__nv_bfloat16* __restrict__ dst, int rows, int cols,
+                                   uint64_t key, float scale, int perm, int head_dim) {
+  const long long total = (long long)rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int pr = (int)(idx / cols);
+    const int c = (int)(idx - (long long)pr * cols);
+    int lr = pr;
+    if (perm == 1) {
+      const int h = pr / head_dim, e = pr - h * head_dim;
+      lr = h * head_dim + ((e & 1) ? (e >> 1) + head_dim / 2 : (e >> 1));
+    }
+    dst[idx] = __float2bfloat16_rn(synth_value(key, (uint64_t)lr * cols + c, scale));
+  }
+}
+
+// LoRA shrink (segmented by adapter): u[t][j] = scale_t * <A_{a(t)}[j], x[t]> for j < r3, where
+// a(t) = idx[t] (-1: no adapter, u = 0) and scale_t = rstd of the token's fused RMSNorm (from the
+// residual producer's sums of squares, as the GEMM computes it) or 1 without a norm. One CTA per
+// token; the row is staged in shared memory as fp32, each warp takes rows j = warp, warp + 4, ...
+__global__ void lora_shrink_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int d,
+                                   const float* __restrict__ ss, int ss_groups, float eps,
+                                   LoraTable A, int r3, const int* __restrict__ idx,
+                                   float* __restrict__ u) {
+  extern __shared__ float xs[];
+  const int t = blockIdx.x;
+  const int a = idx[t];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a < 0) {
+    for (int j = threadIdx.x; j < r3; j += blockDim.x) u[(size_t)t * r3 + j] = 0.f;
+    return;
+  }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) xs[c] = __bfloat162float(x[(size_t)t * ldx + c]);
+  __shared__ float s_scale;
+  if (warp == 0) {
+    float sc = 1.f;
+    if (ss != nullptr) {
+      float sum = 0.f;
+      for (int g = lane; g < ss_groups; g += 32) sum += ss[(size_t)t * ss_groups + g];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      sc = rsqrtf(sum / (float)d + eps);
+    }
+    if (lane == 0) s_scale = sc;
+  }
+  __syncthreads();
+  const __nv_bfloat16* Aa = A.p[a];
+  for (int j = warp; j < r3; j += blockDim.x >> 5) {
+    const __nv_bfloat16* row = Aa + (size_t)j * d;
+    float acc = 0.f;
+    for (int c = lane * 2; c < d; c += 64) {
+      const float2 w = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(row + c));
+      acc += w.x * xs[c] + w.y * xs[c + 1];
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) u[(size_t)t * r3 + j] = acc * s_scale;
+  }
+}
+
 // row-major [rows][cols] -> packed tile layout (ptx.cuh packed_index)
 __global__ void pack_weight_kernel(const __nv_bfloat16* __restrict__ src,
                                    __nv_bfloat16* __restrict__ dst, int rows, int cols) {
@@ -238,6 +301,20 @@ cudaError_t launch_synth_weight(__nv_bfloat16* dst, int rows, int cols, uint64_t
                                 const float* gamma, cudaStream_t st, int src_cols) {
   synth_weight_kernel<<<grid_for((long long)rows * cols, 256, 148 * 32), 256, 0, st>>>(
       dst, rows, cols, key0, key1, scale, perm, head_dim, gamma, src_cols > 0 ? src_cols : cols);
+  return cudaGetLastError();
+}
+cudaError_t launch_synth_plain(__nv_bfloat16* dst, int rows, int cols, uint64_t key, float scale,
+                               int perm, int head_dim, cudaStream_t st) {
+  synth_plain_kernel<<<grid_for((long long)rows * cols, 256, 148 * 32), 256, 0, st>>>(
+      dst, rows, cols, key, scale, perm, head_dim);
+  return cudaGetLastError();
+}
+cudaError_t launch_lora_shrink(const __nv_bfloat16* x, int ldx, int d, const float* ss,
+                               int ss_groups, float eps, const LoraTable& A, int r3,
+                               const int* idx, float* u, int ntok, cudaStream_t st) {
+  if (ntok <= 0) return cudaSuccess;
+  lora_shrink_kernel<<<ntok, 128, d * sizeof(float), st>>>(x, ldx, d, ss, ss_groups, eps, A, r3,
+                                                            idx, u);
   return cudaGetLastError();
 }
 cudaError_t launch_pack_weight(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int cols,

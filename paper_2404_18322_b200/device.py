@@ -236,6 +236,44 @@ def exec_batch(ctx: Context, block: Block, pool: KvPool, ws: Workspace, phase: i
                               stream if stream is not None else C.c_void_p(0)), ctx.h)
 
 
+class Lora:
+    """A rank-16 LoRA adapter of a block's attention components (be_lora_load): W'_x = W_x +
+    B_x A_x, x in q, k, v, o; synthetic factors from the stream "lora:<name>:<layer>:<t>"."""
+
+    def __init__(self, ctx: Context, base: "Block", name: str, seed: int = 1,
+                 scale_a: float | None = None, scale_b: float | None = None):
+        self.ctx, self.name, self.seed = ctx, name, seed
+        s = base.shape.init_scale
+        self.scale_a = s if scale_a is None else scale_a
+        self.scale_b = s if scale_b is None else scale_b
+        h = C.c_void_p()
+        check(lib().be_lora_load(ctx.h, base.h, name.encode(), seed, self.scale_a, self.scale_b,
+                                 C.byref(h)), ctx.h)
+        self.h = h
+
+    def free(self):
+        if self.h:
+            lib().be_lora_free(self.h)
+            self.h = None
+
+
+def exec_lora_batch(ctx: Context, block: "Block", pool: "KvPool", ws: "Workspace", phase: int,
+                    tokens, page_table: np.ndarray, loras, lora_idx, arena_in, arena_out,
+                    stream=None) -> None:
+    """exec_batch with adapters: token i uses loras[lora_idx[i]] (-1: the base block)."""
+    toks = tokens_array(tokens)
+    n = len(tokens)
+    pt = np.ascontiguousarray(page_table, dtype=np.int32)
+    idx = np.ascontiguousarray(lora_idx, dtype=np.int32)
+    arr = (C.c_void_p * max(1, len(loras)))(*[lo.h.value for lo in loras])
+    check(lib().be_exec_lora_batch(ctx.h, block.h, pool.h, ws.h, phase, n,
+                                   C.cast(toks, C.c_void_p), pt.shape[0], pt.shape[1],
+                                   pt.ctypes.data_as(C.c_void_p), len(loras), arr,
+                                   idx.ctypes.data_as(C.c_void_p), _ptr(arena_in),
+                                   _ptr(arena_out),
+                                   stream if stream is not None else C.c_void_p(0)), ctx.h)
+
+
 class SpecStage(C.Structure):
     _fields_ = [("blk", C.c_void_p), ("pool", C.c_void_p), ("ws", C.c_void_p),
                 ("tokens", C.c_void_p), ("n_pt_rows", C.c_int), ("pt_stride", C.c_int),
