@@ -42,36 +42,63 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // token 2p and the odd lane features (f-1, f) of token 2p+1, so every store is a bf16x2 / float2.
 // rs: the chunk's 16 per-token RMSNorm scales (shared memory), nullptr = no norm.
 // LoRA delta of feature row f for the chunk's tokens: v[i] += <B_a[f][0..r), u[t][seg*r ..)>.
-// B rows are 32 bytes (r = 16 bf16), u slices are broadcast loads shared by the warp.
-__device__ __forceinline__ void lora_add(const EpiParams& E, int f, int t0, int nvalid,
-                                         float (&v)[16]) {
-  const int seg = f / E.lora_seg;
+// B rows are 32 bytes (r = 16 bf16), u slices are broadcast loads shared by the warp. A chunk's
+// 16 tokens usually belong to one adapter (batches are segmented by tenant): then B's row is
+// loaded once and the u slices of 4 tokens at a time are all in flight together.
+__device__ __forceinline__ float lora_dot(const float (&b)[kLoraRank], const float4* u) {
+  float acc = 0.f;
+#pragma unroll
+  for (int q = 0; q < kLoraRank / 4; ++q) {
+    const float4 uu = u[q];
+    acc += b[4 * q] * uu.x + b[4 * q + 1] * uu.y + b[4 * q + 2] * uu.z + b[4 * q + 3] * uu.w;
+  }
+  return acc;
+}
+__device__ __forceinline__ void lora_brow(const EpiParams& E, int a, int f, float (&b)[kLoraRank]) {
+  const uint4* p = reinterpret_cast<const uint4*>(E.lora_b.p[a] + (size_t)f * kLoraRank);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint4 w = __ldg(p + h);
+    const __nv_bfloat162* bb = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 x = __bfloat1622float2(bb[q]);
+      b[8 * h + 2 * q] = x.x;
+      b[8 * h + 2 * q + 1] = x.y;
+    }
+  }
+}
+// lu: the tile's u slices in shared memory, [BN][kLoraRank] from token n0; li: adapters [BN]
+__device__ __forceinline__ void lora_add(const EpiParams& E, int f, int tt0, int nvalid,
+                                         float (&v)[16], const float* lu, const int* li) {
+  const int lane = threadIdx.x & 31;
+  const int my_a = (lane & 15) < nvalid ? li[tt0 + (lane & 15)] : -1;
+  const int a0 = __shfl_sync(0xffffffffu, my_a, 0);
+  const bool uniform = __all_sync(0xffffffffu, (lane & 15) >= nvalid || my_a == a0);
+  const float4* ub = reinterpret_cast<const float4*>(lu + (size_t)tt0 * kLoraRank);
+  if (uniform) {
+    if (a0 < 0) return;
+    float b[kLoraRank];
+    lora_brow(E, a0, f, b);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < nvalid) v[i] += lora_dot(b, ub + i * (kLoraRank / 4));
+    return;
+  }
 #pragma unroll 1
   for (int i = 0; i < nvalid; ++i) {
-    const int a = __ldg(E.lora_idx + t0 + i);  // warp-uniform
+    const int a = __shfl_sync(0xffffffffu, my_a, i);
     if (a < 0) continue;
-    const uint4* b = reinterpret_cast<const uint4*>(E.lora_b.p[a] + (size_t)f * kLoraRank);
-    const float4* u = reinterpret_cast<const float4*>(E.lora_u + (size_t)(t0 + i) * E.lora_ustride +
-                                                      seg * kLoraRank);
-    float acc = 0.f;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint4 bw = __ldg(b + h);
-      const __nv_bfloat162* bb = reinterpret_cast<const __nv_bfloat162*>(&bw);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const float4 uu = __ldg(u + 2 * h + q);
-        const float2 b0 = __bfloat1622float2(bb[2 * q]), b1 = __bfloat1622float2(bb[2 * q + 1]);
-        acc += b0.x * uu.x + b0.y * uu.y + b1.x * uu.z + b1.y * uu.w;
-      }
-    }
-    v[i] += acc;
+    float b[kLoraRank];
+    lora_brow(E, a, f, b);
+    v[i] += lora_dot(b, ub + i * (kLoraRank / 4));
   }
 }
 
 template <int MODE>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0, float (&v)[16],
-                                               const float* rs) {
+                                               const float* rs, const float* lu = nullptr,
+                                               const int* li = nullptr, int n0 = 0) {
   // the adapter modes run their base epilogue after adding the LoRA delta
   constexpr int BASE = MODE == kQKVLora ? kQKV
                        : MODE == kResidLora ? kResid
@@ -85,7 +112,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] *= rs[i];
   }
-  if constexpr (kLora && BASE != kQKV) lora_add(E, f, t0, nvalid, v);
+  if constexpr (kLora && BASE != kQKV) lora_add(E, f, t0 - n0, nvalid, v, lu, li);
   if constexpr (BASE == kStore || BASE == kResid || BASE == kResidOut) {
     const int fe = f & ~1;
     float sq[8];  // kResid: this lane's x^2 + x'^2 of token pair p
@@ -186,7 +213,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] *= rs[i];
     }
-    if constexpr (kLora) lora_add(E, f, t0, nvalid, v);
+    if constexpr (kLora) lora_add(E, f, t0 - n0, nvalid, v, lu, li);
     if (sec < 2) {
       // rows are pair-interleaved per head: even = dim j, odd = dim j + hd/2 (rotate_half)
 #pragma unroll
@@ -293,6 +320,8 @@ __global__ void __launch_bounds__(192, CTAS)
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   float* rs_smem = reinterpret_cast<float*>(tmem_holder + 4);  // [2][BN] per-token rstd
+  float* lu_smem = rs_smem + 2 * BN;                           // k*Lora: [BN][r] u slices
+  int* li_smem = reinterpret_cast<int*>(lu_smem + BN * kLoraRank);  // k*Lora: [BN] adapters
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -440,6 +469,24 @@ __global__ void __launch_bounds__(192, CTAS)
         tile_rstd<BN>(E, n0, q, rs);
         named_bar_sync(2, 128);
       }
+      if constexpr (MODE >= kQKVLora) {
+        if (runs_epilogue) {
+          // the tile's LoRA u slices (its 128 rows lie in one q / k / v segment) and adapters
+          named_bar_sync(3, 128);  // the previous tile's readers are done with the buffer
+          const int et = threadIdx.x - 64;  // epilogue thread 0..127
+          const int sg = m0 / E.lora_seg;
+          float4* lu4 = reinterpret_cast<float4*>(lu_smem);
+          for (int k = et; k < BN * (kLoraRank / 4); k += 128) {
+            const int tt = k / (kLoraRank / 4), qq = k % (kLoraRank / 4);
+            lu4[k] = n0 + tt < E.ntok
+                         ? __ldg(reinterpret_cast<const float4*>(
+                               E.lora_u + (size_t)(n0 + tt) * E.lora_ustride + sg * kLoraRank) + qq)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          for (int k = et; k < BN; k += 128) li_smem[k] = n0 + k < E.ntok ? __ldg(E.lora_idx + n0 + k) : -1;
+          named_bar_sync(3, 128);
+        }
+      }
       mbar_wait(&tfull[a], u & 1u);
       tc_fence_after();
       if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
@@ -451,7 +498,7 @@ __global__ void __launch_bounds__(192, CTAS)
           if (n0 + c0 >= E.ntok) break;
           float acc[16];
           tmem_ld16(t_lane + c0, acc);
-          epilogue_chunk<MODE>(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr);
+          epilogue_chunk<MODE>(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr, lu_smem, li_smem, n0);
         }
       } else {
         // Partial tile. Its owner is the CTA holding the tile's first k-block (c_first): for
@@ -536,7 +583,7 @@ __global__ void __launch_bounds__(192, CTAS)
             for (int c0 = 0; c0 < BN; c0 += 16) {
               if (n0 + c0 >= E.ntok) break;
               epilogue_chunk<MODE>(E, f, n0 + c0, *reinterpret_cast<float(*)[16]>(acc + c0),
-                                   rs ? rs + c0 : nullptr);
+                                   rs ? rs + c0 : nullptr, lu_smem, li_smem, n0);
             }
           } else {
 #pragma unroll 1
@@ -565,7 +612,7 @@ __global__ void __launch_bounds__(192, CTAS)
                 }
               }
             }
-            epilogue_chunk<MODE>(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr);
+            epilogue_chunk<MODE>(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr, lu_smem, li_smem, n0);
           }
           }
         }
@@ -592,7 +639,8 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   constexpr int STAGES = gemm_stages_deep<BN>();
   constexpr int CTAS = 1;
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
-                       2 * BN * 4 /*rstd*/;
+                       2 * BN * 4 /*rstd*/ +
+                       (MODE >= kQKVLora ? BN * (kLoraRank + 1) * 4 : 0) /*LoRA u, adapters*/;
   auto kern = gemm_sk_kernel<BN, STAGES, CTAS, MODE>;
   static unsigned long long configured = 0;  // per device: the attribute is device state
   int dev = 0;

@@ -191,20 +191,32 @@ __global__ void synth_plain_kernel(__nv_bfloat16* __restrict__ dst, int rows, in
 // LoRA shrink (segmented by adapter): u[t][j] = scale_t * <A_{a(t)}[j], x[t]> for j < r3, where
 // a(t) = idx[t] (-1: no adapter, u = 0) and scale_t = rstd of the token's fused RMSNorm (from the
 // residual producer's sums of squares, as the GEMM computes it) or 1 without a norm. One CTA per
-// token; the row is staged in shared memory as fp32, each warp takes rows j = warp, warp + 4, ...
-__global__ void lora_shrink_kernel(const __nv_bfloat16* __restrict__ x, int ldx, int d,
-                                   const float* __restrict__ ss, int ss_groups, float eps,
-                                   LoraTable A, int r3, const int* __restrict__ idx,
-                                   float* __restrict__ u) {
+// (token, 8 rows of A): the token's row is staged in shared memory as fp32, each warp takes one
+// A row with 16-byte loads, all of them in flight (d <= 8192: at most 32 per lane).
+__global__ void __launch_bounds__(256) lora_shrink_kernel(
+    const __nv_bfloat16* __restrict__ x, int ldx, int d, const float* __restrict__ ss,
+    int ss_groups, float eps, LoraTable A, int r3, const int* __restrict__ idx,
+    float* __restrict__ u) {
   extern __shared__ float xs[];
   const int t = blockIdx.x;
   const int a = idx[t];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (a < 0) {
-    for (int j = threadIdx.x; j < r3; j += blockDim.x) u[(size_t)t * r3 + j] = 0.f;
+    const int j = blockIdx.y * 8 + (int)threadIdx.x;
+    if (threadIdx.x < 8 && j < r3) u[(size_t)t * r3 + j] = 0.f;
     return;
   }
-  for (int c = threadIdx.x; c < d; c += blockDim.x) xs[c] = __bfloat162float(x[(size_t)t * ldx + c]);
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)t * ldx);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
+    const uint4 w = xr[c];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = __bfloat1622float2(h[q]);
+      xs[8 * c + 2 * q] = f.x;
+      xs[8 * c + 2 * q + 1] = f.y;
+    }
+  }
   __shared__ float s_scale;
   if (warp == 0) {
     float sc = 1.f;
@@ -218,13 +230,22 @@ __global__ void lora_shrink_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
     if (lane == 0) s_scale = sc;
   }
   __syncthreads();
-  const __nv_bfloat16* Aa = A.p[a];
-  for (int j = warp; j < r3; j += blockDim.x >> 5) {
-    const __nv_bfloat16* row = Aa + (size_t)j * d;
+  const int nv = d / 8 / 32;  // uint4 loads per lane per row
+  // blockIdx.y picks this CTA's 8 rows of A (one per warp)
+  for (int j = blockIdx.y * 8 + warp; j < r3 && j < blockIdx.y * 8 + 8; j += 8) {
+    const uint4* row = reinterpret_cast<const uint4*>(A.p[a] + (size_t)j * d);
     float acc = 0.f;
-    for (int c = lane * 2; c < d; c += 64) {
-      const float2 w = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(row + c));
-      acc += w.x * xs[c] + w.y * xs[c + 1];
+#pragma unroll 16
+    for (int i = 0; i < nv; ++i) {
+      const int c = lane + 32 * i;
+      const uint4 w = __ldg(row + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+      const float* xv = xs + 8 * c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(h[q]);
+        acc += f.x * xv[2 * q] + f.y * xv[2 * q + 1];
+      }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -313,7 +334,8 @@ cudaError_t launch_lora_shrink(const __nv_bfloat16* x, int ldx, int d, const flo
                                int ss_groups, float eps, const LoraTable& A, int r3,
                                const int* idx, float* u, int ntok, cudaStream_t st) {
   if (ntok <= 0) return cudaSuccess;
-  lora_shrink_kernel<<<ntok, 128, d * sizeof(float), st>>>(x, ldx, d, ss, ss_groups, eps, A, r3,
+  if (d % 256 != 0 || d > 8192) return cudaErrorInvalidValue;  // whole uint4 sweeps per lane
+  lora_shrink_kernel<<<dim3(ntok, (r3 + 7) / 8), 256, d * sizeof(float), st>>>(x, ldx, d, ss, ss_groups, eps, A, r3,
                                                             idx, u);
   return cudaGetLastError();
 }
