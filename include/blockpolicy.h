@@ -13,6 +13,7 @@
  *   bh_policy_placement_moves    Scheduler::placement_moves  scheduler.cpp:321-366
  *   bh_policy_migration_rates    Scheduler::migration_rates  scheduler.cpp:368-381
  *   bh_plan_migration            plan_migration              kv.cpp:16-58
+ *   bh_policy_kv_review          Simulation::kv_review       scenario.cpp:844-900
  *
  * Ids are NUL-terminated strings (the reference's instance / block / model ids). List outputs
  * are written as '\n'-separated ids into a caller buffer. Every call returns a be_status code
@@ -140,6 +141,31 @@ int bh_policy_placement_moves(bh_policy* p, char* ids, int cap, int* devices, in
 int bh_policy_migration_rates(bh_policy* p, const char* block, int src, int dst,
                               int64_t* rec_us_per_page, int64_t* cp_us_per_page);
 int bh_policy_param_bytes_needed(bh_policy* p, const char* block, int device, int64_t* out);
+
+/* Proactive KV review (Simulation::kv_review, scenario.cpp:844-900): the interception tracker
+ * (InterceptionTracker, kv.cpp:70-103) and the queued decode entries whose cache is remote;
+ * order_out receives indices into q of the entries to migrate now, in order_migrations order
+ * (kv.cpp:60-68). */
+typedef struct {
+  const char* instance;     /* the instance holding the queued entry */
+  const char* inst_block;   /* its serving block */
+  int device;               /* its device */
+  uint64_t request_id;
+  const char* chain_block;  /* the request chain's block at the entry's step */
+  int owner;                /* device of the (request, chain block) cache segment, -1 none */
+  int pages, shared_pages;
+  int pending;              /* an interception sample is open for this step */
+  const char* pending_key;
+  int64_t t_call;
+} bh_queued_decode;
+
+int bh_policy_interception_record(bh_policy* p, const char* key, int64_t sample);
+/* key NULL: the global accumulator */
+int bh_policy_interception_set(bh_policy* p, const char* key, double sum, uint64_t n);
+int bh_policy_interception_predict(bh_policy* p, const char* key, int64_t t_call, int64_t now,
+                                   int64_t* out, int* found);
+int bh_policy_kv_review(bh_policy* p, const bh_queued_decode* q, int n, int64_t now,
+                        int recalc_only, int* order_out, int cap, int* n_out);
 
 /* out6 = pages, recompute_pages, copy_pages, completion_us, rec_us_per_page, cp_us_per_page */
 int bh_plan_migration(int pages, int64_t rec_us_per_page, int64_t cp_us_per_page, int64_t* out6);

@@ -773,6 +773,68 @@ rs_policy_trace* rs_policy_trace_run(const char* spec_json) {
           sn["queries"].push_back(qj);
         }
       }
+      // proactive KV review inputs (scenario.cpp:844-900) and the reference primitives' answers:
+      // queued decode entries with remote caches, the interception tracker, and the migration
+      // order kv_review's loop produces from them (order_migrations, predicted_remaining)
+      sn["kvq"] = nlohmann::json::array();
+      std::vector<MigrationCandidate> mcs;
+      std::vector<int> picked;
+      int qi = 0;
+      for (const auto& [iid, inst] : s.pool_.all()) {
+        for (const auto& e : inst.queue) {
+          if (e.phase != Phase::kDecode) continue;
+          const auto& r = s.live_.at((std::uint64_t)e.request_id);
+          const std::string& cb = (*r.chain)[(std::size_t)e.chain_step];
+          const int owner = s.kv_.device_of(r.req.id, cb);
+          auto pend = s.tint_pending_.find({r.req.id, e.chain_step});
+          const bool pending = pend != s.tint_pending_.end();
+          nlohmann::json ej = {{"instance", iid}, {"inst_block", inst.block_id},
+                               {"device", inst.device}, {"request", r.req.id}, {"chain_block", cb},
+                               {"owner", owner},
+                               {"pages", owner >= 0 ? s.kv_.pages(r.req.id, cb) : 0},
+                               {"shared", owner >= 0 ? s.kv_.shared_pages(r.req.id, cb) : 0},
+                               {"pending", pending},
+                               {"pending_key", pending ? pend->second.first : std::string()},
+                               {"t_call", pending ? pend->second.second : (SimTime)0}};
+          sn["kvq"].push_back(ej);
+          if (owner >= 0 && owner != inst.device) {
+            auto [rec, cp] = s.sched_.migration_rates(inst.block_id, owner, inst.device);
+            if (s.cfg_.kv_recalc_only) cp = 0;
+            MigrationPlan plan = plan_migration(s.kv_.pages(r.req.id, cb), rec, cp);
+            const std::string key = pending ? pend->second.first : inst.id;
+            const SimTime t_call = pending ? pend->second.second : now;
+            auto pred = s.tint_.predicted_remaining(key, t_call, now);
+            if (pred.has_value() && *pred >= plan.completion_us) {
+              MigrationCandidate mc;
+              mc.request_id = r.req.id;
+              mc.block_id = cb;
+              mc.shared_pages = s.kv_.shared_pages(r.req.id, cb);
+              mc.resume_time = t_call + *pred;
+              mcs.push_back(mc);
+              picked.push_back(qi);
+            }
+          }
+          ++qi;
+        }
+      }
+      std::vector<MigrationCandidate> ord = mcs;
+      order_migrations(ord);
+      sn["kv_review"] = nlohmann::json::array();
+      for (const auto& mc : ord)
+        for (std::size_t k = 0; k < mcs.size(); ++k)
+          if (mcs[k].request_id == mc.request_id && mcs[k].block_id == mc.block_id) {
+            sn["kv_review"].push_back(picked[k]);
+            break;
+          }
+      sn["tint"] = {{"keys", nlohmann::json::array()},
+                    {"global", {s.tint_.global_sum_, s.tint_.global_n_}}};
+      for (const auto& [k, v] : s.tint_.per_key_) {
+        sn["tint"]["keys"].push_back({k, v.first, v.second});
+        for (SimTime dt : {(SimTime)0, (SimTime)500, (SimTime)5000}) {
+          auto pr = s.tint_.predicted_remaining(k, now - dt, now);
+          sn["tint_predict"].push_back({k, now - dt, pr.has_value() ? *pr : (SimTime)-1});
+        }
+      }
       sn["marks"] = s.sched_.speculation_marks();
       sn["scale"] = nlohmann::json::array();
       for (const auto& d : s.sched_.scale_decisions(now)) sn["scale"].push_back({d.instance_id, d.device});

@@ -601,4 +601,68 @@ std::vector<std::pair<std::string, int>> Policy::placement_moves() const {
   return moves;
 }
 
+// ------------------------------------------------------------------ proactive KV review
+void Interception::record(const std::string& key, std::int64_t sample) {
+  if (sample < 0) throw PolicyError("negative interception sample");
+  auto& [sum, n] = per_key_[key];
+  sum += static_cast<double>(sample);
+  ++n;
+  global_sum_ += static_cast<double>(sample);
+  ++global_n_;
+}
+std::optional<double> Interception::mean(const std::string& key) const {
+  auto it = per_key_.find(key);
+  if (it == per_key_.end() || it->second.second == 0) return std::nullopt;
+  return it->second.first / static_cast<double>(it->second.second);
+}
+std::optional<double> Interception::global_mean() const {
+  if (global_n_ == 0) return std::nullopt;
+  return global_sum_ / static_cast<double>(global_n_);
+}
+std::optional<std::int64_t> Interception::predicted_remaining(const std::string& key,
+                                                              std::int64_t t_call,
+                                                              std::int64_t now) const {
+  auto m = mean(key);
+  if (!m) m = global_mean();
+  if (!m) return std::nullopt;
+  const double left = std::max(0.0, *m - static_cast<double>(now - t_call));
+  return static_cast<std::int64_t>(std::llround(left));  // round_us, time.hpp:22-25
+}
+
+void order_migrations(std::vector<MigrationCandidate>& c) {
+  std::sort(c.begin(), c.end(), [](const MigrationCandidate& a, const MigrationCandidate& b) {
+    return std::tie(a.shared_pages, a.resume_time, a.request_id, a.block_id) <
+           std::tie(b.shared_pages, b.resume_time, b.request_id, b.block_id);
+  });
+}
+
+std::vector<int> Policy::kv_review(const std::vector<QueuedDecode>& q, const Interception& tint,
+                                   std::int64_t now, bool recalc_only) const {
+  std::vector<int> picked;
+  std::vector<MigrationCandidate> cands;
+  for (int i = 0; i < (int)q.size(); ++i) {
+    const QueuedDecode& e = q[i];
+    if (e.owner < 0 || e.owner == e.device) continue;
+    auto [rec, cp] = migration_rates(e.inst_block, e.owner, e.device);
+    if (recalc_only) cp = 0;
+    const Migration plan = plan_migration(e.pages, rec, cp);
+    const std::string& key = e.pending ? e.pending_key : e.instance;
+    const std::int64_t t_call = e.pending ? e.t_call : now;
+    const auto left = tint.predicted_remaining(key, t_call, now);
+    if (!left || *left < plan.completion_us) continue;  // would not finish before it is needed
+    picked.push_back(i);
+    cands.push_back({e.request_id, e.chain_block, e.shared_pages, t_call + *left});
+  }
+  std::vector<MigrationCandidate> order = cands;
+  order_migrations(order);
+  std::vector<int> out;
+  for (const auto& mc : order)
+    for (std::size_t k = 0; k < cands.size(); ++k)
+      if (cands[k].request_id == mc.request_id && cands[k].block_id == mc.block_id) {
+        out.push_back(picked[k]);  // the first queued entry of that (request, block)
+        break;
+      }
+  return out;
+}
+
 }  // namespace bh

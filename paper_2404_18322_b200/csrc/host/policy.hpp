@@ -100,6 +100,48 @@ struct Migration {
 // earliest-free claim per page (kv.cpp:16-58).
 Migration plan_migration(int pages, std::int64_t rec_us_per_page, std::int64_t cp_us_per_page);
 
+// Idle-time predictor for parked KV (InterceptionTracker, kv.cpp:70-103): mean of the observed
+// gaps per key (instance id), the global mean as the fallback.
+class Interception {
+ public:
+  void record(const std::string& key, std::int64_t sample);
+  void set(const std::string& key, double sum, std::uint64_t n) { per_key_[key] = {sum, n}; }
+  void set_global(double sum, std::uint64_t n) {
+    global_sum_ = sum;
+    global_n_ = n;
+  }
+  std::optional<double> mean(const std::string& key) const;
+  std::optional<double> global_mean() const;
+  std::optional<std::int64_t> predicted_remaining(const std::string& key, std::int64_t t_call,
+                                                  std::int64_t now) const;
+
+ private:
+  std::map<std::string, std::pair<double, std::uint64_t>> per_key_;
+  double global_sum_ = 0.0;
+  std::uint64_t global_n_ = 0;
+};
+
+struct MigrationCandidate {
+  std::uint64_t request_id = 0;
+  std::string block_id;
+  int shared_pages = 0;
+  std::int64_t resume_time = 0;
+};
+// fewest shared pages first, then earliest resumption, then ids (kv.cpp:60-68)
+void order_migrations(std::vector<MigrationCandidate>& c);
+
+// A queued decode entry seen by the proactive KV review (scenario.cpp:844-900)
+struct QueuedDecode {
+  std::string instance, inst_block;  // the instance holding the entry, its serving block
+  int device = -1;                   // that instance's device
+  std::uint64_t request_id = 0;
+  std::string chain_block;           // the request chain's block at this step
+  int owner = -1, pages = 0, shared_pages = 0;  // the cache segment of (request, chain block)
+  bool pending = false;              // an interception sample is open for this step
+  std::string pending_key;
+  std::int64_t t_call = 0;
+};
+
 class Policy {
  public:
   explicit Policy(PolicyConfig cfg) : cfg_(cfg) {}
@@ -143,6 +185,11 @@ class Policy {
   std::pair<std::int64_t, std::int64_t> migration_rates(const std::string& block, int src,
                                                         int dst) const;
   std::int64_t max_queue_len(const PolicyInstance& inst) const;
+  // Proactive migrations (Simulation::kv_review, scenario.cpp:844-900): entries whose cache is
+  // remote and predicted to stay idle long enough for the planned move; returned as indices
+  // into `q`, in migration order.
+  std::vector<int> kv_review(const std::vector<QueuedDecode>& q, const Interception& tint,
+                             std::int64_t now, bool recalc_only) const;
 
   // ---- model queries (costmodel.cpp)
   double block_us(const std::string& block, bool decode, double batch, double tokens,

@@ -9,6 +9,7 @@
 struct bh_policy {
   explicit bh_policy(const bh::PolicyConfig& c) : p(c) {}
   bh::Policy p;
+  bh::Interception tint;
   std::string err;
 };
 
@@ -267,6 +268,51 @@ int bh_policy_migration_rates(bh_policy* p, const char* b, int src, int dst, int
 }
 int bh_policy_param_bytes_needed(bh_policy* p, const char* b, int dev, int64_t* out) {
   return guard(p, [&] { *out = p->p.param_bytes_needed(str(b), dev); });
+}
+
+int bh_policy_interception_record(bh_policy* p, const char* key, int64_t sample) {
+  return guard(p, [&] { p->tint.record(str(key), sample); });
+}
+int bh_policy_interception_set(bh_policy* p, const char* key, double sum, uint64_t n) {
+  return guard(p, [&] {
+    if (key == nullptr)
+      p->tint.set_global(sum, n);
+    else
+      p->tint.set(key, sum, n);
+  });
+}
+int bh_policy_interception_predict(bh_policy* p, const char* key, int64_t t_call, int64_t now,
+                                   int64_t* out, int* found) {
+  return guard(p, [&] {
+    const auto r = p->tint.predicted_remaining(str(key), t_call, now);
+    *found = r.has_value() ? 1 : 0;
+    *out = r.value_or(0);
+  });
+}
+int bh_policy_kv_review(bh_policy* p, const bh_queued_decode* q, int n, int64_t now,
+                        int recalc_only, int* order, int cap, int* n_out) {
+  return guard(p, [&] {
+    std::vector<bh::QueuedDecode> v;
+    for (int i = 0; i < n; ++i) {
+      bh::QueuedDecode e;
+      e.instance = str(q[i].instance);
+      e.inst_block = str(q[i].inst_block);
+      e.device = q[i].device;
+      e.request_id = q[i].request_id;
+      e.chain_block = str(q[i].chain_block);
+      e.owner = q[i].owner;
+      e.pages = q[i].pages;
+      e.shared_pages = q[i].shared_pages;
+      e.pending = q[i].pending != 0;
+      e.pending_key = str(q[i].pending_key);
+      e.t_call = q[i].t_call;
+      v.push_back(std::move(e));
+    }
+    const auto out = p->p.kv_review(v, p->tint, now, recalc_only != 0);
+    if ((int)out.size() > cap) throw bh::PolicyError("order buffer too small");
+    for (std::size_t i = 0; i < out.size(); ++i) order[i] = out[i];
+    *n_out = (int)out.size();
+  });
 }
 
 int bh_plan_migration(int pages, int64_t rec, int64_t cp, int64_t* out6) {

@@ -43,6 +43,13 @@ class _Instance(C.Structure):
                 ("queued_cost_us", C.c_double), ("queued_cost_hwm", C.c_double)]
 
 
+class _QueuedDecode(C.Structure):
+    _fields_ = [("instance", C.c_char_p), ("inst_block", C.c_char_p), ("device", C.c_int),
+                ("request_id", C.c_uint64), ("chain_block", C.c_char_p), ("owner", C.c_int),
+                ("pages", C.c_int), ("shared_pages", C.c_int), ("pending", C.c_int),
+                ("pending_key", C.c_char_p), ("t_call", C.c_int64)]
+
+
 class _Query(C.Structure):
     _fields_ = [("request_id", C.c_uint64), ("chain_block", C.c_char_p), ("phase", C.c_int),
                 ("tokens", C.c_int), ("context_tokens", C.c_int), ("from_device", C.c_int),
@@ -98,6 +105,10 @@ def _bind():
         "bh_policy_migration_rates": (I, [P, S, I, I, C.POINTER(I64), C.POINTER(I64)]),
         "bh_policy_param_bytes_needed": (I, [P, S, I, C.POINTER(I64)]),
         "bh_plan_migration": (I, [I, I64, I64, P]),
+        "bh_policy_interception_record": (I, [P, S, I64]),
+        "bh_policy_interception_set": (I, [P, S, D, U64]),
+        "bh_policy_interception_predict": (I, [P, S, I64, I64, C.POINTER(I64), C.POINTER(I)]),
+        "bh_policy_kv_review": (I, [P, C.POINTER(_QueuedDecode), I, I64, I, P, I, C.POINTER(I)]),
     }
     for n, (r, a) in sig.items():
         fn = getattr(L, n)
@@ -299,6 +310,38 @@ class Policy:
         n = C.c_int64(0)
         self._ck(self._L.bh_policy_param_bytes_needed(self.h, _b(block), device, C.byref(n)))
         return n.value
+
+    # ---- proactive KV review
+    def interception_record(self, key, sample):
+        self._ck(self._L.bh_policy_interception_record(self.h, _b(key), int(sample)))
+
+    def interception_set(self, key, total, n):
+        """key None: the global accumulator."""
+        self._ck(self._L.bh_policy_interception_set(self.h, _b(key) if key is not None else None,
+                                                    float(total), int(n)))
+
+    def predicted_remaining(self, key, t_call, now):
+        out, found = C.c_int64(0), C.c_int(0)
+        self._ck(self._L.bh_policy_interception_predict(self.h, _b(key), int(t_call), int(now),
+                                                        C.byref(out), C.byref(found)))
+        return out.value if found.value else None
+
+    def kv_review(self, entries, now, recalc_only=False):
+        """entries: dicts (instance, inst_block, device, request, chain_block, owner, pages,
+        shared, pending, pending_key, t_call); returns indices to migrate, in order."""
+        arr = (_QueuedDecode * max(1, len(entries)))()
+        keep = []
+        for i, e in enumerate(entries):
+            vals = [_b(e["instance"]), _b(e["inst_block"]), e["device"], e["request"],
+                    _b(e["chain_block"]), e["owner"], e["pages"], e["shared"],
+                    int(e["pending"]), _b(e.get("pending_key") or ""), e["t_call"]]
+            keep.append(vals)
+            arr[i] = _QueuedDecode(*vals)
+        out = (C.c_int * max(1, len(entries)))()
+        n = C.c_int(0)
+        self._ck(self._L.bh_policy_kv_review(self.h, arr, len(entries), int(now),
+                                             int(recalc_only), out, len(entries), C.byref(n)))
+        return list(out[:n.value])
 
     # ---- descriptions
     @classmethod

@@ -177,3 +177,30 @@ def test_routing_prices_with_measured_profiles():
     want = n_layers * (lookup("attention:4096", 1, 512) + lookup("ffn:4096", 1, 512))
     assert abs(ch["est"][1] - want) <= 1e-9 * want
     assert ch["device"] == 0 and ch["est"][0] == 0.0
+
+
+@pytest.mark.parametrize("name", sorted(SPECS))
+def test_kv_review_matches_reference(name):
+    """Proactive KV review (§8(f) rank 1): the interception tracker's predictions and the
+    migration order over the queued decode entries with remote caches, at every snapshot, equal
+    the reference's (InterceptionTracker, order_migrations, kv_review's selection rule)."""
+    t = trace(name)
+    pol = P.Policy.from_static(t["static"])
+    for sn in t["snapshots"]:
+        pol.load_state(sn)
+        tint = sn["tint"]
+        for key, total, n in tint["keys"]:
+            pol.interception_set(key, total, n)
+        pol.interception_set(None, *tint["global"])
+        for key, t_call, want in sn.get("tint_predict", []):
+            got = pol.predicted_remaining(key, t_call, sn["now"])
+            assert (got if got is not None else -1) == want
+        got = pol.kv_review(sn["kvq"], sn["now"])
+        assert got == sn["kv_review"], sn["now"]
+
+
+def test_kv_review_sees_migrations():
+    seen = sum(len(sn["kv_review"]) for name in SPECS for sn in trace(name)["snapshots"])
+    remote = sum(1 for name in SPECS for sn in trace(name)["snapshots"] for e in sn["kvq"]
+                 if e["owner"] >= 0 and e["owner"] != e["device"])
+    assert remote > 0 and seen > 0, (remote, seen)
