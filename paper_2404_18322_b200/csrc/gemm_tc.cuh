@@ -92,10 +92,13 @@ struct GemmSmem {
 // Ring depth: up to 8 stages / ~200 KB, one CTA per SM. Measured slower: deeper rings
 // (12 x 18-24 KB), ~100 KB rings with two CTAs per SM, and ~100 KB rings leaving room for the
 // next PDL-launched GEMM beside this one.
+#ifndef BE_GEMM_RING_KB
+#define BE_GEMM_RING_KB 200  // experiments: -DBE_GEMM_RING_KB=96 leaves room for a second CTA
+#endif
 template <int BN>
 __host__ __device__ constexpr int gemm_stages_deep() {
-  const int s = (200 * 1024) / GemmSmem<BN>::kStageBytes;
-  return s > 8 ? 8 : s;
+  const int s = (BE_GEMM_RING_KB * 1024) / GemmSmem<BN>::kStageBytes;
+  return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
 
 template <int BN>
