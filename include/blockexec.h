@@ -231,6 +231,18 @@ int be_exec_lora_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_work
                            const int32_t* d_lora_idx, const void* d_arena_in, void* d_arena_out,
                            void* stream);
 
+/* Stitches: the linear map that lets a chain step of width dim_in enter an
+ * equivalent block of width dim_out (Zoo::candidate_instances, zoo.cpp:568-589; its cost is
+ * CostModel::stitch_us). y = x W^T with W [dim_out][dim_in] synthetic from stream
+ * "stitch:<name>" (scale as block weights); rows are bf16 [rows][dim]. dim_in % 64 == 0,
+ * dim_out % 128 == 0. */
+typedef struct be_stitch be_stitch;
+int be_stitch_load(be_ctx* ctx, int dim_in, int dim_out, const char* name, uint64_t seed,
+                   float scale, be_stitch** out);
+int be_stitch_free(be_stitch* s);
+int be_stitch_rows(be_ctx* ctx, const be_stitch* s, const void* d_in, int rows, void* d_out,
+                   void* stream);
+
 /* KV migration with overlapped recompute / copy (the plan is
  * plan_migration, kv.cpp:16-58, bh_plan_migration; the move is start_kv_migration,
  * scenario.cpp:361-431). A segment's n_pages pages (src_slots -> dst_slots, token order, from

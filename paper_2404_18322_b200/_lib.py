@@ -78,6 +78,9 @@ def lib() -> C.CDLL:
         "be_kv_migrate": (I, [P, P, P, P, P, P, P, I, I, I, P, P]),
         "be_lora_load": (I, [P, P, C.c_char_p, U64, F, F, PP]),
         "be_lora_free": (I, [P]),
+        "be_stitch_load": (I, [P, I, I, C.c_char_p, U64, F, PP]),
+        "be_stitch_free": (I, [P]),
+        "be_stitch_rows": (I, [P, P, P, I, P, P]),
         "be_exec_lora_batch": (I, [P, P, P, P, I, I, P, I, I, P, I, P, P, P, P, P]),
         "be_exec_lora_batch_dev": (I, [P, P, P, P, I, I, P, I, P, I, P, P, P, P, P]),
         "be_exec_batch_dev": (I, [P, P, P, P, I, I, P, I, P, P, P, P]),

@@ -1422,6 +1422,64 @@ extern "C" int be_pack_weight(be_ctx* ctx, const void* src, void* dst, int N, in
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "pack: %s", cudaGetErrorString(e));
 }
 
+// ------------------------------------------------------------------------------ stitches
+// A stitch maps activations of width dim_in to dim_out when a chain step is served by an
+// equivalent block of another width (Zoo::candidate_instances, zoo.cpp:568-589; priced by
+// CostModel::stitch_us): one linear layer, y = x W^T, W [dim_out][dim_in] synthetic from stream
+// "stitch:<name>" (same counter-mode generator as block weights), run on the tcgen05 GEMM.
+struct be_stitch {
+  be_ctx* ctx = nullptr;
+  int dim_in = 0, dim_out = 0;
+  bf16* w = nullptr;  // packed tile layout
+};
+
+extern "C" int be_stitch_load(be_ctx* ctx, int dim_in, int dim_out, const char* name,
+                              uint64_t seed, float scale, be_stitch** out) {
+  if (ctx == nullptr || name == nullptr || out == nullptr || dim_in <= 0 || dim_in % 64 != 0 ||
+      dim_out <= 0 || dim_out % 128 != 0)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_stitch_load: dims must be multiples of 64 (in) "
+                                           "and 128 (out)")
+               : BE_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  auto* s = new be_stitch();
+  s->ctx = ctx;
+  s->dim_in = dim_in;
+  s->dim_out = dim_out;
+  if (cudaMalloc(&s->w, (size_t)dim_in * dim_out * sizeof(bf16)) != cudaSuccess) {
+    delete s;
+    return fail(ctx, BE_ERR_NOMEM, "be_stitch_load: allocation failed");
+  }
+  bx::launch_synth_weight(s->w, dim_out, dim_in, stream_key(seed, std::string("stitch:") + name),
+                          0, scale, 0, 64, nullptr, ctx->stream);
+  const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(s->w);
+    delete s;
+    return fail(ctx, BE_ERR_CUDA, "be_stitch_load: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return BE_OK;
+}
+
+extern "C" int be_stitch_free(be_stitch* s) {
+  if (s == nullptr) return BE_ERR_INVALID;
+  cudaSetDevice(s->ctx->device);
+  if (s->w) cudaFree(s->w);
+  delete s;
+  return BE_OK;
+}
+
+extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out, int N, int K,
+                            int ntok, int grid_cap, void* stream);
+
+extern "C" int be_stitch_rows(be_ctx* ctx, const be_stitch* s, const void* d_in, int rows,
+                              void* d_out, void* stream) {
+  if (ctx == nullptr || s == nullptr || d_in == nullptr || d_out == nullptr || rows <= 0)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_stitch_rows: bad arguments") : BE_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  return be_gemm_bf16(ctx, s->w, d_in, d_out, s->dim_out, s->dim_in, rows, 0, stream);
+}
+
 extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out, int N, int K,
                             int ntok, int grid_cap, void* stream) {
   if (ctx == nullptr || N % 128 != 0 || K % 64 != 0 || ntok <= 0 || grid_cap < 0)

@@ -274,6 +274,29 @@ def exec_lora_batch(ctx: Context, block: "Block", pool: "KvPool", ws: "Workspace
                                    stream if stream is not None else C.c_void_p(0)), ctx.h)
 
 
+class Stitch:
+    """Width adapter between equivalent blocks of different embed dims (be_stitch_load):
+    y = x W^T, W [dim_out][dim_in] synthetic from stream "stitch:<name>"."""
+
+    def __init__(self, ctx: Context, dim_in: int, dim_out: int, name: str, seed: int = 1,
+                 scale: float = 0.02 * 3 ** 0.5):
+        self.ctx, self.dim_in, self.dim_out, self.name, self.seed, self.scale = (
+            ctx, dim_in, dim_out, name, seed, scale)
+        h = C.c_void_p()
+        check(lib().be_stitch_load(ctx.h, dim_in, dim_out, name.encode(), seed, scale,
+                                   C.byref(h)), ctx.h)
+        self.h = h
+
+    def __call__(self, x, out, stream=None) -> None:
+        check(lib().be_stitch_rows(self.ctx.h, self.h, _ptr(x), x.shape[0], _ptr(out),
+                                   stream if stream is not None else C.c_void_p(0)), self.ctx.h)
+
+    def free(self):
+        if self.h:
+            lib().be_stitch_free(self.h)
+            self.h = None
+
+
 class SpecStage(C.Structure):
     _fields_ = [("blk", C.c_void_p), ("pool", C.c_void_p), ("ws", C.c_void_p),
                 ("tokens", C.c_void_p), ("n_pt_rows", C.c_int), ("pt_stride", C.c_int),

@@ -123,3 +123,22 @@ def test_kv_copy_pages_moves_whole_pages(ctx):
     a.free()
     b.free()
     blk.free()
+
+
+@pytest.mark.parametrize("dims,rows", [((4096, 5120), 16), ((5120, 4096), 64), ((256, 512), 3)])
+def test_stitch_rows_match_fp32(ctx, dims, rows):
+    """§8(f) rank 3 stitch: y = x W^T on the tcgen05 GEMM equals the fp32 product of the same
+    synthetic W (stream "stitch:<name>") within bf16 output rounding."""
+    from oracle import oracle as O
+    din, dout = dims
+    st = dev.Stitch(ctx, din, dout, "s01", seed=5)
+    w = O.synth(din * dout, 5, "stitch:s01", st.scale).reshape(dout, din)
+    g = torch.Generator().manual_seed(2)
+    x = torch.randn(rows, din, generator=g).to(torch.bfloat16).cuda()
+    y = torch.empty(rows, dout, dtype=torch.bfloat16, device="cuda")
+    st(x, y)
+    ctx.sync()
+    ref = x.float().cpu().numpy() @ w.T
+    got = y.float().cpu().numpy()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-2
+    st.free()
