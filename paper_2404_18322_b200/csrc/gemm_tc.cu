@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(192, CTAS)
 template <int BN, int MODE>
 static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   constexpr int STAGES = gemm_stages_deep<BN>();
-  constexpr int CTAS = 1;
+  constexpr int CTAS = gemm_ctas<BN>();  // resident CTAs per SM the register budget allows
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
                        2 * BN * 4 /*rstd*/ +
                        (MODE >= kQKVLora ? BN * (kLoraRank + 1) * 4 : 0) /*LoRA u, adapters*/;

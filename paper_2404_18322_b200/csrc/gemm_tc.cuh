@@ -92,12 +92,21 @@ struct GemmSmem {
 // Ring depth: up to 8 stages / ~200 KB, one CTA per SM. Measured slower: deeper rings
 // (12 x 18-24 KB), ~100 KB rings with two CTAs per SM, and ~100 KB rings leaving room for the
 // next PDL-launched GEMM beside this one.
-#ifndef BE_GEMM_RING_KB
-#define BE_GEMM_RING_KB 200  // experiments: -DBE_GEMM_RING_KB=96 leaves room for a second CTA
+#ifndef BE_GEMM_CTAS
+#define BE_GEMM_CTAS 1  // experiments: 2 (with a <= 100 KB ring) lets the next PDL launch co-reside
 #endif
+#ifndef BE_GEMM_RING_KB
+#define BE_GEMM_RING_KB 96  // ring of a CTA that shares its SM (BE_GEMM_CTAS = 2)
+#endif
+// resident CTAs per SM for a tile width: the co-residency experiment covers the decode widths
+template <int BN>
+__host__ __device__ constexpr int gemm_ctas() {
+  return BN <= 64 ? BE_GEMM_CTAS : 1;
+}
 template <int BN>
 __host__ __device__ constexpr int gemm_stages_deep() {
-  const int s = (BE_GEMM_RING_KB * 1024) / GemmSmem<BN>::kStageBytes;
+  const int ring_kb = gemm_ctas<BN>() > 1 ? BE_GEMM_RING_KB : 200;
+  const int s = (ring_kb * 1024) / GemmSmem<BN>::kStageBytes;
   return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
 
