@@ -619,7 +619,8 @@ def run_ours(args, world, rank, local):
             "synthetic prompt embeddings; greedy feedback of the last hidden state)",
             "config": {"workload": wl.name, "model": {"c2": "Llama-2-7B-shaped", "c3": "Llama-2-7B-shaped",
                                  "c4": "Llama-2-13B-shaped",
-                                 "c5": "Llama-2-7B-shaped"}.get(args.config, wl.name), "tenants": len(wl.chains), "global_batch": n_live * world,
+                                 "c5": "Llama-2-7B-shaped",
+                                 "c2lora": "Llama-2-7B-shaped + rank-16 LoRA tenants"}.get(args.config, wl.name), "tenants": len(wl.chains), "global_batch": n_live * world,
                        "prompt": wl.req_prompt[0], "decode": wl.req_output[0],
                        "blocks": f"{len(wl.block_names)} blocks x {wl.shape.n_layers} layers",
                        "rows_per_block": wl.rows_at_block(), "batches_per_step": nb,
@@ -691,7 +692,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c2lora"])
     ap.add_argument("--prompt", type=int, default=None, help="default: the config's own")
     ap.add_argument("--output", type=int, default=None, help="default: the config's own")
     ap.add_argument("--no-e2e", action="store_true")

@@ -224,6 +224,14 @@ int be_exec_lora_batch(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspac
                        const int32_t* page_table, int n_lora, const be_lora* const* loras,
                        const int32_t* lora_idx, const void* d_arena_in, void* d_arena_out,
                        void* stream);
+/* LoRA variants of ONE base block at a chain position in one launch: group g's rows (n_tokens /
+ * n_blocks, padded as be_exec_group_dev) keep their own KV pool pools[g]; blks[g] must all be
+ * the base block (its weights stream once for every row); d_lora_idx picks each row's adapter. */
+int be_exec_lora_group_dev(be_ctx* ctx, int n_blocks, be_block* const* blks,
+                           be_kv_pool* const* pools, be_workspace* ws, int phase, int n_tokens,
+                           const be_token* d_tokens, int pt_stride, const int32_t* d_page_table,
+                           int n_lora, const be_lora* const* loras, const int32_t* d_lora_idx,
+                           const void* d_arena_in, void* d_arena_out, void* stream);
 /* Same with every per-token array already on the device (graph-capturable). */
 int be_exec_lora_batch_dev(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* ws,
                            int phase, int n_tokens, const be_token* d_tokens, int pt_stride,

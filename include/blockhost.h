@@ -108,6 +108,11 @@ typedef struct {
   int plan_ahead;              /* 1: bh_runner_decode_step plans step k+1 on the host while step
                                   k runs on the device (hides host bookkeeping behind the GPU);
                                   the request counters then run one step ahead */
+  const int32_t* block_lora_base;     /* NULL, or [n_blocks]: the block whose weights a LoRA
+                                         variant shares (-1: a block with its own weights) */
+  const char* const* block_lora_name; /* [n_blocks] adapter names of the LoRA variants
+                                         (be_lora_load); LoRA variants of one base at a chain
+                                         position decode in one launch (be_exec_lora_group_dev) */
 } bh_workload;
 
 typedef struct {

@@ -756,6 +756,7 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
 
 // One batch of one block, or a grouped batch of n_grp independent blocks of one shape whose
 // token rows sit side by side in groups of grp_rows = ntok / n_grp (one GEMM n-tile each).
+int check_loras(be_ctx* ctx, const be_block* blk, int n_lora, const be_lora* const* loras);
 // Adapters of one launch: token t uses loras[idx[t]] (idx on the device, -1 = base block only)
 struct LoraSet {
   int n = 0;
@@ -781,7 +782,10 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
   if (ntok == 0) return BE_OK;
   const int* tok = reinterpret_cast<const int*>(d_tok);
   const int grp_rows = n_grp > 1 ? ntok / n_grp : ntok;
-  const int bn = n_grp > 1 ? grp_rows : bx::gemm_pick_bn(ntok);
+  // grouped blocks stream their own weights per n-tile (BN = rows per block); LoRA variants of one
+  // base share its weights, so their rows form one matrix streamed once
+  const int bn = n_grp > 1 && lora == nullptr ? grp_rows : bx::gemm_pick_bn(ntok);
+  const int wcopies = lora != nullptr ? 1 : n_grp;  // weight streams per GEMM (byte accounting)
   if (n_grp > 1) {
     if (n_grp > bx::kMaxGroup || ntok % n_grp != 0 || (grp_rows != 16 && grp_rows != 32 && grp_rows != 64))
       return fail(ctx, BE_ERR_INVALID, "grouped batch: %d blocks x %d rows unsupported", n_grp, grp_rows);
@@ -848,7 +852,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
       {
         eg.tl = tl_slot(ctx, BE_K_GEMM_GATE_UP);
         eg.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_GATE_UP, ntok, 2 * F, d, gemm_bytes(2 * F, d, ntok) + 2.0 * (n_grp - 1) * (2 * F) * (d),
+        ProfScope ps(ctx, st, BE_K_GEMM_GATE_UP, ntok, 2 * F, d, gemm_bytes(2 * F, d, ntok) + 2.0 * (wcopies - 1) * (2 * F) * (d),
                      2.0 * (2 * F) * (d) * ntok);
         rc = run_gemm(ctx, ws, L.wgu, &ws->m_xb[bn], 2 * F, d, ntok, bn, eg, st);
       }
@@ -866,7 +870,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
       {
         ed.tl = tl_slot(ctx, BE_K_GEMM_DOWN);
         ed.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F, gemm_bytes(d, F, ntok) + 2.0 * (n_grp - 1) * (d) * (F),
+        ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F, gemm_bytes(d, F, ntok) + 2.0 * (wcopies - 1) * (d) * (F),
                      2.0 * (d) * (F) * ntok);
         rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st);
       }
@@ -913,7 +917,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     {
       eq.tl = tl_slot(ctx, BE_K_GEMM_QKV);
         eq.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_QKV, ntok, 3 * d, d, gemm_bytes(3 * d, d, ntok) + 2.0 * (n_grp - 1) * (3 * d) * (d),
+        ProfScope ps(ctx, st, BE_K_GEMM_QKV, ntok, 3 * d, d, gemm_bytes(3 * d, d, ntok) + 2.0 * (wcopies - 1) * (3 * d) * (d),
                      2.0 * (3 * d) * (d) * ntok);
       rc = run_gemm(ctx, ws, L.wqkv, &ws->m_xb[bn], 3 * d, d, ntok, bn, eq, st);
     }
@@ -996,7 +1000,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     {
       eo.tl = tl_slot(ctx, BE_K_GEMM_O);
         eo.tl_cap = ctx->tl_cap;
-        ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d, gemm_bytes(d, d, ntok) + 2.0 * (n_grp - 1) * (d) * (d),
+        ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d, gemm_bytes(d, d, ntok) + 2.0 * (wcopies - 1) * (d) * (d),
                      2.0 * (d) * (d) * ntok);
       rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st);
     }
@@ -1039,6 +1043,28 @@ extern "C" int be_exec_group_dev(be_ctx* ctx, int n_blocks, be_block* const* blk
     return fail(ctx, BE_ERR_INVALID, "unknown phase %d", phase);
   return exec_dev(ctx, n_blocks, blks, pools, ws, phase, n_tokens, d_tokens, pt_stride,
                   d_page_table, d_arena_in, d_arena_out, pick_stream(ctx, stream));
+}
+
+extern "C" int be_exec_lora_group_dev(be_ctx* ctx, int n_blocks, be_block* const* blks,
+                                      be_kv_pool* const* pools, be_workspace* ws, int phase,
+                                      int n_tokens, const be_token* d_tokens, int pt_stride,
+                                      const int32_t* d_page_table, int n_lora,
+                                      const be_lora* const* loras, const int32_t* d_lora_idx,
+                                      const void* d_arena_in, void* d_arena_out, void* stream) {
+  if (ctx == nullptr || n_blocks < 1 || blks == nullptr || pools == nullptr || ws == nullptr ||
+      n_tokens <= 0 || d_tokens == nullptr || d_page_table == nullptr || d_lora_idx == nullptr ||
+      d_arena_in == nullptr || d_arena_out == nullptr || pt_stride <= 0)
+    return ctx ? fail(ctx, BE_ERR_INVALID, "be_exec_lora_group_dev: bad arguments") : BE_ERR_INVALID;
+  for (int g = 0; g < n_blocks; ++g)
+    if (blks[g] == nullptr || pools[g] == nullptr || blks[g] != blks[0])
+      return fail(ctx, BE_ERR_INVALID, "be_exec_lora_group_dev: the groups must share one base block");
+  int rc = check_loras(ctx, blks[0], n_lora, loras);
+  if (rc != BE_OK) return rc;
+  if (phase != BE_PHASE_PREFILL && phase != BE_PHASE_DECODE)
+    return fail(ctx, BE_ERR_INVALID, "unknown phase %d", phase);
+  LoraSet set{n_lora, loras, d_lora_idx};
+  return exec_dev(ctx, n_blocks, blks, pools, ws, phase, n_tokens, d_tokens, pt_stride,
+                  d_page_table, d_arena_in, d_arena_out, pick_stream(ctx, stream), &set);
 }
 
 namespace {

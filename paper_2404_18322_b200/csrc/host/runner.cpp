@@ -116,6 +116,16 @@ class Runner {
   std::vector<be_block_desc> descs_;
   std::vector<std::string> names_;
   std::vector<be_block*> blocks_;
+  // LoRA variants: base block index (-1: own weights), adapters, which blocks_ entries we own
+  std::vector<int> lora_base_;
+  std::vector<be_lora*> loras_;
+  std::vector<char> own_block_;
+  int32_t* d_zero_idx_ = nullptr;  // adapter index 0 for every row of a single-variant launch
+  int wbase(int b) const { return lora_base_[b] >= 0 ? lora_base_[b] : b; }
+  // a LoRA launch adds two shrink kernels per attention component
+  int lora_launches(int b) const {
+    return lora_base_[b] >= 0 ? 2 * (int)(kv_bpt_[b] / (4LL * d_)) : 0;  // n_att from KV bytes
+  }
   std::vector<be_kv_pool*> pools_;
   std::vector<int> chain_ptr_, chain_blocks_;
   std::vector<Request> reqs_;
@@ -142,6 +152,8 @@ class Runner {
     std::vector<be_token> toks;  // grouped: concatenated, page-table rows renumbered
     std::vector<int32_t> pt;
     int stride = 1;
+    bool lora = false;           // LoRA variants of one base: one weight stream, per-row adapters
+    std::vector<int32_t> lidx;   // lora: adapter slot per token (group index, -1 = the base)
   };
   std::vector<LaunchEntry> group_plans(const std::vector<PlannedBatch>& plans) const;
   // one planned decode step: host bookkeeping done, metadata laid out, nothing on the device yet
@@ -151,7 +163,7 @@ class Runner {
     std::vector<int> rows;  // live requests of the step, request order (host row order)
     std::vector<PlannedBatch> plans;
     std::vector<LaunchEntry> entries;
-    std::vector<size_t> off_tok, off_pt;
+    std::vector<size_t> off_tok, off_pt, off_idx;
     size_t total = 0;
     std::vector<std::tuple<int, int, int>> sig;
     bh_step_stats stats{};
@@ -162,7 +174,7 @@ class Runner {
   StepPlan pending_;
   void copy_host_rows(const std::vector<int>& rows, bool to_dev, void* host);
   void launch_entry(const std::vector<PlannedBatch>& plans, const LaunchEntry& le,
-                    const be_token* d_tok, const int32_t* d_pt);
+                    const be_token* d_tok, const int32_t* d_pt, const int32_t* d_idx);
   struct GraphSlot {
     std::vector<std::tuple<int, int, int>> sig;  // (block, n_tokens, stride*16+n) per launch
     cudaGraphExec_t exec = nullptr;
@@ -233,6 +245,22 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
       pages_needed[chain_blocks_[s]] += pages_for(total) + 1;
     reqs_.push_back(r);
   }
+  lora_base_.assign(w.n_blocks, -1);
+  if (w.block_lora_base != nullptr) {
+    for (int b = 0; b < w.n_blocks; ++b) {
+      const int base = w.block_lora_base[b];
+      if (base < -1 || base >= w.n_blocks || base == b ||
+          (base >= 0 && (w.block_lora_base[base] >= 0 || w.block_lora_name == nullptr ||
+                         w.block_lora_name[b] == nullptr)))
+        throw BeError(BE_ERR_INVALID, "runner: bad LoRA base for block " + std::to_string(b));
+      lora_base_[b] = base;
+    }
+  }
+  blocks_.assign(w.n_blocks, nullptr);
+  pools_.assign(w.n_blocks, nullptr);
+  loras_.assign(w.n_blocks, nullptr);
+  own_block_.assign(w.n_blocks, 0);
+  std::vector<int> np_of(w.n_blocks, 1);
   int dff = 0, H = 0;
   for (int b = 0; b < w.n_blocks; ++b) {
     // component sequence -> KV bytes per token (4 * d per attention component,
@@ -256,18 +284,33 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
     } else if (dff != descs_[b].d_ff || H != descs_[b].n_heads) {
       throw BeError(BE_ERR_INVALID, "runner: blocks differ in d_ff / heads");
     }
-    if (dry_) continue;
+    np_of[b] = np;
+    if (dry_ || lora_base_[b] >= 0) continue;  // LoRA variants: after their base is loaded
     be_block_desc d = descs_[b];
     d.name = names_[b].c_str();
     d.components = comps_[b].empty() ? nullptr : comps_[b].c_str();
     be_block* blk = nullptr;
     int rc = be_block_load(ctx, &d, &blk);
     if (rc != BE_OK) throw BeError(rc, std::string("block load: ") + be_last_error(ctx));
-    blocks_.push_back(blk);
+    blocks_[b] = blk;
+    own_block_[b] = 1;
     be_kv_pool* kp = nullptr;
     rc = be_kv_pool_create(ctx, blk, np, &kp);
     if (rc != BE_OK) throw BeError(rc, std::string("kv pool: ") + be_last_error(ctx));
-    pools_.push_back(kp);
+    pools_[b] = kp;
+  }
+  // LoRA variants: the base's weights, their own adapter and KV pool
+  for (int b = 0; b < w.n_blocks && !dry_; ++b) {
+    const int base = lora_base_[b];
+    if (base < 0) continue;
+    if (comps_[b] != comps_[base] || descs_[b].d_ff != descs_[base].d_ff)
+      throw BeError(BE_ERR_INVALID, "runner: a LoRA variant must have its base's shape");
+    blocks_[b] = blocks_[base];
+    int rc = be_lora_load(ctx, blocks_[base], w.block_lora_name[b], w.seed, descs_[b].init_scale,
+                          descs_[b].init_scale, &loras_[b]);
+    if (rc != BE_OK) throw BeError(rc, std::string("lora load: ") + be_last_error(ctx));
+    rc = be_kv_pool_create(ctx, blocks_[base], np_of[b], &pools_[b]);
+    if (rc != BE_OK) throw BeError(rc, std::string("kv pool: ") + be_last_error(ctx));
   }
   inst_of_block_.assign(w.n_blocks, "");
   inst_index_.assign(w.n_blocks, -1);
@@ -276,6 +319,10 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   const int max_tok = std::max(std::min(poff, std::max(max_batch_tokens_, max_prompt)), w.n_requests);
   int rc = be_workspace_create(ctx, d_, dff, H, max_tok, w.n_requests, pages_for(max_ctx_) + 1, &ws_);
   if (rc != BE_OK) throw BeError(rc, std::string("workspace: ") + be_last_error(ctx));
+  if (std::any_of(lora_base_.begin(), lora_base_.end(), [](int x) { return x >= 0; })) {
+    ck(cudaMalloc(&d_zero_idx_, (size_t)max_tok * sizeof(int32_t)), "lora idx");
+    ck(cudaMemsetAsync(d_zero_idx_, 0, (size_t)max_tok * sizeof(int32_t), st_), "lora idx");
+  }
   ck(cudaMalloc(&arena_, (size_t)w.n_requests * d_ * 2), "arena");
   ck(cudaMalloc(&parena_, (size_t)poff * d_ * 2), "prefill arena");
   prefill_rows_ = poff;
@@ -300,7 +347,11 @@ Runner::~Runner() {
   if (parena_) cudaFree(parena_);
   if (ws_) be_workspace_free(ws_);
   for (auto* p : pools_) be_kv_pool_free(p);
-  for (auto* b : blocks_) be_block_free(b);
+  for (size_t b = 0; b < blocks_.size(); ++b)
+    if (own_block_[b] && blocks_[b]) be_block_free(blocks_[b]);
+  for (auto* l : loras_)
+    if (l) be_lora_free(l);
+  if (d_zero_idx_) cudaFree(d_zero_idx_);
 }
 
 int Runner::live() const {
@@ -380,6 +431,16 @@ PlannedBatch Runner::plan(const std::string& inst_id, const Batch& b) {
 
 void Runner::launch(const PlannedBatch& pb, const be_token* d_tok, const int32_t* d_pt) {
   void* arena = pb.phase == Phase::kPrefill ? parena_ : arena_;
+  if (loras_[pb.block] != nullptr) {
+    const be_lora* l = loras_[pb.block];
+    const int rc = be_exec_lora_batch_dev(
+        ctx_, blocks_[pb.block], pools_[pb.block], ws_,
+        pb.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE,
+        static_cast<int>(pb.toks.size()), d_tok, pb.stride, d_pt, 1, &l, d_zero_idx_, arena, arena,
+        st_);
+    if (rc != BE_OK) throw BeError(rc, std::string("exec lora: ") + be_last_error(ctx_));
+    return;
+  }
   const int rc = be_exec_batch_dev(ctx_, blocks_[pb.block], pools_[pb.block], ws_,
                                    pb.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE,
                                    static_cast<int>(pb.toks.size()), d_tok, pb.stride, d_pt, arena,
@@ -390,6 +451,17 @@ void Runner::launch(const PlannedBatch& pb, const be_token* d_tok, const int32_t
 void Runner::execute_direct(const PlannedBatch& pb) {
   if (dry_) return;
   void* arena = pb.phase == Phase::kPrefill ? parena_ : arena_;
+  if (loras_[pb.block] != nullptr) {
+    const be_lora* l = loras_[pb.block];
+    const std::vector<int32_t> zeros(pb.toks.size(), 0);
+    const int rc = be_exec_lora_batch(ctx_, blocks_[pb.block], pools_[pb.block], ws_,
+                                      pb.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE,
+                                      static_cast<int>(pb.toks.size()), pb.toks.data(), pb.n_rows,
+                                      pb.stride, pb.pt.data(), 1, &l, zeros.data(), arena, arena, st_);
+    if (rc != BE_OK) throw BeError(rc, std::string("exec lora: ") + be_last_error(ctx_));
+    ck(cudaStreamSynchronize(st_), "batch");
+    return;
+  }
   const int rc = be_exec_batch(ctx_, blocks_[pb.block], pools_[pb.block], ws_,
                                pb.phase == Phase::kPrefill ? BE_PHASE_PREFILL : BE_PHASE_DECODE,
                                static_cast<int>(pb.toks.size()), pb.toks.data(), pb.n_rows,
@@ -429,7 +501,8 @@ void Runner::account(const PlannedBatch& pb) {
   stats.flops += 2.0 * n * (La * 4.0 * d * d + Lf * 3.0 * d * F) + 4.0 * ctx_sum * d * La;
   if (!dry_)
     stats.launches += be_exec_batch_launches(ctx_, blocks_[pb.block],
-                                             static_cast<int>(pb.toks.size()), pb.stride);
+                                             static_cast<int>(pb.toks.size()), pb.stride) +
+                      lora_launches(pb.block);
 }
 
 void Runner::pump() {
@@ -557,6 +630,9 @@ std::vector<Runner::LaunchEntry> Runner::group_plans(const std::vector<PlannedBa
       if (b.phase != Phase::kDecode || b.toks.size() > 64 || comps_[b.block] != comps_[a.block] ||
           descs_[b.block].d_ff != descs_[a.block].d_ff || b.block == a.block)
         break;
+      // LoRA variants group only with variants of the same base (one shared weight stream)
+      const bool la = lora_base_[a.block] >= 0, lb = lora_base_[b.block] >= 0;
+      if ((la || lb) && wbase(a.block) != wbase(b.block)) break;
       bool disjoint = true;
       for (const auto& t : b.toks)
         if (std::find(seen.begin(), seen.end(), t.src_row) != seen.end()) disjoint = false;
@@ -592,6 +668,12 @@ std::vector<Runner::LaunchEntry> Runner::group_plans(const std::vector<PlannedBa
             le.pt.push_back(c < pb.stride ? pb.pt[(size_t)r * pb.stride + c] : -1);
         row0 += pb.n_rows;
       }
+      for (int k : le.plans) le.lora = le.lora || lora_base_[plans[k].block] >= 0;
+      if (le.lora)
+        for (size_t g = 0; g < le.plans.size(); ++g)
+          for (size_t p = 0; p < R; ++p)
+            le.lidx.push_back(lora_base_[plans[le.plans[g]].block] >= 0 && p < plans[le.plans[g]].toks.size()
+                                  ? static_cast<int32_t>(g) : -1);
     }
     out.push_back(std::move(le));
     i = j;
@@ -600,7 +682,7 @@ std::vector<Runner::LaunchEntry> Runner::group_plans(const std::vector<PlannedBa
 }
 
 void Runner::launch_entry(const std::vector<PlannedBatch>& plans, const LaunchEntry& le,
-                          const be_token* d_tok, const int32_t* d_pt) {
+                          const be_token* d_tok, const int32_t* d_pt, const int32_t* d_idx) {
   if (le.plans.size() == 1) {
     launch(plans[le.plans[0]], d_tok, d_pt);
     return;
@@ -610,6 +692,23 @@ void Runner::launch_entry(const std::vector<PlannedBatch>& plans, const LaunchEn
   for (size_t g = 0; g < le.plans.size(); ++g) {
     blks[g] = blocks_[plans[le.plans[g]].block];
     pls[g] = pools_[plans[le.plans[g]].block];
+  }
+  if (le.lora) {
+    // adapter slot g = group g's variant (a group of the base itself keeps index -1)
+    const be_lora* ls[8];
+    const be_lora* any = nullptr;
+    for (size_t g = 0; g < le.plans.size(); ++g)
+      if (loras_[plans[le.plans[g]].block]) any = loras_[plans[le.plans[g]].block];
+    for (size_t g = 0; g < le.plans.size(); ++g) {
+      const be_lora* l = loras_[plans[le.plans[g]].block];
+      ls[g] = l ? l : any;
+    }
+    const int rc = be_exec_lora_group_dev(
+        ctx_, static_cast<int>(le.plans.size()), blks, pls, ws_, BE_PHASE_DECODE,
+        static_cast<int>(le.toks.size()), d_tok, le.stride, d_pt,
+        static_cast<int>(le.plans.size()), ls, d_idx, arena_, arena_, st_);
+    if (rc != BE_OK) throw BeError(rc, std::string("exec lora group: ") + be_last_error(ctx_));
+    return;
   }
   const int rc = be_exec_group_dev(ctx_, static_cast<int>(le.plans.size()), blks, pls, ws_,
                                    BE_PHASE_DECODE, static_cast<int>(le.toks.size()), d_tok,
@@ -666,14 +765,33 @@ Runner::StepPlan Runner::plan_step(int group, const std::vector<int>* members) {
     sp.stats.launches = 0;
     for (const auto& le : sp.entries) {
       const PlannedBatch& p0 = plans[le.plans[0]];
+      int lora_extra = 0;
+      for (int k : le.plans) lora_extra = std::max(lora_extra, lora_launches(plans[k].block));
       sp.stats.launches += be_exec_batch_launches(ctx_, blocks_[p0.block],
                                                   static_cast<int>(ent_toks(le).size()),
-                                                  le.plans.size() == 1 ? p0.stride : le.stride);
+                                                  le.plans.size() == 1 ? p0.stride : le.stride) +
+                           lora_extra;
     }
+  }
+  // LoRA groups stream the shared base weights once (account() charged every variant), plus
+  // each variant's adapter factors (8 r d bf16 per attention component)
+  for (const auto& le : sp.entries) {
+    if (!le.lora) continue;
+    const PlannedBatch& p0 = plans[le.plans[0]];
+    const be_block_desc& D = descs_[p0.block];
+    const double d = D.d_model, F = D.d_ff;
+    const double La = static_cast<double>(kv_bpt_[p0.block]) / (4.0 * d);
+    const double Lf = comps_[p0.block].empty() ? D.n_layers
+                                               : static_cast<double>(comps_[p0.block].size()) - La;
+    const double w = 2.0 * (La * 4.0 * d * d + Lf * 3.0 * d * F);
+    const double g = static_cast<double>(le.plans.size());
+    sp.stats.weight_bytes -= (g - 1.0) * w;
+    sp.stats.weight_bytes += g * La * 8.0 * 16.0 * d * 2.0;
   }
   // metadata layout: per launch [tokens][page table], 256-byte aligned
   sp.off_tok.resize(sp.entries.size());
   sp.off_pt.resize(sp.entries.size());
+  sp.off_idx.resize(sp.entries.size());
   for (size_t i = 0; i < sp.entries.size(); ++i) {
     const LaunchEntry& le = sp.entries[i];
     const auto& tk = ent_toks(le);
@@ -682,6 +800,8 @@ Runner::StepPlan Runner::plan_step(int group, const std::vector<int>* members) {
     sp.total += (tk.size() * sizeof(be_token) + 255) & ~size_t(255);
     sp.off_pt[i] = sp.total;
     sp.total += (pt.size() * sizeof(int32_t) + 255) & ~size_t(255);
+    sp.off_idx[i] = sp.total;  // LoRA groups: adapter slot per token
+    sp.total += (le.lidx.size() * sizeof(int32_t) + 255) & ~size_t(255);
     const int stride = le.plans.size() == 1 ? plans[le.plans[0]].stride : le.stride;
     sp.sig.emplace_back(plans[le.plans[0]].block, static_cast<int>(tk.size()),
                         stride * 16 + static_cast<int>(le.plans.size()));
@@ -720,13 +840,16 @@ void Runner::stage_and_launch(StepPlan& sp, const void* host_in) {
     const auto& pt = le.plans.size() == 1 ? plans[le.plans[0]].pt : le.pt;
     std::memcpy(stage + sp.off_tok[i], tk.data(), tk.size() * sizeof(be_token));
     std::memcpy(stage + sp.off_pt[i], pt.data(), pt.size() * sizeof(int32_t));
+    if (!le.lidx.empty())
+      std::memcpy(stage + sp.off_idx[i], le.lidx.data(), le.lidx.size() * sizeof(int32_t));
   }
   ck(cudaMemcpyAsync(meta_dev_, stage, sp.total, cudaMemcpyHostToDevice, st_), "meta h2d");
   ck(cudaEventRecord(meta_ev_[slot], st_), "meta ev record");
   auto launch_all = [&]() {
     for (size_t i = 0; i < entries.size(); ++i)
       launch_entry(plans, entries[i], reinterpret_cast<const be_token*>(meta_dev_ + sp.off_tok[i]),
-                   reinterpret_cast<const int32_t*>(meta_dev_ + sp.off_pt[i]));
+                   reinterpret_cast<const int32_t*>(meta_dev_ + sp.off_pt[i]),
+                   reinterpret_cast<const int32_t*>(meta_dev_ + sp.off_idx[i]));
   };
   stats = sp.stats;
   stats.graph_replayed = 0;

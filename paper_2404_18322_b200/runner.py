@@ -27,7 +27,8 @@ class WorkloadC(C.Structure):
                 ("n_requests", C.c_int), ("req_tenant", C.c_void_p),
                 ("req_prompt", C.c_void_p), ("req_output", C.c_void_p),
                 ("max_batch_tokens", C.c_int), ("mode", C.c_int), ("use_graphs", C.c_int),
-                ("seed", C.c_uint64), ("dry_run", C.c_int), ("plan_ahead", C.c_int)]
+                ("seed", C.c_uint64), ("dry_run", C.c_int), ("plan_ahead", C.c_int),
+                ("block_lora_base", C.c_void_p), ("block_lora_name", C.c_void_p)]
 
 
 _bound = False
@@ -89,11 +90,18 @@ class Runner:
                       np.array(wl.req_tenant, np.int32), np.array(wl.req_prompt, np.int32),
                       np.array(wl.req_output, np.int32)]
         k = self._keep
+        lora_base, lora_names = None, None
+        if getattr(wl, "block_lora", None):
+            base = np.array([-1 if x is None else x[0] for x in wl.block_lora], np.int32)
+            names = (C.c_char_p * len(wl.block_lora))(
+                *[None if x is None else x[1].encode() for x in wl.block_lora])
+            self._keep += [base, names]
+            lora_base, lora_names = base.ctypes.data, C.cast(names, C.c_void_p)
         w = WorkloadC(len(wl.block_names), C.cast(descs, C.c_void_p), len(wl.chains),
                       k[1].ctypes.data, k[2].ctypes.data, wl.n_requests, k[3].ctypes.data,
                       k[4].ctypes.data, k[5].ctypes.data, wl.max_batch_tokens, mode,
                       1 if use_graphs else 0, wl.seed, 1 if dry_run else 0,
-                      1 if plan_ahead else 0)
+                      1 if plan_ahead else 0, lora_base, lora_names)
         h = C.c_void_p()
         rc = lib().bh_runner_create(ctx.h if ctx is not None else None, C.byref(w), C.byref(h))
         if rc != 0:

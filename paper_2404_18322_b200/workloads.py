@@ -25,6 +25,9 @@ class Workload:
     seed: int = 1
     notes: dict = field(default_factory=dict)
     block_comps: list[str] | None = None  # per block 'a'/'f' component sequence (zoo blocks)
+    # per block: None, or (base block index, adapter name) for a LoRA variant that shares the
+    # base's weights (the reference zoo's fused attention, attach "fuse"; gen_configs.py:88-106)
+    block_lora: list | None = None
 
     @property
     def n_requests(self) -> int:
@@ -103,5 +106,37 @@ def c5_llama7b_8tenant(prompt: int = 512, output: int = 128) -> Workload:
                              max_batch_tokens=8192)
 
 
+def lora_variant(wl: Workload, name: str) -> Workload:
+    """The same zoo with every tenant-private block made a rank-16 LoRA variant of one shared
+    base block per chain position (the base's weights + the tenant's adapter): the reference's
+    LoRA models whose fused attention layers are their own blocks. Private positions then decode
+    in one launch per position that streams the base weights once (be_exec_lora_group_dev)."""
+    import dataclasses
+    names = list(wl.block_names)
+    comps = list(wl.block_comps) if wl.block_comps else None
+    lora = [None] * len(names)
+    base_of = {}
+    shared = set.intersection(*[set(c) for c in wl.chains]) if len(wl.chains) > 1 else set()
+    for t, ch in enumerate(wl.chains):
+        for p, b in enumerate(ch):
+            if b in shared:
+                continue
+            if p not in base_of:
+                base_of[p] = len(names)
+                names.append(f"base.b{p}")
+                lora.append(None)
+                if comps is not None:
+                    comps.append(comps[b])
+            lora[b] = (base_of[p], f"t{t}.p{p}")
+    return dataclasses.replace(wl, name=name, block_names=names, block_comps=comps,
+                               block_lora=lora)
+
+
+def c2_lora(prompt: int = 512, output: int = 128) -> Workload:
+    """C2 with the tenants' private blocks as LoRA variants of shared base blocks (not a BASELINE
+    config: the multi-tenant adapter path of SURVEY §8(f) rank 3, measured beside C2)."""
+    return lora_variant(c2_llama7b(prompt, output), "c2-lora-llama7b-4tenant")
+
+
 CONFIGS = {"c1": c1_tiny, "c2": c2_llama7b, "c3": c3_llama7b_16tenant, "c4": c4_llama13b,
-           "c5": c5_llama7b_8tenant}
+           "c5": c5_llama7b_8tenant, "c2lora": c2_lora}

@@ -24,7 +24,14 @@ def oracle_chain(wl, n_steps, gpu_inputs):
     """Runs the oracle over the workload; gpu_inputs[k] = GPU input rows of decode step k."""
     from oracle import oracle as O
     s = wl.shape
-    blocks = {b: O.OracleBlock(s, name, seed=wl.seed) for b, name in enumerate(wl.block_names)}
+    blocks = {}
+    lora = getattr(wl, "block_lora", None) or [None] * len(wl.block_names)
+    for b, name in enumerate(wl.block_names):
+        if lora[b] is None:
+            blocks[b] = O.OracleBlock(s, name, seed=wl.seed)
+        else:  # LoRA variant: the base's weights with the adapter folded in
+            blocks[b] = O.OracleBlock(s, wl.block_names[lora[b][0]], seed=wl.seed)
+            blocks[b].add_lora(lora[b][1], wl.seed, s.init_scale, s.init_scale)
     max_tok = max(p + o for p, o in zip(wl.req_prompt, wl.req_output)) + 1
     seqs = {}
     first = []
@@ -86,4 +93,32 @@ def test_c1_lockstep_trace_is_convoy(ctx):
     assert [m[0] for m in tr[1][3]] == [1, 3, 5, 7]  # tenant 0 requests (round-robin arrivals)
     assert [m[0] for m in tr[2][3]] == [2, 4, 6, 8]
     assert all(m[2] == 17 for m in tr[0][3])  # context = prompt + first token
+    run.close()
+
+
+def test_c1_lora_runner_matches_oracle(ctx):
+    """The executor loop with LoRA variants (workloads.lora_variant): the tenants' private
+    blocks share one base block's weights plus their own rank-16 adapters; prefill runs each
+    variant alone, decode runs both variants in one launch (be_exec_lora_group_dev). Same
+    oracle comparison as the full-weight C1 test, the oracle folding each adapter into W."""
+    from paper_2404_18322_b200.workloads import lora_variant
+    wl = lora_variant(c1_tiny(output=6), "c1-lora")
+    run = Runner(ctx, wl, mode=1, use_graphs=True)
+    run.run()
+    n, d = wl.n_requests, wl.shape.d_model
+    outs = []
+    buf = torch.empty(n, d, dtype=torch.bfloat16)
+    for k in range(5):
+        run.decode_step(None, buf)
+        outs.append(buf.float().numpy().copy())
+    first_ref, _ = oracle_chain(wl, 0, [])
+    ins = [first_ref] + outs[:-1]
+    _, ref = oracle_chain(wl, 5, ins)
+    for k in range(1, 5):
+        g, r = outs[k], ref[k]
+        rel = np.linalg.norm(g - r) / np.linalg.norm(r)
+        cos = ((g * r).sum(1) / np.linalg.norm(g, axis=1) / np.linalg.norm(r, axis=1)).min()
+        assert rel <= 2e-2 and cos >= 0.995, (k, rel, cos)
+    st = run.step_stats()
+    assert st["graph_replayed"] == 1
     run.close()
