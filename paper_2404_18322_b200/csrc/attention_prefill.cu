@@ -94,6 +94,16 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// B fragments of two 8x8 bf16 tiles stacked along k, from a row-major [k][n] smem tile:
+// lanes 0-15 address rows k0..k0+15 (16-byte aligned), .trans hands thread (g, t) the pairs
+// (k = 2t, 2t+1 | n = g) of each tile - the m16n8k16 "col" operand.
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t& b0, uint32_t& b1, const void* row) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(row));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+               : "=r"(b0), "=r"(b1)
+               : "r"(a));
+}
+
 template <int HD>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) {
   constexpr int BR = 64, BC = 64;
@@ -234,10 +244,8 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) 
         o[j][3] *= cb;
 #pragma unroll
         for (int kk = 0; kk < BC / 16; ++kk) {
-          const int kr = kk * 16 + 2 * t, n = j * 8 + g;
-          const uint32_t b0 = pack2(__bfloat162float(sV[kr][n]), __bfloat162float(sV[kr + 1][n]));
-          const uint32_t b1 =
-              pack2(__bfloat162float(sV[kr + 8][n]), __bfloat162float(sV[kr + 9][n]));
+          uint32_t b0, b1;
+          ldsm_x2_trans(b0, b1, &sV[kk * 16 + (lane & 15)][j * 8]);
           mma16816(o[j], pf[kk], b0, b1);
         }
       }
