@@ -104,13 +104,24 @@ __device__ __forceinline__ void ldsm_x2_trans(uint32_t& b0, uint32_t& b1, const 
                : "r"(a));
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem),
+               "r"(valid ? 16 : 0));  // src-size 0: zero fill
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
 template <int HD>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) {
   constexpr int BR = 64, BC = 64;
   constexpr int LD = HD + 8;  // padded smem row (bf16): conflict-free fragment loads
   constexpr int KS = HD / 16; // k-steps over the head dim
-  __shared__ __align__(16) __nv_bfloat16 sK[BC][LD];
-  __shared__ __align__(16) __nv_bfloat16 sV[BC][LD];
+  // K/V tiles double-buffered: tile kt+1 streams in (cp.async) while tile kt is consumed
+  extern __shared__ __align__(16) uint8_t smem_pf[];
+  auto sKb = reinterpret_cast<__nv_bfloat16(*)[BC][LD]>(smem_pf);
+  auto sVb = reinterpret_cast<__nv_bfloat16(*)[BC][LD]>(smem_pf + 2 * BC * LD * 2);
   __shared__ int sPos[BR];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -157,25 +168,35 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) 
     float ma = -FLT_MAX, mb = -FLT_MAX, la = 0.f, lb = 0.f;
 
     const int n_kt = max_pos / BC + 1;
-    for (int kt = 0; kt < n_kt; ++kt) {
-      // K/V of tokens [kt*64, kt*64+64): 4 pages, each head's 16 x HD run contiguous
-      __syncthreads();
+    // K/V of tokens [kt*64, kt*64+64): 4 pages, each head's 16 x HD run contiguous
+    auto load_tile = [&](int kt, int buf) {
       constexpr int kChunks = BC * HD / 8;  // 16-byte chunks per tile
       for (int c = threadIdx.x; c < kChunks; c += blockDim.x) {
         const int tok = c / (HD / 8), col = (c % (HD / 8)) * 8;
         const int p = kt * BC + tok;
-        uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
         const int page = p <= max_pos ? pt[p >> 4] : -1;
-        if (page >= 0) {
-          const size_t off = (size_t)page * P.page_elems + (size_t)P.layer * P.layer_elems +
-                             ((size_t)head * 16 + (p & 15)) * HD + col;
-          kv = *reinterpret_cast<const uint4*>(P.pool + off);
-          vv = *reinterpret_cast<const uint4*>(P.pool + off + v_off);
-        }
-        *reinterpret_cast<uint4*>(&sK[tok][col]) = kv;
-        *reinterpret_cast<uint4*>(&sV[tok][col]) = vv;
+        const size_t off = page >= 0 ? (size_t)page * P.page_elems +
+                                           (size_t)P.layer * P.layer_elems +
+                                           ((size_t)head * 16 + (p & 15)) * HD + col
+                                     : 0;
+        cp_async16(&sKb[buf][tok][col], P.pool + off, page >= 0);
+        cp_async16(&sVb[buf][tok][col], P.pool + off + v_off, page >= 0);
+      }
+      cp_async_commit();
+    };
+    __syncthreads();  // the previous item is done with both buffers
+    load_tile(0, 0);
+    for (int kt = 0; kt < n_kt; ++kt) {
+      const int buf = kt & 1;
+      if (kt + 1 < n_kt) {
+        load_tile(kt + 1, buf ^ 1);
+        cp_async_wait<1>();  // tile kt landed (kt + 1 may still be in flight)
+      } else {
+        cp_async_wait<0>();
       }
       __syncthreads();
+      auto& sK = sKb[buf];
+      auto& sV = sVb[buf];
       // S = Q K^T: 16 rows x 64 keys per warp (8 n-tiles of 8 keys)
       float s[BC / 8][4];
 #pragma unroll
@@ -249,6 +270,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) 
           mma16816(o[j], pf[kk], b0, b1);
         }
       }
+      __syncthreads();  // every warp is done with this buffer before it is refilled
     }
     // normalise and store this warp's rows
     const float ia = la > 0.f ? 1.f / la : 0.f, ib = lb > 0.f ? 1.f / lb : 0.f;
@@ -270,13 +292,23 @@ cudaError_t launch_attention_prefill(const PrefillAttnParams& P, int head_dim, i
   if (P.rows <= 0) return cudaSuccess;
   tile_index_kernel<<<1, 1024, 0, stream>>>(P.tok, P.rows, P.tiles);
   const int grid = num_sms * 4;
-  if (head_dim == 128) {
-    attn_prefill_kernel<128><<<grid, 128, 0, stream>>>(P);
-  } else if (head_dim == 64) {
-    attn_prefill_kernel<64><<<grid, 128, 0, stream>>>(P);
-  } else {
-    return cudaErrorInvalidValue;
-  }
+  auto run = [&](auto kern, int hd) {
+    const int smem = 2 * 2 * 64 * (hd + 8) * 2;  // [K,V][2 buffers][64][hd + 8] bf16
+    static int configured = 0;  // per head dim, per device (bit)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int bit = (hd == 128 ? 1 : 2) << (2 * dev);
+    if (!(configured & bit)) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      configured |= bit;
+    }
+    kern<<<grid, 128, smem, stream>>>(P);
+    return cudaGetLastError();
+  };
+  if (head_dim == 128) return run(attn_prefill_kernel<128>, 128);
+  if (head_dim == 64) return run(attn_prefill_kernel<64>, 64);
+  return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
