@@ -744,6 +744,7 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
   if (p.ws_needed > ws->splitws_elems || p.tiles > ws->n_counters)
     return fail(ctx, BE_ERR_INVALID, "gemm N=%d K=%d ntok=%d: stream-K workspace too small", N, K, ntok);
   L.grid = p.grid;
+  L.rr = p.rr;
   L.pdl = ctx->use_pdl;
   epi.ws = ws->splitws;
   epi.counters = ws->counters;
@@ -1535,6 +1536,7 @@ extern "C" int be_gemm_bf16(be_ctx* ctx, const void* w, const void* x, void* out
   L.K = K;
   L.bn = bn;
   L.grid = p.grid;
+  L.rr = p.rr;
   L.pdl = ctx->use_pdl;
   L.epi.mode = bx::kStore;
   L.epi.ntok = ntok;

@@ -302,7 +302,10 @@ struct SkRange {
   }
 };
 
-template <int BN, int STAGES, int CTAS, int MODE>
+// RR: many token tiles (prefill): CTA c takes whole tiles c, c + G, c + 2G, ... so the CTAs in
+// flight share a few token tiles and all weight tiles stay L2-resident; the per-CTA iteration
+// range [it_begin, it_end) is then virtual (its own tiles back to back).
+template <int BN, int STAGES, int CTAS, int MODE, bool RR>
 __global__ void __launch_bounds__(192, CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
@@ -327,8 +330,15 @@ __global__ void __launch_bounds__(192, CTAS)
   const int lane = threadIdx.x & 31;
   const int nkb = K / kBK;
   SkRange R{(long long)m_tiles * n_tiles * nkb, (int)gridDim.x};
-  const long long it_begin = R.begin(blockIdx.x);
-  const long long it_end = R.begin(blockIdx.x + 1);
+  const int n_my_tiles =
+      RR ? (m_tiles * n_tiles > (int)blockIdx.x
+                ? (m_tiles * n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
+                : 0)
+         : 0;
+  const long long it_begin = RR ? 0 : R.begin(blockIdx.x);
+  const long long it_end = RR ? (long long)n_my_tiles * nkb : R.begin(blockIdx.x + 1);
+  // real tile of a (virtual) tile index of this CTA's range
+  auto real_tile = [&](int vt) { return RR ? (int)blockIdx.x + vt * (int)gridDim.x : vt; };
 
   if (threadIdx.x == 0) {
     stamp(E, 0);
@@ -363,16 +373,23 @@ __global__ void __launch_bounds__(192, CTAS)
       struct Cur {
         int tile, kb, m, n;
       };
-      const int tile0 = (int)(it_begin / nkb);
-      Cur cw{tile0, (int)(it_begin - (long long)tile0 * nkb), tile0 % m_tiles, tile0 / m_tiles};
+      const int vt0 = (int)(it_begin / nkb);
+      const int tile0 = real_tile(vt0);
+      Cur cw{tile0, (int)(it_begin - (long long)vt0 * nkb), tile0 % m_tiles, tile0 / m_tiles};
       Cur cb = cw;
       auto step = [&](Cur& c) {
         if (++c.kb == nkb) {
           c.kb = 0;
-          ++c.tile;
-          if (++c.m == m_tiles) {
-            c.m = 0;
-            ++c.n;
+          if constexpr (RR) {
+            c.tile += (int)gridDim.x;
+            c.m = c.tile % m_tiles;
+            c.n = c.tile / m_tiles;
+          } else {
+            ++c.tile;
+            if (++c.m == m_tiles) {
+              c.m = 0;
+              ++c.n;
+            }
           }
         }
       };
@@ -450,8 +467,9 @@ __global__ void __launch_bounds__(192, CTAS)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int seg = 0;
     for (long long it = it_begin; it < it_end; ++seg) {
-      const int tile = (int)((unsigned)it / (unsigned)nkb);  // it < 2^31
-      const int kb0 = (int)it - tile * nkb;
+      const int vt = (int)((unsigned)it / (unsigned)nkb);  // it < 2^31
+      const int kb0 = (int)it - vt * nkb;
+      const int tile = real_tile(vt);
       const long long left = it_end - it;
       const int kb1 = (int)((nkb - kb0) < left ? nkb : kb0 + left);
       it += kb1 - kb0;
@@ -634,14 +652,14 @@ __global__ void __launch_bounds__(192, CTAS)
   if (warp == 1) tmem_free<kTmemCols>(tmem_base);
 }
 
-template <int BN, int MODE>
-static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
+template <int BN, int MODE, bool RR>
+static cudaError_t launch_bn_rr(const GemmLaunch& L, cudaStream_t stream) {
   constexpr int STAGES = gemm_stages_deep<BN>();
   constexpr int CTAS = gemm_ctas<BN>();  // resident CTAs per SM the register budget allows
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
                        2 * BN * 4 /*rstd*/ +
                        (MODE >= kQKVLora ? BN * (kLoraRank + 1) * 4 : 0) /*LoRA u, adapters*/;
-  auto kern = gemm_sk_kernel<BN, STAGES, CTAS, MODE>;
+  auto kern = gemm_sk_kernel<BN, STAGES, CTAS, MODE, RR>;
   static unsigned long long configured = 0;  // per device: the attribute is device state
   int dev = 0;
   cudaGetDevice(&dev);
@@ -664,6 +682,15 @@ static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
   cfg.numAttrs = L.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, L.w_packed, *L.map_x, L.K, m_tiles, n_tiles,
                             L.epi);
+}
+
+// the round-robin variant only for wide tiles (prefill-sized token counts)
+template <int BN, int MODE>
+static cudaError_t launch_bn(const GemmLaunch& L, cudaStream_t stream) {
+  if constexpr (BN == 256 && MODE != kQKVLora && MODE != kResidLora && MODE != kResidOutLora) {
+    if (L.rr) return launch_bn_rr<BN, MODE, true>(L, stream);
+  }
+  return launch_bn_rr<BN, MODE, false>(L, stream);
 }
 
 template <int MODE>
@@ -737,6 +764,19 @@ GemmPlan gemm_plan(int N, int K, int ntok, int bn, int num_sms, size_t ws_elems,
   } else {
     const long long s = (kMinStreamCtas + tiles - 1) / tiles;  // even k-splits per tile
     g = tiles * s < sms ? tiles * s : sms;
+  }
+  // many token tiles (prefill): whole tiles dealt round-robin, the CTAs in flight share a few
+  // token tiles (BE_GEMM_RR=0 keeps stream-K ranges)
+  static const bool kRR = [] {
+    const char* e = getenv("BE_GEMM_RR");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (kRR && bn == 256 && n_tiles > 16 && tiles >= 4 * sms) {  // M > 4096: measured crossover
+    p.grid = (int)sms;
+    p.ws_needed = 0;
+    p.tiles = tiles;
+    p.rr = 1;
+    return p;
   }
   if (g > total / 4) g = total / 4 > 0 ? total / 4 : 1;
   // partial-tile slots: one per CTA (its first segment; owners never publish theirs)

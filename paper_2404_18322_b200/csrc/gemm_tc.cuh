@@ -123,6 +123,7 @@ struct GemmLaunch {
   int bn;                    // 16/32/64/128/256
   int grid;                  // persistent CTAs (stream-K ranges)
   int pdl;                   // launch with programmatic stream serialization
+  int rr;                    // whole tiles dealt round-robin (large M), see gemm_plan
   EpiParams epi;
 };
 
@@ -130,6 +131,7 @@ struct GemmPlan {
   int grid;
   size_t ws_needed;  // fp32 elements of split-tile partials
   long long tiles;   // arrival counters needed
+  int rr;            // 1: whole tiles round-robin over the CTAs (no split, no partials)
 };
 
 // Launches on `stream`; returns cudaError_t.

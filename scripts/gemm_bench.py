@@ -23,7 +23,8 @@ SHAPES = [  # (name, N, K, ntok)
     ("qkv7b_m16", 12288, 4096, 16), ("o7b_m16", 4096, 4096, 16), ("gu7b_m16", 22016, 4096, 16),
     ("down7b_m16", 4096, 11008, 16),
     ("gu7b_m256", 22016, 4096, 256), ("gu7b_m2048", 22016, 4096, 2048),
-    ("qkv7b_m4096", 12288, 4096, 4096), ("qkv7b_m32768", 12288, 4096, 32768),
+    ("qkv7b_m4096", 12288, 4096, 4096), ("qkv7b_m8192", 12288, 4096, 8192),
+    ("qkv7b_m16384", 12288, 4096, 16384), ("qkv7b_m32768", 12288, 4096, 32768),
     ("o7b_m32768", 4096, 4096, 32768),
 ]
 
