@@ -85,8 +85,10 @@ __device__ __forceinline__ void lora_add(const EpiParams& E, int f, int tt0, int
       if (i < nvalid) v[i] += lora_dot(b, ub + i * (kLoraRank / 4));
     return;
   }
-#pragma unroll 1
-  for (int i = 0; i < nvalid; ++i) {
+  // mixed adapters in the chunk: per token, static indices so v stays in registers
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i >= nvalid) break;  // warp-uniform
     const int a = __shfl_sync(0xffffffffu, my_a, i);
     if (a < 0) continue;
     float b[kLoraRank];
