@@ -195,7 +195,8 @@ __global__ void synth_plain_kernel(__nv_bfloat16* __restrict__ dst, int rows, in
 // A row with 16-byte loads, all of them in flight (d <= 8192: at most 32 per lane).
 __global__ void __launch_bounds__(256) lora_shrink_kernel(
     const __nv_bfloat16* __restrict__ x, int ldx, int d, const float* __restrict__ ss,
-    int ss_groups, float eps, LoraTable A, int r3, const int* __restrict__ idx,
+    int ss_groups, float eps, const __grid_constant__ LoraTable A, int r3,
+    const int* __restrict__ idx,
     float* __restrict__ u) {
   extern __shared__ float xs[];
   const int t = blockIdx.x;
