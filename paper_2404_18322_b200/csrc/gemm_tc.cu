@@ -265,25 +265,32 @@ __device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, flo
   const int G4 = G >> 2;
   const float inv_d = 1.0f / (float)(G * 32);
   constexpr int J = BN / 4;  // tokens per warp
-  float s[J];
+  // wide tiles (BN > 64) in rounds of 16 tokens: all 64 at once would exceed the register file
+  constexpr int JC = J < 16 ? J : 16;
+#pragma unroll 1
+  for (int j0 = 0; j0 < J; j0 += JC) {
+    float s[JC];
 #pragma unroll
-  for (int jj = 0; jj < J; ++jj) {
-    const int t = n0 + q + 4 * jj;
-    const float4* p = reinterpret_cast<const float4*>(E.ss_in + (size_t)t * G);
-    const bool ok = t < E.ntok;
-    const float4 a = (ok && lane < G4) ? __ldcg(p + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 b = (ok && lane + 32 < G4) ? __ldcg(p + lane + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
-    s[jj] = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
-  }
+    for (int jj = 0; jj < JC; ++jj) {
+      const int t = n0 + q + 4 * (j0 + jj);
+      const float4* p = reinterpret_cast<const float4*>(E.ss_in + (size_t)t * G);
+      const bool ok = t < E.ntok;
+      const float4 a = (ok && lane < G4) ? __ldcg(p + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 b = (ok && lane + 32 < G4) ? __ldcg(p + lane + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+      s[jj] = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
+    }
 #pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
+    for (int off = 16; off >= 1; off >>= 1) {
 #pragma unroll
-    for (int jj = 0; jj < J; ++jj) s[jj] += __shfl_xor_sync(0xffffffffu, s[jj], off);
-  }
-  if (lane == 0) {
+      for (int jj = 0; jj < JC; ++jj) s[jj] += __shfl_xor_sync(0xffffffffu, s[jj], off);
+    }
+    if (lane == 0) {
 #pragma unroll
-    for (int jj = 0; jj < J; ++jj)
-      rs[q + 4 * jj] = n0 + q + 4 * jj < E.ntok ? rsqrtf(s[jj] * inv_d + E.norm_eps) : 0.f;
+      for (int jj = 0; jj < JC; ++jj) {
+        const int tt = q + 4 * (j0 + jj);
+        rs[tt] = n0 + tt < E.ntok ? rsqrtf(s[jj] * inv_d + E.norm_eps) : 0.f;
+      }
+    }
   }
 }
 
