@@ -399,7 +399,7 @@ def run_pipeline(args, world, rank, local, depth, why):
 
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    total = ticks_needed(depth, args.steps, args.warmup)
+    total = ticks_needed(depth, 2 * args.steps, args.warmup)  # device leg + end-to-end leg
     need = tokens_per_request_needed(depth, total, depth) + 1
     wl = make_workload(args, need)
     ctx = Context(local)
@@ -434,6 +434,31 @@ def run_pipeline(args, world, rank, local, depth, why):
     fin = torch.tensor([stage.stats.finished - before], device="cuda", dtype=torch.float64)
     dist.all_reduce(fin, op=dist.ReduceOp.SUM)  # only each group's last stage counts tokens
     tokens = float(fin.item())
+    # end to end: stage 0 uploads each micro-batch's input rows from pinned host memory and the
+    # last stage reads its output rows back every tick (decode_group host I/O)
+    stage.set_host_io(True)
+    if stage.host_in is not None:
+        stage.host_in.copy_(torch.randn(stage.host_in.shape).to(torch.bfloat16))
+    ctx.sync()
+    dist.barrier()
+    torch.cuda.synchronize()
+    before = stage.stats.finished
+    t_wall = time.perf_counter()
+    e0.record(stage.stream)
+    for t in range(warm + args.steps, warm + 2 * args.steps):
+        stage.tick(t, total)
+    e1.record(stage.stream)
+    ctx.sync()
+    torch.cuda.synchronize()
+    e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t_wall) * 1e3)
+    em = torch.tensor([e_ms], device="cuda")
+    dist.all_reduce(em, op=dist.ReduceOp.MAX)
+    ef = torch.tensor([stage.stats.finished - before], device="cuda", dtype=torch.float64)
+    dist.all_reduce(ef, op=dist.ReduceOp.SUM)
+    mb_bytes = stage.per_mb * wl.shape.d_model * 2
+    e2e = {"value": round(float(ef.item()) / (float(em.item()) / 1e3), 2), "unit": "tokens/s",
+           "h2d_bytes_per_step": mb_bytes, "d2h_bytes_per_step": mb_bytes,
+           "ms_per_step": round(float(em.item()) / args.steps, 4)}
     stats = stage.run.step_stats()
     hop_bytes = wl.n_requests * wl.shape.d_model * 2
     if rank == 0:
@@ -453,7 +478,7 @@ def run_pipeline(args, world, rank, local, depth, why):
                        "placement": why,
                        "stage_cost_bytes": [round(c) for c in stage.stage_costs],
                        "l2": "inputs larger than L2"},
-            "roofline": None, "e2e": None, "cpu_baseline": None,
+            "roofline": None, "e2e": e2e, "cpu_baseline": None,
             "gpu_launches": int(stats["launches"]) * args.steps, "clocks": clk,
             "prefill_s": round(prefill_s, 2),
             "note": "one step = one pipeline tick = one micro-batch token leaving each group's "

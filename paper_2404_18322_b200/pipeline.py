@@ -286,9 +286,23 @@ class PipelineStage:
             run_tick(self.dist, t, total_ticks, self.rank, self.world, self.n_micro,
                      self._compute, self.mb_rows, self.base)
 
+    def set_host_io(self, on: bool) -> None:
+        """End-to-end leg: stage 0 uploads each micro-batch's input rows from pinned host memory
+        and the last stage reads its output rows back (synchronously) every tick."""
+        self.host_in = self.host_out = None
+        if not on:
+            return
+        d = self.wl.shape.d_model
+        t = self.torch
+        if self.rank == 0:
+            self.host_in = t.zeros(self.per_mb, d, dtype=t.bfloat16).pin_memory()
+        if self.rank == self.world - 1:
+            self.host_out = t.empty(self.per_mb, d, dtype=t.bfloat16).pin_memory()
+
     def _compute(self, m: int) -> None:
         reqs = np.arange(m * self.per_mb, (m + 1) * self.per_mb, dtype=np.int32)
-        self.run.decode_group(m, reqs)
+        self.run.decode_group(m, reqs, getattr(self, "host_in", None),
+                              getattr(self, "host_out", None))
         self.stats.computed += 1
         if self.rank == self.world - 1:
             self.stats.finished += self.per_mb
