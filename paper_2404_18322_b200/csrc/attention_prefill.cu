@@ -113,6 +113,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// Four 8x8 bf16 tiles (no transpose): lane l addresses row (l & 7) of tile l >> 3.
+__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                                        const void* row) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(row));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(a));
+}
+
 template <int HD>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) {
   constexpr int BR = 64, BC = 64;
@@ -203,10 +212,12 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) 
       for (int j = 0; j < BC / 8; ++j) {
         s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&sK[j * 8 + g][ks * 16 + 2 * t]);
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&sK[j * 8 + g][ks * 16 + 2 * t + 8]);
+        for (int ks = 0; ks < KS; ks += 2) {
+          // K rows j*8.. as the B operand of k-steps ks and ks+1 in one ldmatrix
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(b0, b1, b2, b3, &sK[j * 8 + (lane & 7)][ks * 16 + (lane >> 3) * 8]);
           mma16816(s[j], qf[ks], b0, b1);
+          mma16816(s[j], qf[ks + 1], b2, b3);
         }
       }
       // causal mask (key position <= query position), then online softmax in log2 units
