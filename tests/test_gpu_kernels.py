@@ -20,6 +20,9 @@ def _bf16(a: np.ndarray):
 @pytest.mark.parametrize("N,K,ntok,ksplit", [
     (128, 64, 1, 1), (256, 256, 8, 1), (768, 512, 300, 1), (1024, 1024, 16, 4),
     (4096, 4096, 64, 0), (12288, 4096, 64, 0), (4096, 11008, 16, 0), (512, 256, 200, 2),
+    # prefill sizes: M > 4096 with >= 4 x 148 tiles takes the round-robin whole-tile schedule
+    # (gemm_plan rr), a partial last token tile included
+    (2560, 512, 8192 + 77, 0), (12288, 1024, 4097, 0),
 ])
 def test_gemm_matches_fp32(ctx, N, K, ntok, ksplit):
     g = torch.Generator().manual_seed(N * 7 + K + ntok)
