@@ -583,7 +583,7 @@ def run_ours(args, world, rank, local):
         e0.record(stream)
         for _ in range(args.steps):
             run.decode_step(hin, hout)
-            hin.copy_(hout)  # greedy feedback: the step's output is the next input
+            hin, hout = hout, hin  # greedy feedback: the step's output buffer is the next input
         e1.record(stream)
         ctx.sync()
         wall = time.perf_counter() - t_start
