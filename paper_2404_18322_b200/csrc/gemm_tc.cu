@@ -217,16 +217,20 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
     }
     if constexpr (kLora) lora_add(E, f, t0 - n0, nvalid, v, lu, li);
     if (sec < 2) {
-      // rows are pair-interleaved per head: even = dim j, odd = dim j + hd/2 (rotate_half)
+      // rows are pair-interleaved per head: even = dim j, odd = dim j + hd/2 (rotate_half).
+      // All 16 (cos, sin) loads are issued before the first use: one L2 round trip per chunk.
+      float2 cs[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int pos = __shfl_sync(0xffffffffu, my_pos, i);
+        const int pc = i < nvalid && pos > 0 ? pos : 0;  // padding rows of a grouped batch: -1
+        cs[i] = __ldg(E.rope + (size_t)pc * (E.head_dim >> 1) + (e >> 1));
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float other = __shfl_xor_sync(0xffffffffu, v[i], 1);
-        const int pos = __shfl_sync(0xffffffffu, my_pos, i);
-        if (i < nvalid) {
-          const int pc = pos > 0 ? pos : 0;  // padding rows of a grouped batch have pos -1
-          const float2 cs = __ldg(E.rope + (size_t)pc * (E.head_dim >> 1) + (e >> 1));
-          v[i] = odd ? v[i] * cs.x + other * cs.y : v[i] * cs.x - other * cs.y;
-        }
+        if (i < nvalid)
+          v[i] = odd ? v[i] * cs[i].x + other * cs[i].y : v[i] * cs[i].x - other * cs[i].y;
       }
     }
     const int ee = e & ~1;
