@@ -119,6 +119,11 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
     const int fe = f & ~1;
     float sq[8];  // kResid: this lane's x^2 + x'^2 of token pair p
     float2 xv[8];
+    // kResidOut: the chunk's next-hop rows, one load per token (lane i < 16 -> token t0 + i),
+    // all issued before the stores below (which might alias them for the compiler)
+    int my_dst = -1;
+    if constexpr (BASE == kResidOut)
+      my_dst = (lane & 15) < nvalid ? __ldg(E.tok + (size_t)(t0 + (lane & 15)) * 5 + 1) : -1;
     if constexpr (BASE == kResid || BASE == kResidOut) {
       // all residual loads of the chunk in flight before the first store (the stores below may
       // alias them as far as the compiler knows, which would serialise 8 L2 round trips)
@@ -140,8 +145,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
         if (valid)
           *reinterpret_cast<uint32_t*>(E.out + (size_t)t * E.ldo + fe) = pack_bf16x2(lo, hi);
       } else if constexpr (BASE == kResidOut) {
-        const int drow = valid ? __ldg(E.tok + (size_t)t * 5 + 1) : -1;  // be_token.dst_row
-        if (drow >= 0)
+        const int drow = __shfl_sync(0xffffffffu, my_dst, 2 * p + (odd ? 1 : 0));  // dst_row
+        if (valid && drow >= 0)
           *reinterpret_cast<uint32_t*>(E.out + (size_t)drow * E.ldo + fe) =
               pack_bf16x2(xv[p].x + lo, xv[p].y + hi);
       } else {
