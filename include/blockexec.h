@@ -199,7 +199,10 @@ int be_timeline_read(be_ctx* ctx, be_timeline_rec* out, int cap, int* n_out);
 /* KV migration data path (§8 f: the P2P page copy of start_kv_migration, scenario.cpp:361-431):
  * copies whole pages src_slots[i] of src_pool to dst_slots[i] of dst_pool (host arrays) on the
  * destination context's stream; contiguous slot runs move as one copy. The pools may live on
- * different GPUs (peer copy over NVLink; peer access is enabled on first use). Async. */
+ * different GPUs (peer copy over NVLink; peer access is enabled on first use). Async; the copy
+ * is ordered after all work queued so far on the source context's stream. The source slots must
+ * not be rewritten (e.g. reallocated after bh_kv_move_segment_slots freed them) before the copy
+ * has executed: order such writes after `stream` (or synchronize it). */
 int be_kv_copy_pages(be_ctx* dst_ctx, const be_kv_pool* src_pool, be_kv_pool* dst_pool,
                      const int32_t* src_slots, const int32_t* dst_slots, int n, void* stream);
 
@@ -256,7 +259,8 @@ int be_stitch_rows(be_ctx* ctx, const be_stitch* s, const void* d_in, int rows, 
  * scenario.cpp:361-431). A segment's n_pages pages (src_slots -> dst_slots, token order, from
  * bh_kv_move_segment_slots) move to dst_pool: the first n_recompute pages are rebuilt on the
  * destination by a chunked prefill of `blk` over the head tokens' block-input rows
- * (d_head_rows, head_tokens rows, (n_recompute-1)*16 < head_tokens <= n_recompute*16), while the
+ * (d_head_rows, head_tokens rows, (n_recompute-1)*16 < head_tokens <= n_recompute*16, and
+ * head_tokens == n_recompute*16 when tail pages are copied, so no token is left out), while the
  * other pages are copied from src_pool (peer GPU over NVLink, or the same GPU) on a side stream;
  * the call's stream waits for both. `blk`, dst_pool and ws belong to ctx. Async. */
 int be_kv_migrate(be_ctx* ctx, be_block* blk, const be_kv_pool* src_pool, be_kv_pool* dst_pool,
@@ -300,6 +304,28 @@ int be_attention(be_ctx* ctx, const void* d_q, const void* d_pool, int n_layers,
                  int head_dim, int layer, const int32_t* d_page_table, int pt_stride,
                  const int32_t* d_row_pt, const int32_t* d_row_ctx, int rows, int splits,
                  void* d_out, void* stream);
+
+/* ---- inter-block hop (§8 a11; replaces LinkManager::transfer, proj/core/src/cluster.cpp:170-192,
+ * at the Simulation::deliver call, proj/core/src/scenario.cpp:282-308): the bf16 rows of a chain
+ * crossing GPUs move by NCCL point-to-point over NVLink. One communicator per process (one
+ * process per GPU, `rank` = its global rank); every rank passes the same unique id (made by
+ * be_comm_unique_id on one rank and broadcast by the caller). The sends/recvs of one executor
+ * phase go between be_hop_begin / be_hop_end (one NCCL group: no ordering deadlock between
+ * peers) and are enqueued on `stream` (NULL = the context's stream) after the work that
+ * produced the rows. Async; bytes are counted per communicator (be_comm_bytes). */
+typedef struct be_comm be_comm;
+#define BE_COMM_ID_BYTES 128
+int be_comm_unique_id(void* id_out);
+int be_comm_init(be_ctx* ctx, int n_ranks, int rank, const void* id, be_comm** out);
+int be_comm_destroy(be_comm* comm);
+const char* be_comm_last_error(const be_comm* comm);
+int be_comm_rank(const be_comm* comm);
+int be_comm_size(const be_comm* comm);
+int64_t be_comm_bytes(const be_comm* comm, int sent);
+int be_hop_begin(be_comm* comm);
+int be_hop_send(be_comm* comm, int peer, const void* d_rows, int64_t bytes, void* stream);
+int be_hop_recv(be_comm* comm, int peer, void* d_rows, int64_t bytes, void* stream);
+int be_hop_end(be_comm* comm);
 
 #ifdef __cplusplus
 }

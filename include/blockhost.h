@@ -147,6 +147,7 @@ int bh_runner_trace(const bh_runner* r, bh_batch_rec* recs, int cap, int* n_out,
 int bh_runner_clear_trace(bh_runner* r);
 /* Device pointer of the decode activation arena ([n_requests][d] bf16, row = request). */
 void* bh_runner_arena(bh_runner* r);
+int bh_runner_requests(const bh_runner* r); /* n_requests: rows of the decode arena */
 /* Device pointer of the prefill arena ([sum of prompts][d] bf16, requests in order) and its
  * row count; a pipeline stage receives its prompts' hidden states here before bh_runner_run. */
 void* bh_runner_prefill_arena(bh_runner* r, int64_t* rows);
@@ -160,6 +161,46 @@ typedef struct {
   int graph_replayed;    /* 1 when the step ran as a CUDA graph replay */
 } bh_step_stats;
 int bh_runner_step_stats(const bh_runner* r, bh_step_stats* out);
+
+/* ---- cluster: the executor loop over several GPUs with block placement (§8 a11 / a15 / e) ----
+ * Blocks are placed on ranks (one GPU each); a token step is a fixed list of phases. In phase k
+ * every rank steps the runner that holds its rows' k-th leg (a leg = consecutive chain blocks on
+ * one device), then the phase's hops move row ranges between runners: be_hop_send / be_hop_recv
+ * across processes (NCCL over NVLink), a device copy between runners of this process (the
+ * reference's deliver, scenario.cpp:282-308; same-device hops cost nothing there either). The
+ * plan is identical on every rank; each process executes the runs and hops touching its own
+ * ranks, in plan order, on its context's stream (no host synchronisation inside a step).
+ * comm NULL: ranks rank0 .. rank0+n_local-1 all live in this process (e.g. several ranks on one
+ * GPU for tests); with a communicator: one local rank, = be_comm_rank(comm). */
+typedef struct bh_cluster bh_cluster;
+#define BH_ARENA_DECODE 0  /* one row per request (bh_runner_arena) */
+#define BH_ARENA_PREFILL 1 /* prompt rows (bh_runner_prefill_arena) */
+typedef struct {
+  int32_t src_rank, src_runner; /* global rank, runner slot on it */
+  int32_t dst_rank, dst_runner;
+  int32_t arena;                /* BH_ARENA_* (the same on both sides) */
+  int32_t pad_;
+  int64_t src_row, dst_row, rows;
+} bh_hop;
+typedef struct {
+  int64_t steps, batches;
+  int64_t sent_bytes, recv_bytes; /* NCCL P2P payload of this rank */
+  int64_t local_bytes;            /* device copies between runners of this process */
+} bh_cluster_stats;
+int bh_cluster_create(be_comm* comm, int rank0, int n_local, be_ctx* const* ctxs, int d_model,
+                      bh_cluster** out);
+int bh_cluster_free(bh_cluster* c);
+const char* bh_cluster_last_error(const bh_cluster* c);
+int bh_cluster_add_runner(bh_cluster* c, int rank, int slot, bh_runner* r);
+/* kind BE_PHASE_PREFILL (runs bh_runner_run) or BE_PHASE_DECODE (bh_runner_decode_step);
+ * runs = n_runs (rank, slot) pairs. */
+int bh_cluster_add_phase(bh_cluster* c, int kind, int n_runs, const int32_t* runs, int n_hops,
+                         const bh_hop* hops);
+int bh_cluster_prefill(bh_cluster* c);
+/* One token for every request of every rank. host_in / host_out (one local rank only): the
+ * home runner's (slot home_slot, first decode phase) rows in before / out after the step. */
+int bh_cluster_decode_step(bh_cluster* c, int home_slot, const void* host_in, void* host_out);
+int bh_cluster_get_stats(const bh_cluster* c, bh_cluster_stats* out);
 
 #ifdef __cplusplus
 }

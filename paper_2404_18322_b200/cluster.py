@@ -1,0 +1,404 @@
+"""Multi-GPU block placement and the cluster executor (SURVEY §8 a11 / a15 / e).
+
+Placement (place_blocks): the unit is a block instance on a device (agent.hpp:44-56).
+  * A block every tenant routes through (a shared foundation block) serves every request, so
+    each GPU holds an instance of it and runs its own requests through it - the reference's
+    scale-out of its hottest instances to further devices (Scheduler::scale_decisions,
+    scheduler.cpp:227-260), taken to every device since 180 GB holds them all.
+  * A tenant's private blocks are placed one by one in chain order by the reference's device
+    rule (Scheduler::choose_device with the locality preference, scheduler.cpp:262-314, mirrored
+    bit-exactly by bh_policy_choose_device): the device whose resident blocks have the most
+    adjacency weight (static chain neighbours) to the block, ties to the most free memory. The
+    first private block of a tenant neighbours shared blocks present everywhere, so it lands on
+    the emptiest GPU; the tenant's next private block follows it there (one hop out, one back).
+  * Requests are served where they arrive (weak scaling: every GPU receives the config's request
+    mix). A private block then runs ALL tenants' rows for it from every GPU in one batch - its
+    weights stream once per token step instead of once per GPU.
+
+Plan (block_plan / stage_plan): a request's chain is cut into legs (consecutive blocks on one
+device); phase k runs every request's k-th leg, and after it the rows hop to their next leg's
+runner (NCCL P2P across GPUs, a device copy inside a process) or back home after the last leg.
+Each (rank, phase) pair with work is one single-device executor (bh_runner) whose workload is the
+leg's blocks and rows. The plan is the same on every rank; bh_cluster (C++) executes it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import BlockExecError, check, lib
+from .workloads import Workload
+
+PHASE_PREFILL, PHASE_DECODE = 0, 1
+ARENA_DECODE, ARENA_PREFILL = 0, 1
+
+
+class Hop(C.Structure):
+    _fields_ = [("src_rank", C.c_int32), ("src_runner", C.c_int32), ("dst_rank", C.c_int32),
+                ("dst_runner", C.c_int32), ("arena", C.c_int32), ("pad_", C.c_int32),
+                ("src_row", C.c_int64), ("dst_row", C.c_int64), ("rows", C.c_int64)]
+
+
+class ClusterStats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("batches", C.c_int64), ("sent_bytes", C.c_int64),
+                ("recv_bytes", C.c_int64), ("local_bytes", C.c_int64)]
+
+
+_bound = False
+
+
+def _bind():
+    global _bound
+    if _bound:
+        return lib()
+    L = lib()
+    P, I, I64 = C.c_void_p, C.c_int, C.c_int64
+    for name, res, args in [
+        ("be_comm_unique_id", I, [P]),
+        ("be_comm_init", I, [P, I, I, P, C.POINTER(C.c_void_p)]),
+        ("be_comm_destroy", I, [P]),
+        ("be_comm_last_error", C.c_char_p, [P]),
+        ("be_comm_rank", I, [P]),
+        ("be_comm_size", I, [P]),
+        ("be_comm_bytes", I64, [P, I]),
+        ("be_hop_begin", I, [P]),
+        ("be_hop_end", I, [P]),
+        ("be_hop_send", I, [P, I, P, I64, P]),
+        ("be_hop_recv", I, [P, I, P, I64, P]),
+        ("bh_cluster_create", I, [P, I, I, P, I, C.POINTER(C.c_void_p)]),
+        ("bh_cluster_free", I, [P]),
+        ("bh_cluster_last_error", C.c_char_p, [P]),
+        ("bh_cluster_add_runner", I, [P, I, I, P]),
+        ("bh_cluster_add_phase", I, [P, I, I, P, I, P]),
+        ("bh_cluster_prefill", I, [P]),
+        ("bh_cluster_decode_step", I, [P, I, P, P]),
+        ("bh_cluster_get_stats", I, [P, P]),
+        ("bh_runner_requests", I, [P]),
+    ]:
+        fn = getattr(L, name)
+        fn.restype, fn.argtypes = res, args
+    _bound = True
+    return L
+
+
+# ------------------------------------------------------------------------------ placement
+def shared_blocks(wl: Workload) -> set[int]:
+    """Blocks on more than one tenant's chain."""
+    seen: dict[int, set[int]] = {}
+    for t, ch in enumerate(wl.chains):
+        for b in ch:
+            seen.setdefault(b, set()).add(t)
+    return {b for b, ts in seen.items() if len(ts) > 1}
+
+
+def place_blocks(wl: Workload, world: int, hbm_bytes: int = 180 * 10**9) -> list[int]:
+    """Block -> rank (-1: an instance on every rank). Private blocks by the reference's locality
+    rule (bh_policy_choose_device = Scheduler::choose_device, scheduler.cpp:262-314), in chain
+    order, each placement charged to its device's ledger before the next choice."""
+    from .pipeline import routing_policy
+    if world == 1:
+        return [-1] * len(wl.block_names)  # one GPU holds every block: no leg ever leaves it
+    shared = shared_blocks(wl)
+    pol = routing_policy(wl, world, instances=False, hbm_bytes=hbm_bytes)
+    used = [0] * world
+    seq = 0
+    for b in sorted(shared):
+        for dev in range(world):
+            seq += 1
+            pol.put_instance(f"r{dev}.{wl.block_names[b]}", wl.block_names[b], dev, ready=True,
+                             created_seq=seq)
+            used[dev] += wl.shape.param_bytes
+    for dev in range(world):
+        pol.set_ledger(dev, used[dev])
+    place = [-1] * len(wl.block_names)
+    for ch in wl.chains:
+        for b in ch:
+            if b in shared or place[b] >= 0:
+                continue
+            dev = pol.choose_device(wl.block_names[b])
+            if dev < 0:
+                raise ValueError(f"{wl.name}: no device fits block {wl.block_names[b]}")
+            seq += 1
+            pol.put_instance(f"r{dev}.{wl.block_names[b]}", wl.block_names[b], dev, ready=True,
+                             created_seq=seq)
+            used[dev] += wl.shape.param_bytes
+            pol.set_ledger(dev, used[dev])
+            place[b] = dev
+    pol.close()
+    return place
+
+
+# ------------------------------------------------------------------------------ plans
+@dataclass
+class RunnerSpec:
+    rank: int
+    slot: int                      # = phase index
+    wl: Workload                   # the leg's blocks and rows
+    items: list = field(default_factory=list)  # (home rank, request index) per row
+
+
+@dataclass
+class Plan:
+    world: int
+    homes: list[int]                 # ranks that receive requests
+    order: list[int]                 # request order of a home runner (row -> request index)
+    runners: list[RunnerSpec]
+    phases: list[tuple[int, list, list]]  # (kind, [(rank, slot)], [Hop fields tuple])
+    placement: list[int]             # block -> rank (-1 = every rank / home)
+    note: str = ""
+
+    def runner(self, rank: int, slot: int) -> RunnerSpec | None:
+        for r in self.runners:
+            if r.rank == rank and r.slot == slot:
+                return r
+        return None
+
+    def hop_bytes_per_step(self, rank: int, d_model: int) -> tuple[int, int]:
+        """(sent, received) NCCL bytes of one decode step on `rank`."""
+        s = r = 0
+        for kind, _, hops in self.phases:
+            if kind != PHASE_DECODE:
+                continue
+            for h in hops:
+                if h[0] == h[2]:
+                    continue
+                if h[0] == rank:
+                    s += h[8] * d_model * 2
+                if h[2] == rank:
+                    r += h[8] * d_model * 2
+        return s, r
+
+
+def _legs(chain: list[int], placement: list[int]) -> list[tuple[int, list[int]]]:
+    """Consecutive chain blocks on one location; location -1 = the request's home rank."""
+    legs: list[tuple[int, list[int]]] = []
+    for b in chain:
+        loc = placement[b]
+        if legs and legs[-1][0] == loc:
+            legs[-1][1].append(b)
+        else:
+            legs.append((loc, [b]))
+    return legs
+
+
+def _sub_workload(wl: Workload, name: str, items, legs_of, phase) -> Workload:
+    names, comps, remap, chains, tmap = [], [], {}, [], {}
+    req_tenant, req_prompt, req_output = [], [], []
+    for _, i in items:
+        t = wl.req_tenant[i]
+        if t not in tmap:
+            sub = []
+            for b in legs_of[t][phase][1]:
+                if b not in remap:
+                    remap[b] = len(names)
+                    names.append(wl.block_names[b])
+                    if wl.block_comps:
+                        comps.append(wl.block_comps[b])
+                sub.append(remap[b])
+            tmap[t] = len(chains)
+            chains.append(sub)
+        req_tenant.append(tmap[t])
+        req_prompt.append(wl.req_prompt[i])
+        req_output.append(wl.req_output[i])
+    return Workload(name, wl.shape, names, chains, req_tenant, req_prompt, req_output,
+                    wl.max_batch_tokens, wl.seed, dict(wl.notes), comps or None)
+
+
+def make_plan(wl: Workload, world: int, placement: list[int], homes: list[int],
+              order: list[int], note: str = "") -> Plan:
+    legs_of = [_legs(ch, placement) for ch in wl.chains]
+    for t, lg in enumerate(legs_of):
+        if lg[0][0] != -1 and len(homes) > 1:
+            raise ValueError(f"tenant {t}: a chain must start on blocks present at every home")
+    n_phase = max(len(lg) for lg in legs_of)
+
+    def where(loc, home):
+        return home if loc == -1 else loc
+
+    # items per (rank, phase), in (home, request order) order
+    runners: dict[tuple[int, int], RunnerSpec] = {}
+    row_of: dict[tuple[int, int, int], int] = {}  # (phase, home, i) -> row in its runner
+    poff_of: dict[tuple[int, int, int], int] = {}
+    for p in range(n_phase):
+        for s in homes:
+            for i in order:
+                lg = legs_of[wl.req_tenant[i]]
+                if p >= len(lg):
+                    continue
+                q = where(lg[p][0], s)
+                spec = runners.setdefault((q, p), RunnerSpec(q, p, None))
+                row_of[(p, s, i)] = len(spec.items)
+                poff_of[(p, s, i)] = sum(wl.req_prompt[j] for _, j in spec.items)
+                spec.items.append((s, i))
+    for (q, p), spec in runners.items():
+        spec.wl = _sub_workload(wl, f"{wl.name}@r{q}.leg{p}", spec.items, legs_of, p)
+
+    def merge(hops):
+        out = []
+        for h in hops:
+            if out:
+                o = out[-1]
+                if (o[:6] == h[:6] and o[6] + o[8] == h[6] and o[7] + o[8] == h[7]):
+                    out[-1] = o[:8] + (o[8] + h[8],)
+                    continue
+            out.append(h)
+        return out
+
+    phases = []
+    for kind in (PHASE_PREFILL, PHASE_DECODE):
+        for p in range(n_phase):
+            runs = sorted((q, pp) for (q, pp) in runners if pp == p)
+            hops = []
+            for s in homes:
+                for i in order:
+                    lg = legs_of[wl.req_tenant[i]]
+                    if p >= len(lg):
+                        continue
+                    src = where(lg[p][0], s)
+                    if p + 1 < len(lg):
+                        dst, dslot = where(lg[p + 1][0], s), p + 1
+                        if kind == PHASE_PREFILL:
+                            hops.append((src, p, dst, dslot, ARENA_PREFILL, 0,
+                                         poff_of[(p, s, i)], poff_of[(p + 1, s, i)],
+                                         wl.req_prompt[i]))
+                        else:
+                            hops.append((src, p, dst, dslot, ARENA_DECODE, 0, row_of[(p, s, i)],
+                                         row_of[(p + 1, s, i)], 1))
+                    elif p > 0 or src != s:
+                        # the last leg's rows (prefill: the first token) go back home
+                        hops.append((src, p, s, 0, ARENA_DECODE, 0, row_of[(p, s, i)],
+                                     row_of[(0, s, i)], 1))
+            phases.append((kind, runs, merge(hops)))
+    return Plan(world, list(homes), list(order), sorted(runners.values(),
+                key=lambda r: (r.rank, r.slot)), phases, placement, note)
+
+
+def block_plan(wl: Workload, world: int) -> Plan:
+    """Weak scaling with block placement: every rank receives the config's requests (home rows
+    ordered by tenant so each tenant's rows hop as one range)."""
+    placement = place_blocks(wl, world)
+    order = sorted(range(wl.n_requests), key=lambda i: (wl.req_tenant[i], i))
+    owners = sorted({p for p in placement if p >= 0})
+    note = (f"block placement over {world} GPU(s): {len(shared_blocks(wl))} shared blocks on "
+            f"every GPU; private blocks by choose_device(locality) -> ranks "
+            + ",".join(f"{wl.block_names[b]}:{p}" for b, p in enumerate(placement) if p >= 0)
+            + f" ({len(owners)} GPU(s) hold private blocks)")
+    return make_plan(wl, world, placement, list(range(world)), order, note)
+
+
+def stage_plan(wl: Workload, cuts: list[tuple[int, int]]) -> Plan:
+    """Chain positions [a, b) of cut k on rank k; all requests live on rank 0 (request order):
+    the position pipeline of pipeline.py without micro-batches. Batches are composed exactly as
+    in a one-GPU lockstep run."""
+    placement = [-1] * len(wl.block_names)
+    for k, (a, b) in enumerate(cuts):
+        for ch in wl.chains:
+            for blk in ch[a:b]:
+                placement[blk] = k
+    return make_plan(wl, len(cuts), placement, [0], list(range(wl.n_requests)),
+                     f"positions {cuts} on ranks 0..{len(cuts) - 1}")
+
+
+# ------------------------------------------------------------------------------ runtime
+class Comm:
+    """An NCCL communicator of the hop data path (be_comm_*)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        L = _bind()
+        buf = C.create_string_buffer(128)
+        if L.be_comm_unique_id(buf) != 0:
+            raise BlockExecError(5, "be_comm_unique_id failed")
+        return buf.raw
+
+    def __init__(self, ctx, world: int, rank: int, uid: bytes):
+        L = _bind()
+        h = C.c_void_p()
+        rc = L.be_comm_init(ctx.h, world, rank, C.create_string_buffer(uid, 128), C.byref(h))
+        if rc != 0:
+            raise BlockExecError(rc, "be_comm_init failed")
+        self.h = h
+
+    def bytes(self, sent: bool) -> int:
+        return _bind().be_comm_bytes(self.h, 1 if sent else 0)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _bind().be_comm_destroy(self.h)
+            self.h = None
+
+
+class Cluster:
+    """The local ranks' runners of a plan and the bh_cluster executing it. ctxs: {rank: ctx}
+    for the ranks of this process (one with a communicator; any number without)."""
+
+    def __init__(self, ctxs: dict, plan: Plan, comm: Comm | None = None, use_graphs=True,
+                 plan_ahead=False):
+        from .runner import Runner
+        L = _bind()
+        self.plan = plan
+        ranks = sorted(ctxs)
+        if ranks != list(range(ranks[0], ranks[0] + len(ranks))):
+            raise ValueError("local ranks must be consecutive")
+        self.runners = {}
+        for spec in plan.runners:
+            if spec.rank in ctxs:
+                self.runners[(spec.rank, spec.slot)] = Runner(
+                    ctxs[spec.rank], spec.wl, mode=1, use_graphs=use_graphs,
+                    plan_ahead=plan_ahead)
+        arr = (C.c_void_p * len(ranks))(*[ctxs[r].h.value for r in ranks])
+        h = C.c_void_p()
+        d = plan.runners[0].wl.shape.d_model
+        rc = L.bh_cluster_create(comm.h if comm else None, ranks[0], len(ranks), arr, d,
+                                 C.byref(h))
+        if rc != 0:
+            raise BlockExecError(rc, "bh_cluster_create failed")
+        self.h = h
+        for (r, s), run in self.runners.items():
+            self._ck(L.bh_cluster_add_runner(h, r, s, run.h))
+        self._keep = []
+        for kind, runs, hops in plan.phases:
+            ra = np.asarray([x for rs in runs for x in rs] or [0], np.int32)
+            ha = (Hop * max(1, len(hops)))(*[Hop(*x) for x in hops])
+            self._keep += [ra, ha]
+            self._ck(L.bh_cluster_add_phase(h, kind, len(runs), ra.ctypes.data, len(hops),
+                                            C.cast(ha, C.c_void_p)))
+
+    def _ck(self, rc):
+        if rc != 0:
+            raise BlockExecError(rc, _bind().bh_cluster_last_error(self.h).decode())
+
+    def prefill(self):
+        self._ck(_bind().bh_cluster_prefill(self.h))
+
+    def decode_step(self, host_in=None, host_out=None):
+        pin = C.c_void_p(host_in.data_ptr() if host_in is not None else 0)
+        pout = C.c_void_p(host_out.data_ptr() if host_out is not None else 0)
+        self._ck(_bind().bh_cluster_decode_step(self.h, 0, pin, pout))
+
+    def stats(self) -> dict:
+        s = ClusterStats()
+        self._ck(_bind().bh_cluster_get_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in ClusterStats._fields_}
+
+    def home(self, rank: int):
+        return self.runners[(rank, 0)]
+
+    def step_stats(self) -> dict:
+        """Summed per-step accounting of this process's runners (last decode step)."""
+        out = {}
+        for run in self.runners.values():
+            for k, v in run.step_stats().items():
+                out[k] = out.get(k, 0) + v
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            _bind().bh_cluster_free(self.h)
+            self.h = None
+        for run in self.runners.values():
+            run.close()
+        self.runners = {}

@@ -95,6 +95,7 @@ struct be_ctx {
   int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
   int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
   int prefill_tc = 1;     // tensor-core prefill attention (BE_PREFILL_TC=0: the per-row kernel)
+  int attn_splits_force = 0;  // decode attention split-K count (BE_ATTN_SPLITS=1..16; 0 = auto)
   // per-launch event timing of exec_batch kernels (be_prof_enable); off on the hot path
   struct ProfRec {
     be_prof_rec r;
@@ -108,6 +109,9 @@ struct be_ctx {
   // speculation (be_exec_speculative): the draft lane's stream, fork/join events, verdict scratch
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_copy = nullptr;  // be_kv_copy_pages: reads of this context's pools wait on it
+  float* attn_part = nullptr;     // be_attention's split-K partials
+  size_t attn_part_elems = 0;
   float* spec_cos = nullptr;
   int* spec_accept = nullptr;
   int spec_cap = 0;
@@ -243,6 +247,7 @@ cudaStream_t pick_stream(be_ctx* ctx, void* s) {
 const int kBNs[5] = {16, 32, 64, 128, 256};
 
 int attn_splits(const be_ctx* ctx, int rows, int H, int max_pages) {
+  if (ctx->attn_splits_force > 0) return ctx->attn_splits_force;  // tests: the split-K path
   const long long ctas = (long long)rows * H;
   const long long want = 4LL * ctx->num_sms;
   if (ctas >= want) return 1;
@@ -291,6 +296,10 @@ extern "C" int be_ctx_create(int device, be_ctx** out) {
   if (const char* g = getenv("BE_GEMM_GRID")) ctx->gemm_grid_cap = atoi(g);
   if (const char* p = getenv("BE_PDL")) ctx->use_pdl = atoi(p) != 0;
   if (const char* p = getenv("BE_PREFILL_TC")) ctx->prefill_tc = atoi(p) != 0;
+  if (const char* p = getenv("BE_ATTN_SPLITS")) {
+    const int v = atoi(p);
+    ctx->attn_splits_force = v < 0 ? 0 : v > 16 ? 16 : v;
+  }
   *out = ctx;
   return BE_OK;
 }
@@ -304,6 +313,8 @@ extern "C" int be_ctx_destroy(be_ctx* ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
+  if (ctx->attn_part) cudaFree(ctx->attn_part);
   if (ctx->spec_cos) cudaFree(ctx->spec_cos);
   if (ctx->spec_accept) cudaFree(ctx->spec_accept);
   if (ctx->gemm_ws) cudaFree(ctx->gemm_ws);
@@ -1108,6 +1119,19 @@ int exec_batch_host(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* 
   for (int64_t i = 0; i < (int64_t)n_pt_rows * pt_stride; ++i)
     if (page_table[i] < -1 || page_table[i] >= pool->n_pages)
       return fail(ctx, BE_ERR_INVALID, "page table entry %lld out of range", (long long)i);
+  // attention reads pages 0..pos>>4 of the token's row without a guard, and the QKV epilogue
+  // appends K/V at kv_slot: every page up to the token's must be mapped, the last one to the
+  // page holding kv_slot
+  for (int t = 0; t < n_tokens; ++t) {
+    const be_token& k = tokens[t];
+    const int32_t* row = page_table + (size_t)k.pt_row * pt_stride;
+    for (int p = 0; p <= (k.pos >> 4); ++p)
+      if (row[p] < 0)
+        return fail(ctx, BE_ERR_INVALID, "token %d: page %d of its page-table row is unmapped", t, p);
+    if (row[k.pos >> 4] != (k.kv_slot >> 4))
+      return fail(ctx, BE_ERR_INVALID, "token %d: kv_slot %d is not on page-table page %d", t,
+                  k.kv_slot, row[k.pos >> 4]);
+  }
   cudaSetDevice(ctx->device);
   cudaStream_t st = stream;
   if (n_tokens > 0)
@@ -1269,13 +1293,31 @@ extern "C" int be_exec_speculative(be_ctx* ctx, const be_spec_stage* verify,
                          g->pt_stride, g->page_table, in, out, s);
   };
   int rc;
+  // Two lanes run stream-K GEMMs at once. A stream-K tile owner spin-waits for its contributor
+  // CTAs, which is safe only while every CTA of the grid can become resident: each lane's GEMMs
+  // get their own share of the SMs (one CTA per SM each, shares summing to the SM count) and no
+  // programmatic dependent launch (at most one GEMM grid per lane in flight). Restored on exit.
+  struct LaneCaps {
+    be_ctx* c;
+    int cap, pdl;
+    explicit LaneCaps(be_ctx* x) : c(x), cap(x->gemm_grid_cap), pdl(x->use_pdl) { c->use_pdl = 0; }
+    void set(int sms) { c->gemm_grid_cap = cap > 0 && cap < sms ? cap : sms; }
+    ~LaneCaps() {
+      c->gemm_grid_cap = cap;
+      c->use_pdl = pdl;
+    }
+  } caps(ctx);
+  const int side_sms = ctx->num_sms / 2, lane_sms = ctx->num_sms - side_sms;
   // K6: the draft lane (scenario.cpp:521-537) - surrogate, then the next block fed by its output
   BE_CUDA(ctx, cudaEventRecord(ctx->ev_fork, lane));
   BE_CUDA(ctx, cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+  caps.set(side_sms);
   if ((rc = run(draft, draft->tokens, n_tokens, d_x_in, d_y_draft, side)) != BE_OK) return rc;
   if ((rc = run(next, next->tokens, n_tokens, d_y_draft, d_z_out, side)) != BE_OK) return rc;
   // the verifying block on the main lane, concurrently
+  caps.set(lane_sms);
   if ((rc = run(verify, verify->tokens, n_tokens, d_x_in, d_y_true, lane)) != BE_OK) return rc;
+  caps.set(ctx->num_sms);
   BE_CUDA(ctx, cudaEventRecord(ctx->ev_join, side));
   BE_CUDA(ctx, cudaStreamWaitEvent(lane, ctx->ev_join, 0));
   // K7 verdict: per-row cosine(draft, true) >= threshold
@@ -1338,6 +1380,17 @@ extern "C" int be_kv_copy_pages(be_ctx* dst_ctx, const be_kv_pool* src_pool, be_
     }
   }
   cudaStream_t st = pick_stream(dst_ctx, stream);
+  if (src_pool->ctx != dst_ctx || st != src_pool->ctx->stream) {
+    // the copy reads pages the source context's stream may still be writing (KV appends of
+    // kernels in flight): order it after everything queued there so far
+    be_ctx* sc = src_pool->ctx;
+    cudaSetDevice(src_dev);
+    if (sc->ev_copy == nullptr)
+      BE_CUDA(dst_ctx, cudaEventCreateWithFlags(&sc->ev_copy, cudaEventDisableTiming));
+    BE_CUDA(dst_ctx, cudaEventRecord(sc->ev_copy, sc->stream));
+    cudaSetDevice(dst_dev);
+    BE_CUDA(dst_ctx, cudaStreamWaitEvent(st, sc->ev_copy, 0));
+  }
   const size_t page_bytes = (size_t)src_pool->page_elems * sizeof(bf16);
   int i = 0;
   while (i < n) {
@@ -1364,11 +1417,13 @@ extern "C" int be_kv_migrate(be_ctx* ctx, be_block* blk, const be_kv_pool* src_p
       ws == nullptr || n_pages < 0 || n_recompute < 0 || n_recompute > n_pages ||
       (n_pages > 0 && (src_slots == nullptr || dst_slots == nullptr)))
     return ctx ? fail(ctx, BE_ERR_INVALID, "be_kv_migrate: bad arguments") : BE_ERR_INVALID;
-  if (n_recompute > 0 && (d_head_rows == nullptr || head_tokens <= (n_recompute - 1) * 16 ||
+  // with tail pages copied, the head must fill its last recomputed page (no token uncovered)
+  const int head_min = n_recompute < n_pages ? n_recompute * 16 : (n_recompute - 1) * 16 + 1;
+  if (n_recompute > 0 && (d_head_rows == nullptr || head_tokens < head_min ||
                           head_tokens > n_recompute * 16))
     return fail(ctx, BE_ERR_INVALID,
                 "be_kv_migrate: %d recompute pages need %d..%d head tokens (got %d)",
-                n_recompute, (n_recompute - 1) * 16 + 1, n_recompute * 16, head_tokens);
+                n_recompute, head_min, n_recompute * 16, head_tokens);
   if (dst_pool->ctx != ctx || blk->ctx != ctx)
     return fail(ctx, BE_ERR_INVALID, "be_kv_migrate: block and destination pool must be on ctx");
   cudaSetDevice(ctx->device);
@@ -1644,14 +1699,16 @@ extern "C" int be_attention(be_ctx* ctx, const void* q, const void* pool, int n_
                             const int32_t* row_pt, const int32_t* row_ctx, int rows, int splits,
                             void* out, void* stream) {
   if (ctx == nullptr || rows < 0 || (hd != 64 && hd != 128) || splits < 1) return BE_ERR_INVALID;
-  static float* part = nullptr;
-  static size_t part_elems = 0;
-  if (splits > 1) {
+  cudaSetDevice(ctx->device);
+  if (splits > 1) {  // split-K partials: the context's own scratch (one per GPU / context)
     const size_t need = (size_t)rows * H * splits * (hd + 2);
-    if (need > part_elems) {
-      if (part) cudaFree(part);
-      BE_CUDA(ctx, cudaMalloc(&part, need * sizeof(float)));
-      part_elems = need;
+    if (need > ctx->attn_part_elems) {
+      BE_CUDA(ctx, cudaStreamSynchronize(pick_stream(ctx, stream)));
+      if (ctx->attn_part) cudaFree(ctx->attn_part);
+      ctx->attn_part = nullptr;
+      ctx->attn_part_elems = 0;
+      BE_CUDA(ctx, cudaMalloc(&ctx->attn_part, need * sizeof(float)));
+      ctx->attn_part_elems = need;
     }
   }
   bx::AttnParams ap{};
@@ -1669,7 +1726,7 @@ extern "C" int be_attention(be_ctx* ctx, const void* q, const void* pool, int n_
   ap.H = H;
   ap.scale_log2 = (1.0f / sqrtf((float)hd)) * 1.4426950408889634f;
   ap.out = static_cast<bf16*>(out);
-  ap.part = part;
+  ap.part = ctx->attn_part;
   ap.splits = splits;
   cudaError_t e = bx::launch_attention(ap, rows, hd, pick_stream(ctx, stream));
   return e == cudaSuccess ? BE_OK : fail(ctx, BE_ERR_CUDA, "attention: %s", cudaGetErrorString(e));

@@ -176,25 +176,37 @@ std::vector<std::pair<int, int>> KvStore::move_segment(std::uint64_t request,
   for (auto& id : s.page_ids) {
     Page& p = pages_.at(id);
     if (p.ref == 1) {
-      // private page: its bytes move to the destination pool
-      reserve(dst, p.bytes);
-      unreserve(p.device, p.bytes);
+      // private page: its bytes move to the destination pool (slot first: a full pool throws
+      // before the ledger has changed; a ledger failure hands the slot back)
       const int nslot = alloc_slot(p.pool_key, dst);
+      try {
+        reserve(dst, p.bytes);
+      } catch (...) {
+        free_slot(p.pool_key, dst, nslot);
+        throw;
+      }
+      unreserve(p.device, p.bytes);
       copies.emplace_back(p.slot, nslot);
       free_slot(p.pool_key, p.device, p.slot);
       p.slot = nslot;
       p.device = dst;
     } else {
       // shared page stays for its other readers; this segment gets a fresh private copy
+      const int nslot = alloc_slot(p.pool_key, dst);
+      try {
+        reserve(dst, p.bytes);
+      } catch (...) {
+        free_slot(p.pool_key, dst, nslot);
+        throw;
+      }
       --p.ref;
-      reserve(dst, p.bytes);
       const std::uint64_t cid = next_page_++;
       Page c;
       c.bytes = p.bytes;
       c.ref = 1;
       c.device = dst;
       c.pool_key = p.pool_key;
-      c.slot = alloc_slot(p.pool_key, dst);
+      c.slot = nslot;
       copies.emplace_back(p.slot, c.slot);
       pages_[cid] = c;
       id = cid;

@@ -78,6 +78,7 @@ class Runner {
   int live() const;
   std::int64_t generated() const { return tokens_generated_; }
   void* arena() { return arena_; }
+  int requests() const { return static_cast<int>(reqs_.size()); }
   void* prefill_arena() { return parena_; }
   std::int64_t prefill_rows() const { return prefill_rows_; }
 
@@ -992,6 +993,7 @@ extern "C" int bh_runner_decode_group(bh_runner* h, int group, const int32_t* re
 extern "C" int bh_runner_live_requests(const bh_runner* h) { return h ? h->r->live() : 0; }
 extern "C" int64_t bh_runner_tokens_generated(const bh_runner* h) { return h ? h->r->generated() : 0; }
 extern "C" void* bh_runner_arena(bh_runner* h) { return h ? h->r->arena() : nullptr; }
+extern "C" int bh_runner_requests(const bh_runner* h) { return h ? h->r->requests() : 0; }
 extern "C" void* bh_runner_prefill_arena(bh_runner* h, int64_t* rows) {
   if (h == nullptr) return nullptr;
   if (rows) *rows = h->r->prefill_rows();

@@ -111,7 +111,7 @@ def _profile_classes(path: str | None):
 
 
 def routing_policy(wl: Workload, n_devices: int, profiles: str | None = None,
-                   hbm_bytes: int = 180 * 10**9):
+                   hbm_bytes: int = 180 * 10**9, instances: bool = True):
     """A bh_policy (include/blockpolicy.h) describing replica placement of `wl`: every block on
     each of n_devices GPUs of one NVLink server, priced by the measured B200 cost profiles
     (profiles/b200_profiles.json, scripts/make_profiles.py; §8(f) rank 2). Classes the profile
@@ -148,6 +148,8 @@ def routing_policy(wl: Workload, n_devices: int, profiles: str | None = None,
     pol.add_server(0, 900e9)  # NVLink 5 per direction
     for dev in range(n_devices):
         pol.add_device(dev, 0, "b200", hbm_bytes, 7.7e12, 55e9)
+    if not instances:  # the caller places the blocks (cluster.place_blocks)
+        return pol
     seq = 0
     for dev in range(n_devices):
         for name in wl.block_names:

@@ -322,6 +322,22 @@ def test_kv_move_segment_slots_gives_page_copies():
     assert kv.page_slots(3, "b0") == [2]    # request 2's private page freed slot 2 on device 0
 
 
+def test_kv_move_segment_full_pool_leaves_ledger_unchanged():
+    """A move whose destination pool is full throws before the page's bytes are charged to the
+    destination: the ledger still matches where the pages are (kv.cpp move)."""
+    kv = H.KvStore()
+    kv.attach_pool("b0", 0, 4)
+    kv.attach_pool("b0", 1, 1)
+    kv.create_segment(1, "b0", 0, 64)
+    kv.append_tokens(1, "b0", 32)           # 2 private pages on device 0
+    used0, used1 = kv.used(0), kv.used(1)
+    with pytest.raises(H.LogicError):
+        kv.move_segment_slots(1, "b0", 1)   # the second page finds no slot on device 1
+    # the first page moved (slot and bytes together), the second stayed (slot and bytes)
+    page = used0 // 2
+    assert kv.used(0) == used0 - page and kv.used(1) == used1 + page
+
+
 # ---------------------------------------------------------------- whole-simulation traces
 SIM_CASES = [
     # n_layers, dim, n_lora, first_adapted, prompts, outputs, budget

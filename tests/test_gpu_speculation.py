@@ -41,12 +41,17 @@ def test_surrogate_weights_are_the_base_prefix(ctx):
     s.free()
 
 
-@pytest.mark.parametrize("threshold", [-2.0, 0.95, 2.0])
-def test_speculative_step_matches_oracle(ctx, threshold):
+@pytest.mark.parametrize("threshold,d,n", [(-2.0, 256, 8), (0.95, 256, 8), (2.0, 256, 8),
+                                         (0.95, 512, 256), (None, 512, 256)])
+def test_speculative_step_matches_oracle(ctx, threshold, d, n):
+    """8 rows at C1 width, and C5's batch of 256 rows (configs[4]) at d=512 (hd 128) so the
+    oracle stays fast; threshold None = the median cosine (the batch splits into accepted and
+    rejected rows)."""
     from oracle import oracle as O
-    shape = dev.BlockShape(n_layers=2, d_model=256, n_heads=4, d_ff=768, max_pos=64)
+    heads = d // 64 if d == 256 else d // 128
+    shape = dev.BlockShape(n_layers=2, d_model=d, n_heads=heads, d_ff=3 * d, max_pos=64)
     sur = shape.surrogate(0.5)
-    n, prompt = 8, 5
+    prompt = 5
     d = shape.d_model
     names = {"verify": ("b1", shape), "draft": ("b1", sur), "next": ("b2", shape)}
     gpu, orc, pools, seqs = {}, {}, {}, {}
@@ -75,8 +80,16 @@ def test_speculative_step_matches_oracle(ctx, threshold):
     y_draft, y_true, z = (torch.zeros(n, d, dtype=torch.bfloat16, device="cuda") for _ in range(3))
     dtoks = [(r, r, r * 16 + prompt, prompt, r) for r in range(n)]
     st = {k: (gpu[k], pools[k], ws_main if k == "verify" else ws_side, dtoks, pt) for k in names}
+    if threshold is None:
+        # a dry pass to find the median cosine; then the real step (the KV slots of position
+        # `prompt` are rewritten with the same values)
+        cos0, _, _ = dev.exec_speculative(ctx, st["verify"], st["draft"], st["next"], x,
+                                          y_draft, y_true, z, 0.95)
+        threshold = float(np.median(cos0))
     cos, acc, n_acc = dev.exec_speculative(ctx, st["verify"], st["draft"], st["next"], x,
                                            y_draft, y_true, z, threshold)
+    if n == 256 and threshold == float(np.median(cos)):
+        assert 0 < n_acc < n
     pos = [prompt] * n
     seq_ids = list(range(n))
     yt_ref = orc["verify"].forward(seqs["verify"], seq_ids, pos, f32(x))
@@ -106,7 +119,9 @@ def test_speculative_stage_at_c5_scale(ctx):
     """configs[4] (C5): the cosine equivalence check at batch 256 over 8 tenants on 7B-shaped
     4-layer blocks (verify = a shared block, draft = its 50%-FFN surrogate, next = the following
     shared block). Size-independent properties instead of the CPU oracle:
-      * the verify lane's rows equal a plain be_exec_batch of the block bit for bit;
+      * the verify lane's rows equal a plain be_exec_batch of the block within bf16 rounding
+        (the two lanes split the SMs, so the verify GEMMs run stream-K over half the CTAs and
+        sum their k-slices in another grouping);
       * K7's cosine equals an fp32 torch cosine of the draft/true rows; accept = cos >= thr;
       * the next block's rows equal next(draft) for accepted rows and next(true) for rejected
         ones (a plain run on the selected inputs; other batch composition, so within bf16
@@ -154,7 +169,9 @@ def test_speculative_stage_at_c5_scale(ctx):
     dev.exec_batch(ctx, gpu["verify"], pools["verify"], ws_main, dev.PHASE_DECODE, dtoks, pt, x,
                    y_plain)
     ctx.sync()
-    assert torch.equal(y_plain, y_true)
+    assert rel_l2(f32(y_true), f32(y_plain)) <= 1e-2
+    yc = torch.nn.functional.cosine_similarity(y_true.float(), y_plain.float(), dim=1)
+    assert float(yc.min()) >= 0.999
     a = torch.from_numpy(acc).cuda().bool()[:, None]
     z_in = torch.where(a, y_draft, y_true)
     z_plain = torch.empty_like(x)
