@@ -490,6 +490,147 @@ def run_pipeline(args, world, rank, local, depth, why):
     dist.destroy_process_group()
 
 
+def time_steps(step, stream, steps, barrier):
+    """Device time of `steps` calls of step() on `stream` (CUDA events, synchronised both
+    sides), in ms, plus the host wall time."""
+    import torch
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3
+
+
+def run_cluster(args, world, rank, local):
+    """N > 1 with block placement (paper_2404_18322_b200/cluster.py): every GPU holds the shared
+    blocks and serves its own copy of the config's request mix (weak scaling); each tenant's
+    private blocks live on the GPU choose_device(locality) picks and run all GPUs' rows for that
+    tenant in one batch; rows hop there and back by NCCL send/recv (be_hop_*, one NCCL group per
+    phase on the compute stream) inside the C++ executor loop (bh_cluster). The replica layout
+    (every GPU holds every block, no hop) is measured in the same run for comparison."""
+    import torch
+    import torch.distributed as dist
+    from paper_2404_18322_b200.cluster import Cluster, Comm, block_plan
+    from paper_2404_18322_b200.device import Context
+    from paper_2404_18322_b200.runner import Runner
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peaks_kind = load_peaks()
+    wl = make_workload(args)
+    d = wl.shape.d_model
+    ctx = Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream.value)
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(Comm.unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    comm = Comm(ctx, world, rank, bytes(uid.cpu().numpy().tobytes()))
+    plan = block_plan(wl, world)
+    cl = Cluster({rank: ctx}, plan, comm, use_graphs=True, plan_ahead=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.time()
+    cl.prefill()
+    ctx.sync()
+    prefill_s = time.time() - t0
+    home = cl.home(rank)
+    n_live = home.live
+    for _ in range(args.warmup):
+        cl.decode_step()
+    ctx.sync()
+
+    def mx(v):
+        t = torch.tensor([float(v)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    st0 = cl.stats()
+    clocks.mark()
+    ms, _ = time_steps(cl.decode_step, stream, args.steps, dist.barrier)
+    clk = clocks.stop()
+    st1 = cl.stats()
+    ms = mx(ms)
+    value = n_live * world * args.steps / (ms / 1e3)
+    stats = cl.step_stats()
+    step_bytes = stats["weight_bytes"] + stats["kv_bytes"] + stats["act_bytes"]
+    step_bytes_max = mx(step_bytes)
+    sent = (st1["sent_bytes"] - st0["sent_bytes"]) / args.steps
+    recv = (st1["recv_bytes"] - st0["recv_bytes"]) / args.steps
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.randn(n_live, d).to(torch.bfloat16).pin_memory()
+        hout = torch.empty(n_live, d, dtype=torch.bfloat16).pin_memory()
+        cl.decode_step(hin, hout)
+        bufs = [hin, hout]
+
+        def e2e_step():
+            cl.decode_step(bufs[0], bufs[1])
+            bufs.reverse()  # greedy feedback: the step's output rows are the next input
+        e_ms, wall = time_steps(e2e_step, stream, args.steps, dist.barrier)
+        e_ms = mx(max(e_ms, wall))
+        e2e = {"value": round(n_live * world * args.steps / (e_ms / 1e3), 2), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(hin.numel() * 2),
+               "d2h_bytes_per_step": int(hout.numel() * 2),
+               "ms_per_step": round(e_ms / args.steps, 4)}
+    launches = int(stats["launches"])
+    cl.close()
+    comm.close()
+    replicas = None
+    if not args.no_replicas:
+        run = Runner(ctx, wl, mode=1, use_graphs=True, plan_ahead=True)
+        run.run()
+        for _ in range(args.warmup):
+            run.decode_step()
+        ctx.sync()
+        r_ms, _ = time_steps(run.decode_step, stream, args.steps, dist.barrier)
+        r_ms = mx(r_ms)
+        rst = run.step_stats()
+        replicas = {"value": round(run.live * world * args.steps / (r_ms / 1e3), 2),
+                    "ms_per_step": round(r_ms / args.steps, 4),
+                    "bytes_per_step_per_gpu": rst["weight_bytes"] + rst["kv_bytes"]
+                    + rst["act_bytes"],
+                    "layout": "every GPU holds every block and serves its own request mix"}
+        run.close()
+    if rank == 0:
+        hbm = peaks["hbm_gbs"]
+        ms_step = ms / args.steps
+        line = {
+            "metric": "block-chain decode tokens/s", "value": round(value, 2), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, synthetic prompt embeddings; greedy "
+                    "feedback of the last hidden state)",
+            "config": {"workload": wl.name, "tenants": len(wl.chains),
+                       "global_batch": n_live * world, "prompt": wl.req_prompt[0],
+                       "decode": wl.req_output[0],
+                       "parallelism": f"block placement over {world} GPUs (one process each)",
+                       "placement": plan.note,
+                       "hop_bytes_per_step_rank0": {"nccl_sent": sent, "nccl_recv": recv},
+                       "l2": "inputs larger than L2 (weights+KV streamed per step)"},
+            "roofline": None,
+            "step_roofline": {"bound": "hbm", "bytes_per_step_max_gpu": step_bytes_max,
+                              "achieved": round(step_bytes_max / (ms_step / 1e3) / 1e9, 1),
+                              "peak": hbm, "unit": "GB/s",
+                              "frac": round(step_bytes_max / (ms_step / 1e3) / 1e9 / hbm, 4)},
+            "replicas": replicas, "e2e": e2e, "cpu_baseline": None,
+            "gpu_launches": launches * args.steps, "clocks": clk,
+            "prefill_s": round(prefill_s, 2),
+            "note": "gpu_launches: this rank's kernels (NCCL's send/recv kernels not counted)",
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    dist.destroy_process_group()
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
@@ -498,6 +639,8 @@ def run_ours(args, world, rank, local):
     from paper_2404_18322_b200.workloads import CONFIGS
 
     placement = "1 GPU"
+    if world > 1 and args.placement == "blocks":
+        return run_cluster(args, world, rank, local)
     if world > 1:
         from paper_2404_18322_b200.pipeline import choose_layout
         lay = choose_layout(make_workload(args), world)
@@ -723,9 +866,14 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
-    ap.add_argument("--placement", default="auto", choices=["auto", "pipeline", "replica"],
-                    help="N>1: the placement model's choice (auto), chain positions cut into N "
-                         "pipeline stages with NCCL P2P hops, or one replica of the zoo per GPU")
+    ap.add_argument("--placement", default="blocks",
+                    choices=["blocks", "auto", "pipeline", "replica"],
+                    help="N>1: block placement (shared blocks on every GPU, private blocks by "
+                         "choose_device, NCCL hops; default), the position-pipeline model's "
+                         "choice (auto), chain positions cut into N pipeline stages, or one "
+                         "replica of the zoo per GPU")
+    ap.add_argument("--no-replicas", action="store_true",
+                    help="N>1 block placement: skip the replica comparison leg")
     ap.add_argument("--isolated", action="store_true",
                     help="also time the dominant kernels alone (standalone launches, > L2)")
     ap.add_argument("--profile", action="store_true",
