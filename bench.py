@@ -145,42 +145,88 @@ def dist_setup():
 
 
 # ------------------------------------------------------------------------------------ CPU leg
-_CPU_BLOCK = {}
+class CpuDecodeStep:
+    """TEST INFRASTRUCTURE (the cpu_baseline leg and --impl reference only): one whole lockstep
+    decode step of the workload restated on the host by the oracle (fp32 C, OpenMP over
+    `threads`): every block run of the step at its own per-block batch (C2: 6 shared blocks at 64
+    rows, 8 private blocks at 16 rows), each row attending over `ctx` tokens of K/V. Blocks with
+    the same batch size share one restated weight set (the arithmetic does not depend on the
+    values; the host holds ~3.2 GB fp32 per 7B 4-layer block), so memory stays bounded."""
+
+    def __init__(self, wl, threads: int, ctx: int | None = None):
+        import numpy as np
+        from oracle import oracle as O
+        self.wl, self.threads = wl, threads
+        self.rows = [r for r in wl.rows_at_block() if r > 0]
+        self.ctx = ctx or min(wl.req_prompt[0] + wl.req_output[0] // 2, wl.shape.max_pos - 2)
+        self.blocks, self.seqs, self.x = {}, {}, {}
+        for r in sorted(set(self.rows)):
+            ob = O.OracleBlock(wl.shape, f"cpu-step-{r}", seed=wl.seed)
+            seqs = [ob.new_seq(self.ctx + 1) for _ in range(r)]
+            for q in seqs:
+                q.fill(self.ctx)
+            self.blocks[r], self.seqs[r] = ob, seqs
+            self.x[r] = np.random.default_rng(r).standard_normal(
+                (r, wl.shape.d_model)).astype(np.float32)
+
+    def step(self) -> float:
+        """Seconds for one decode step (all block runs, in chain-position order)."""
+        t0 = time.perf_counter()
+        for r in self.rows:
+            self.blocks[r].forward(self.seqs[r], list(range(r)), [self.ctx] * r, self.x[r],
+                                   threads=self.threads)
+        return time.perf_counter() - t0
+
+    def sample(self) -> str:
+        from collections import Counter
+        c = Counter(self.rows)
+        return ("one whole decode step per sample: " + " + ".join(
+            f"{n} block runs at {r} rows" for r, n in sorted(c.items(), reverse=True))
+            + f", context {self.ctx}, oracle fp32 C restatement (OpenMP)")
 
 
-def cpu_block_sample(wl, threads: int, rows_list=(64, 16), ctx: int = 576, reps: int = 1):
-    """Times the oracle (fp32 C restatement, OpenMP) on one block of the workload at each row
-    count; returns {rows: seconds}. TEST-INFRASTRUCTURE use: the CPU baseline only."""
+def blocksim_run(wl):
+    """TEST INFRASTRUCTURE: the reference's own CPU path - blocksim's Simulation::run (the
+    unmodified reference sources in oracle/_ref, scenario.cpp:152-175) on the same requests over
+    a zoo of the config's shape (a foundation plus one LoRA variant per tenant from the first
+    private layer up, partitioned by the reference), single-threaded as the simulator is. It
+    prices block runs from cost tables and computes no tensors. None if oracle/_ref is absent."""
+    import json as _j
     import numpy as np
-    from oracle import oracle as O
-    if wl.name not in _CPU_BLOCK:
-        _CPU_BLOCK[wl.name] = O.OracleBlock(wl.shape, "cpu-sample", seed=wl.seed)
-    ob = _CPU_BLOCK[wl.name]
-    ctx = min(ctx, wl.req_prompt[0] + wl.req_output[0] // 2, wl.shape.max_pos - reps - 2)
-    out = {}
-    for rows in rows_list:
-        seqs = [ob.new_seq(ctx + reps + 1) for _ in range(rows)]
-        for s in seqs:
-            s.fill(ctx)
-        x = np.random.default_rng(0).standard_normal((rows, wl.shape.d_model)).astype(np.float32)
-        best = None
-        for rep in range(reps):
-            t0 = time.perf_counter()
-            ob.forward(seqs, list(range(rows)), [ctx + rep] * rows, x, threads=threads)
-            dt = time.perf_counter() - t0
-            best = dt if best is None else min(best, dt)
-        out[rows] = best
-        del seqs
-    return out
-
-
-def cpu_step_tokens_per_s(wl, times: dict) -> float:
-    rows = wl.rows_at_block()
-    step = 0.0
-    for r in rows:
-        key = min(times, key=lambda k: abs(k - r))
-        step += times[key] * (r / key if key else 1.0) if r > key else times[key]
-    return wl.n_requests / step
+    try:
+        from oracle import refshim as R
+        if not R.available():
+            return None
+        L = R.lib()
+    except Exception:
+        return None
+    s = wl.shape
+    n_pos = max(len(c) for c in wl.chains)
+    shared = set.intersection(*[set(c) for c in wl.chains]) if len(wl.chains) > 1 else set()
+    n_shared = sum(1 for b in wl.chains[0] if b in shared)
+    p = np.ascontiguousarray(wl.req_prompt, np.int32)
+    o = np.ascontiguousarray(wl.req_output, np.int32)
+    t0 = time.perf_counter()
+    h = L.rs_sim_run(n_pos * s.n_layers, s.d_model, len(wl.chains), n_shared * s.n_layers,
+                     wl.n_requests, p.ctypes.data, o.ctypes.data, wl.max_batch_tokens, 0)
+    wall = time.perf_counter() - t0
+    try:
+        err = L.rs_sim_error(h).decode()
+        if err:
+            return {"error": err}
+        rep = _j.loads(L.rs_sim_report(h).decode())
+        nb = L.rs_sim_n_batches(h)
+    finally:
+        L.rs_sim_free(h)
+    return {"wall_s": round(wall, 4), "cores": 1, "kind": "reference",
+            "what": "blocksim Simulation::run (oracle/_ref, unmodified reference sources) on the "
+                    f"config's {wl.n_requests} requests ({wl.req_prompt[0]}+{wl.req_output[0]} "
+                    f"tokens), {len(wl.chains)} tenants sharing the first "
+                    f"{n_shared * s.n_layers} layers; prices blocks by cost tables, computes no "
+                    "tensors",
+            "batches": nb, "generated_tokens": rep.get("generated_tokens"),
+            "simulated_tokens_per_s": rep.get("throughput_tokens_per_s"),
+            "simulated_p95_latency_us": (rep.get("latency") or {}).get("p95_us")}
 
 
 # ------------------------------------------------------------------------------------ GPU leg
@@ -609,13 +655,10 @@ def run_cluster(args, world, rank, local):
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, synthetic prompt embeddings; greedy "
                     "feedback of the last hidden state)",
-            "config": {"workload": wl.name, "tenants": len(wl.chains),
-                       "global_batch": n_live * world, "prompt": wl.req_prompt[0],
-                       "decode": wl.req_output[0],
-                       "parallelism": f"block placement over {world} GPUs (one process each)",
-                       "placement": plan.note,
-                       "hop_bytes_per_step_rank0": {"nccl_sent": sent, "nccl_recv": recv},
-                       "l2": "inputs larger than L2 (weights+KV streamed per step)"},
+            "config": run_config(wl, world),
+            "config_detail": {"placement": plan.note, "processes": "one per GPU",
+                              "hop_bytes_per_step_rank0": {"nccl_sent": sent,
+                                                           "nccl_recv": recv}},
             "roofline": None,
             "step_roofline": {"bound": "hbm", "bytes_per_step_max_gpu": step_bytes_max,
                               "achieved": round(step_bytes_max / (ms_step / 1e3) / 1e9, 1),
@@ -771,12 +814,13 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        times = cpu_block_sample(wl, threads)
-        cpu = {"value": round(cpu_step_tokens_per_s(wl, times), 3), "unit": "tokens/s",
-               "cores": threads, "kind": "port",
-               "sample": "oracle fp32 C restatement (OpenMP): one 4-layer block decode at 64 and "
-                         "16 rows, ctx 576; step = sum over the 14 block runs of the workload "
-                         f"(t64={times[64]:.3f}s, t16={times[16]:.3f}s)"}
+        cs = CpuDecodeStep(wl, threads)
+        cs.step()  # first touch
+        t_step = cs.step()
+        cpu = {"value": round(n_live / t_step, 3), "unit": "tokens/s", "cores": threads,
+               "kind": "port", "sample": cs.sample() + f" ({t_step:.2f} s)",
+               "reference_sim": blocksim_run(wl)}
+        del cs
 
     if rank == 0:
         line = {
@@ -785,16 +829,15 @@ def run_ours(args, world, rank, local):
             "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, "
             "synthetic prompt embeddings; greedy feedback of the last hidden state)",
-            "config": {"workload": wl.name, "model": {"c2": "Llama-2-7B-shaped", "c3": "Llama-2-7B-shaped",
-                                 "c4": "Llama-2-13B-shaped",
-                                 "c5": "Llama-2-7B-shaped",
-                                 "c2lora": "Llama-2-7B-shaped + rank-16 LoRA tenants"}.get(args.config, wl.name), "tenants": len(wl.chains), "global_batch": n_live * world,
-                       "prompt": wl.req_prompt[0], "decode": wl.req_output[0],
-                       "blocks": f"{len(wl.block_names)} blocks x {wl.shape.n_layers} layers",
-                       "rows_per_block": wl.rows_at_block(), "batches_per_step": nb,
-                       "l2": "inputs larger than L2 (weights+KV streamed per step)",
-                       "parallelism": f"replica per GPU x{world}" if world > 1 else "1 GPU",
-                       "placement": placement},
+            "config": run_config(wl, world),
+            "config_detail": {"model": {"c1": "tiny decoder", "c2": "Llama-2-7B-shaped",
+                                        "c3": "Llama-2-7B-shaped", "c4": "Llama-2-13B-shaped",
+                                        "c5": "Llama-2-7B-shaped",
+                                        "c2lora": "Llama-2-7B-shaped + rank-16 LoRA tenants"
+                                        }.get(args.config, wl.name),
+                              "batches_per_step": nb,
+                              "parallelism": f"replica per GPU x{world}" if world > 1 else "1 GPU",
+                              "placement": placement},
             "roofline": roofline, "step_roofline": step_roofline,
             "kernels": prof["families"] if prof else None,
             "kernels_isolated": kr or None,
@@ -827,31 +870,45 @@ def routed_share(wl, world, rank):
 
 
 def run_reference(args, world, rank, local):
-    """The reference arm: the path's arithmetic on the host cores (the reference computes no
-    tensors — blocksim prices a block with CostModel::block_us — so the timed CPU implementation
-    is our fp32 oracle port of the block forward, with all host threads)."""
+    """The reference arm: the path's arithmetic on the host cores, whole decode steps. The
+    reference computes no tensors (blocksim prices a block with CostModel::block_us), so the
+    timed CPU implementation is the oracle port of the block forward (CpuDecodeStep: every block
+    run of a step, all host threads); blocksim's own Simulation::run on the same requests is
+    reported beside it (reference_sim)."""
     if rank != 0:
         return
     wl = make_workload(args)
     threads = os.cpu_count() or 1
-    vals = []
-    for i in range(args.warmup + args.steps):
-        times = cpu_block_sample(wl, threads)
-        if i >= args.warmup:
-            vals.append(cpu_step_tokens_per_s(wl, times))
-    v = statistics.mean(vals)
+    cs = CpuDecodeStep(wl, threads)
+    t_wall = time.perf_counter()
+    for _ in range(args.warmup):
+        cs.step()
+    times = [cs.step() for _ in range(args.steps)]
+    wall = time.perf_counter() - t_wall
+    ms_step = 1e3 * sum(times) / len(times)
+    v = wl.n_requests / (ms_step / 1e3)
+    sim = blocksim_run(wl)
     line = {"impl": "reference", "metric": "block-chain decode tokens/s", "value": round(v, 3),
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(wl.n_requests / v * 1e3, 2), "higher_is_better": True,
+            "ms_per_step": round(ms_step, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl.name, "global_batch": wl.n_requests},
+            "config": run_config(wl, world),
             "cpu_baseline": {"value": round(v, 3), "unit": "tokens/s", "cores": threads,
-                             "kind": "port", "sample": "per step: one 4-layer block decode at 64 "
-                             "and at 16 rows (ctx 576), extrapolated to the 14 block runs of a "
-                             "decode step"},
+                             "kind": "port", "sample": cs.sample(),
+                             "timed_wall_s": round(wall, 2), "reference_sim": sim},
             "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_config(wl, world):
+    """The `config` object of a bench line (both arms): the workload and its shape."""
+    return {"workload": wl.name, "tenants": len(wl.chains), "global_batch": wl.n_requests * world,
+            "prompt": wl.req_prompt[0], "decode": wl.req_output[0],
+            "blocks": f"{len(wl.block_names)} blocks x {wl.shape.n_layers} layers",
+            "rows_per_block": wl.rows_at_block(),
+            "parallelism": "1 GPU" if world == 1 else f"block placement over {world} GPUs",
+            "l2": "inputs larger than L2 (weights+KV streamed per step)"}
 
 
 def main():
