@@ -804,6 +804,10 @@ def run_ours(args, world, rank, local):
         except Exception as exc:  # diagnostics only
             prof["families"]["_in_step_timeline"] = {"error": str(exc)}
     kr = kernel_rooflines(ctx, wl, peaks) if rank == 0 and args.isolated else {}
+    live = None
+    if world == 1 and not args.no_live:
+        run.close()  # the live runner loads its own copy of the zoo
+        live = live_leg(ctx, args, wl)
     hbm = peaks["hbm_gbs"]
     step_bytes = stats["weight_bytes"] + stats["kv_bytes"] + stats["act_bytes"]
     step_roofline = {"bound": "hbm", "bytes_per_step": step_bytes,
@@ -841,6 +845,7 @@ def run_ours(args, world, rank, local):
             "roofline": roofline, "step_roofline": step_roofline,
             "kernels": prof["families"] if prof else None,
             "kernels_isolated": kr or None,
+            "latency": live,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(stats["launches"]) * args.steps,
             "graph_replayed": bool(stats["graph_replayed"]), "clocks": clk,
             "prefill_s": round(prefill_s, 2),
@@ -901,6 +906,35 @@ def run_reference(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def live_leg(ctx, args, wl):
+    """p95 request latency (BASELINE.json metric): the config's request mix (2x its requests,
+    tenants round-robin) arriving as a Poisson process at --qps, served live by one runner
+    (bh_runner_serve: arrivals prefilled as they come, then boarding the next lockstep decode
+    iteration); latency = completion - arrival, ttft = first token - arrival, nearest-rank
+    percentiles and tokens / drain time as the reference reports them (metrics.cpp:30-38,
+    159-190). Wall-clock time stamps on the host after the device finished each token."""
+    import dataclasses
+    from paper_2404_18322_b200.metrics import poisson_arrivals, serving_report
+    from paper_2404_18322_b200.runner import Runner
+    n = args.live_requests or 2 * wl.n_requests
+    T = len(wl.chains)
+    out = wl.req_output[0] if args.output is None else min(wl.req_output[0], 128)
+    lw = dataclasses.replace(wl, req_tenant=[i % T for i in range(n)],
+                             req_prompt=[wl.req_prompt[0]] * n, req_output=[out] * n)
+    arr = poisson_arrivals(n, args.qps, seed=wl.seed)
+    run = Runner(ctx, lw, mode=1, use_graphs=True)
+    try:
+        first, done = run.serve(arr)
+        rep = serving_report(arr, first, done, run.tokens_generated)
+    finally:
+        run.close()
+    rep.update({"qps": args.qps, "arrivals": f"Poisson, seed {wl.seed}",
+                "prompt": lw.req_prompt[0], "output": out,
+                "scheduling": "arrivals prefilled on arrival (token budget "
+                              f"{wl.max_batch_tokens}), then join the next lockstep decode step"})
+    return rep
+
+
 def run_config(wl, world):
     """The `config` object of a bench line (both arms): the workload and its shape."""
     return {"workload": wl.name, "tenants": len(wl.chains), "global_batch": wl.n_requests * world,
@@ -929,6 +963,11 @@ def main():
                          "choose_device, NCCL hops; default), the position-pipeline model's "
                          "choice (auto), chain positions cut into N pipeline stages, or one "
                          "replica of the zoo per GPU")
+    ap.add_argument("--no-live", action="store_true", help="skip the live p95-latency leg")
+    ap.add_argument("--qps", type=float, default=32.0,
+                    help="live leg: Poisson arrival rate (requests/s)")
+    ap.add_argument("--live-requests", type=int, default=None,
+                    help="live leg: requests (default 2x the config's)")
     ap.add_argument("--no-replicas", action="store_true",
                     help="N>1 block placement: skip the replica comparison leg")
     ap.add_argument("--isolated", action="store_true",

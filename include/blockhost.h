@@ -138,6 +138,15 @@ int bh_runner_decode_step(bh_runner* r, const void* host_in, void* host_out, int
  * own CUDA graph. */
 int bh_runner_decode_group(bh_runner* r, int group, const int32_t* reqs, int n,
                            const void* host_in, void* host_out, int* n_batches);
+/* Live serving (lockstep mode, on a fresh runner): request i arrives arrival_us[i] after the
+ * call starts; arrivals are prefilled in arrival order as they come and then board the next
+ * lockstep decode iteration (continuous batching at the iteration boundary, the decode-join rule
+ * of Simulation::try_join_running, scenario.cpp:432-463). Returns when every request finished;
+ * first_token_us[i] / completion_us[i] receive host times (us since the call) taken after the
+ * device finished the batch / step producing the token (MetricsCollector's first_token_us /
+ * completion_us, metrics.cpp:159-190). */
+int bh_runner_serve(bh_runner* r, const int64_t* arrival_us, int64_t* first_token_us,
+                    int64_t* completion_us);
 int bh_runner_live_requests(const bh_runner* r);
 int64_t bh_runner_tokens_generated(const bh_runner* r);
 /* Batch trace since creation. members: request ids, steps, context tokens (may be NULL). */

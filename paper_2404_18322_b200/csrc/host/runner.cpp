@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -75,6 +77,7 @@ class Runner {
   // group -1 / members null: every live request; else one micro-batch (own CUDA graph)
   void decode_step(const void* host_in, void* host_out, int* n_batches, int group = -1,
                    const std::vector<int>* members = nullptr);
+  void serve(const std::int64_t* arrival_us, std::int64_t* first_us, std::int64_t* done_us);
   int live() const;
   std::int64_t generated() const { return tokens_generated_; }
   void* arena() { return arena_; }
@@ -143,6 +146,9 @@ class Runner {
   Batch running_;
   PlannedBatch running_plan_;
   std::vector<int> step_done_order_;  // lockstep: completion order of the last step
+  // live serving: requests whose first token / last token the bookkeeping just produced
+  bool serving_ = false;
+  std::vector<int> just_first_, just_done_;
   bool in_lockstep_step_ = false;
   std::int64_t tokens_generated_ = 0;
   int batches_run_ = 0;
@@ -557,8 +563,10 @@ void Runner::advance_from(Request& r, int step) {
     r.generated = 1;
     ++tokens_generated_;
     r.ctx = r.prompt + 1;
+    if (serving_) just_first_.push_back(r.idx);
     if (r.generated >= r.output) {
       r.done = true;
+      if (serving_) just_done_.push_back(r.idx);
       kv_.release_request(r.id);
       return;
     }
@@ -577,6 +585,7 @@ void Runner::advance_from(Request& r, int step) {
   r.ctx += 1;
   if (r.generated >= r.output) {
     r.done = true;
+    if (serving_) just_done_.push_back(r.idx);
     kv_.release_request(r.id);
     return;
   }
@@ -927,6 +936,91 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
   }
 }
 
+// Live serving (lockstep mode). Requests arrive at arrival_us (relative to the call) and are
+// admitted in arrival order; every admission round prefills the new arrivals through their
+// chains (pop_batch under the token budget, batches run as they form, as one device lane does:
+// Simulation::pump, scenario.cpp:465-557) and the new decoders board the next lockstep decode
+// iteration with everyone already decoding - continuous batching at the iteration boundary, the
+// rule try_join_running applies to decode arrivals (scenario.cpp:432-463). Time stamps are taken
+// on the host after the stream has drained the batch or step that produced the token.
+void Runner::serve(const std::int64_t* arrival_us, std::int64_t* first_us, std::int64_t* done_us) {
+  if (mode_ != 1) throw BeError(BE_ERR_STATE, "serve needs lockstep mode");
+  if (batches_run_ != 0 || has_running_) throw BeError(BE_ERR_STATE, "serve on a used runner");
+  const int n = static_cast<int>(reqs_.size());
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) {
+    if (arrival_us[i] < 0) throw BeError(BE_ERR_INVALID, "negative arrival time");
+    order[i] = i;
+    first_us[i] = done_us[i] = -1;
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return arrival_us[a] < arrival_us[b]; });
+  const bool saved_plan_ahead = plan_ahead_;
+  plan_ahead_ = false;  // admissions change the next step's membership
+  serving_ = true;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto now_us = [&] {
+    return std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() -
+                                                                  t0).count();
+  };
+  auto stamp = [&](std::vector<int>& v, std::int64_t* out) {
+    const std::int64_t t = now_us();
+    for (int idx : v) out[idx] = t;
+    v.clear();
+  };
+  size_t next = 0;
+  int completed = 0;
+  try {
+    while (completed < n) {
+      bool admitted = false;
+      while (next < order.size() && arrival_us[order[next]] <= now_us()) {
+        dispatch(reqs_[order[next++]]);
+        admitted = true;
+      }
+      if (admitted) {
+        // prefill the arrivals: batches run one at a time (execute_direct drains the stream)
+        // new decoders board the next decode iteration after everyone already decoding
+        auto boarded = [&] {
+          for (int idx : just_first_)
+            if (!reqs_[idx].done) step_done_order_.push_back(idx);
+          stamp(just_first_, first_us);
+        };
+        pump();
+        while (has_running_) {
+          finish_running();
+          boarded();
+        }
+        if (!dry_) ck(cudaStreamSynchronize(st_), "serve prefill");
+        boarded();
+        completed += static_cast<int>(just_done_.size());
+        stamp(just_done_, done_us);
+        continue;  // arrivals that came during the prefill board before the next step
+      }
+      if (!step_done_order_.empty()) {
+        int nb = 0;
+        decode_step(nullptr, nullptr, &nb);
+        if (!dry_) ck(cudaStreamSynchronize(st_), "serve step");
+        completed += static_cast<int>(just_done_.size());
+        stamp(just_done_, done_us);
+        continue;
+      }
+      if (next < order.size()) {
+        // idle until the next arrival
+        const std::int64_t wait = arrival_us[order[next]] - now_us();
+        if (wait > 200) std::this_thread::sleep_for(std::chrono::microseconds(wait - 100));
+      } else {
+        throw BeError(BE_ERR_STATE, "serve: requests left but nothing to run");
+      }
+    }
+  } catch (...) {
+    serving_ = false;
+    plan_ahead_ = saved_plan_ahead;
+    throw;
+  }
+  serving_ = false;
+  plan_ahead_ = saved_plan_ahead;
+}
+
 }  // namespace bh
 
 // ------------------------------------------------------------------------------ C ABI
@@ -989,6 +1083,12 @@ extern "C" int bh_runner_decode_group(bh_runner* h, int group, const int32_t* re
   if (h == nullptr || group < 0 || (n > 0 && reqs == nullptr)) return BE_ERR_INVALID;
   std::vector<int> members(reqs, reqs + n);
   return guard(h, [&] { h->r->decode_step(in, out, n_batches, group, &members); });
+}
+extern "C" int bh_runner_serve(bh_runner* h, const int64_t* arrival_us, int64_t* first_token_us,
+                               int64_t* completion_us) {
+  if (h == nullptr || arrival_us == nullptr || first_token_us == nullptr || completion_us == nullptr)
+    return BE_ERR_INVALID;
+  return guard(h, [&] { h->r->serve(arrival_us, first_token_us, completion_us); });
 }
 extern "C" int bh_runner_live_requests(const bh_runner* h) { return h ? h->r->live() : 0; }
 extern "C" int64_t bh_runner_tokens_generated(const bh_runner* h) { return h ? h->r->generated() : 0; }

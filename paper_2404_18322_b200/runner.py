@@ -54,6 +54,7 @@ def _bind():
         ("bh_runner_prefill_arena", P, [P, C.POINTER(C.c_int64)]),
         ("bh_runner_decode_group", I, [P, I, P, I, P, P, P]),
         ("bh_runner_step_stats", I, [P, P]),
+        ("bh_runner_serve", I, [P, P, P, P]),
     ]:
         fn = getattr(L, name)
         fn.restype, fn.argtypes = res, args
@@ -134,6 +135,18 @@ class Runner:
         self._check(lib().bh_runner_decode_group(self.h, group, req.ctypes.data, req.size, pin,
                                                  pout, C.byref(n)))
         return n.value
+
+    def serve(self, arrival_us):
+        """Live serving on a fresh lockstep runner (bh_runner_serve): request i arrives
+        arrival_us[i] after the call; returns (first_token_us, completion_us) arrays."""
+        arr = np.ascontiguousarray(arrival_us, np.int64)
+        if arr.size != self.wl.n_requests:
+            raise ValueError("one arrival time per request")
+        first = np.full(arr.size, -1, np.int64)
+        done = np.full(arr.size, -1, np.int64)
+        self._check(lib().bh_runner_serve(self.h, arr.ctypes.data, first.ctypes.data,
+                                          done.ctypes.data))
+        return first, done
 
     def prefill_arena(self):
         """(device pointer, rows) of the prompt hidden-state rows (all requests, in order)."""
