@@ -1121,8 +1121,8 @@ int exec_batch_host(be_ctx* ctx, be_block* blk, be_kv_pool* pool, be_workspace* 
       return fail(ctx, BE_ERR_INVALID, "page table entry %lld out of range", (long long)i);
   // attention reads pages 0..pos>>4 of the token's row without a guard, and the QKV epilogue
   // appends K/V at kv_slot: every page up to the token's must be mapped, the last one to the
-  // page holding kv_slot
-  for (int t = 0; t < n_tokens; ++t) {
+  // page holding kv_slot (blocks without attention components touch no KV page)
+  for (int t = 0; t < n_tokens && blk->n_att > 0; ++t) {
     const be_token& k = tokens[t];
     const int32_t* row = page_table + (size_t)k.pt_row * pt_stride;
     for (int p = 0; p <= (k.pos >> 4); ++p)
