@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(192, CTAS)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* fixbar = tempty + 2;     // the owner's staged partials (split-tile fixup)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(fixbar + 2);  // keeps rs/lu 16B-aligned
   float* rs_smem = reinterpret_cast<float*>(tmem_holder + 4);  // [2][BN] per-token rstd
   float* lu_smem = rs_smem + 2 * BN;                           // k*Lora: [BN][r] u slices
   int* li_smem = reinterpret_cast<int*>(lu_smem + BN * kLoraRank);  // k*Lora: [BN] adapters
@@ -372,6 +373,7 @@ __global__ void __launch_bounds__(192, CTAS)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
+    mbar_init(fixbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_holder);
@@ -585,35 +587,45 @@ __global__ void __launch_bounds__(192, CTAS)
           __syncwarp();
           named_bar_sync(1, 128);  // everyone's loads are ordered after the acquire
           if constexpr (BN <= 64) {
-            // whole tile in registers: one L2 round trip per contributor, not one per chunk
+            // whole tile in registers; the contributors' partials are staged into the ring
+            // (idle now: this is the CTA's last segment and its MMAs are complete) by bulk
+            // copies, every partial of a round in flight at once - one L2 round trip per round
+            // instead of one per contributor - and summed from shared memory in contributor
+            // order (deterministic)
             float acc[BN];
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 16)
               tmem_ld16(t_lane + c0, *reinterpret_cast<float(*)[16]>(acc + c0));
-            // contributors in rounds of R with all their loads in flight (16 float4 per lane)
-            constexpr int R = BN >= 64 ? 1 : 64 / BN;
-            for (int o0 = 1; o0 < n_contrib; o0 += R) {
-              float4 v[R][BN / 4];
+            constexpr int kPartBytes = BN * kBM * 4;
+            constexpr int kPerRound = STAGES * S::kStageBytes / kPartBytes;
+            static_assert(kPerRound >= 1, "ring smaller than one partial tile");
+            const float4* staged = reinterpret_cast<const float4*>(smem);
+            uint32_t fph = 0;
+            for (int o0 = 1; o0 < n_contrib; o0 += kPerRound) {
+              const int nr = n_contrib - o0 < kPerRound ? n_contrib - o0 : kPerRound;
+              if (warp == 2 && lane == 0) {
+                // the acquire above ordered the contributors' stores; order the async-proxy
+                // reads after it
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                mbar_arrive_expect_tx(fixbar, (uint32_t)(nr * kPartBytes));
+                for (int j = 0; j < nr; ++j)
+                  bulk_load(smem + j * kPartBytes, part4(c_first + o0 + j), kPartBytes, fixbar,
+                            kEvictFirst);
+              }
+              mbar_wait(fixbar, fph);
+              fph ^= 1u;
+              for (int j = 0; j < nr; ++j) {
+                const float4* p = staged + (size_t)j * (kPartBytes / 16) + row;
 #pragma unroll
-              for (int j = 0; j < R; ++j) {
-                if (o0 + j < n_contrib) {
-                  const float4* p = part4(c_first + o0 + j) + row;
-#pragma unroll
-                  for (int k = 0; k < BN / 4; ++k) v[j][k] = __ldcg(p + k * kBM);
+                for (int k = 0; k < BN / 4; ++k) {
+                  const float4 v = p[k * kBM];
+                  acc[4 * k] += v.x;
+                  acc[4 * k + 1] += v.y;
+                  acc[4 * k + 2] += v.z;
+                  acc[4 * k + 3] += v.w;
                 }
               }
-#pragma unroll
-              for (int j = 0; j < R; ++j) {
-                if (o0 + j < n_contrib) {
-#pragma unroll
-                  for (int k = 0; k < BN / 4; ++k) {
-                    acc[4 * k] += v[j][k].x;
-                    acc[4 * k + 1] += v[j][k].y;
-                    acc[4 * k + 2] += v[j][k].z;
-                    acc[4 * k + 3] += v[j][k].w;
-                  }
-                }
-              }
+              if (o0 + kPerRound < n_contrib) named_bar_sync(1, 128);  // the ring is reused
             }
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 16) {
