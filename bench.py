@@ -804,10 +804,13 @@ def run_ours(args, world, rank, local):
         except Exception as exc:  # diagnostics only
             prof["families"]["_in_step_timeline"] = {"error": str(exc)}
     kr = kernel_rooflines(ctx, wl, peaks) if rank == 0 and args.isolated else {}
-    live = None
+    live = spec = None
     if world == 1 and not args.no_live:
         run.close()  # the live runner loads its own copy of the zoo
         live = live_leg(ctx, args, wl)
+    if world == 1 and (args.spec or (args.spec is None and args.config == "c5")):
+        run.close()
+        spec = spec_leg(ctx, args, wl, peaks, stream)
     hbm = peaks["hbm_gbs"]
     step_bytes = stats["weight_bytes"] + stats["kv_bytes"] + stats["act_bytes"]
     step_roofline = {"bound": "hbm", "bytes_per_step": step_bytes,
@@ -845,7 +848,7 @@ def run_ours(args, world, rank, local):
             "roofline": roofline, "step_roofline": step_roofline,
             "kernels": prof["families"] if prof else None,
             "kernels_isolated": kr or None,
-            "latency": live,
+            "latency": live, "speculation": spec,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(stats["launches"]) * args.steps,
             "graph_replayed": bool(stats["graph_replayed"]), "clocks": clk,
             "prefill_s": round(prefill_s, 2),
@@ -917,6 +920,12 @@ def live_leg(ctx, args, wl):
     from paper_2404_18322_b200.metrics import poisson_arrivals, serving_report
     from paper_2404_18322_b200.runner import Runner
     n = args.live_requests or 2 * wl.n_requests
+    # every live request holds full-length KV in every block of its chain: stay within HBM
+    per_req = max(len(c) for c in wl.chains) * (wl.req_prompt[0] + wl.req_output[0] + 32) \
+        * wl.shape.kv_bytes_per_token
+    weights = len(wl.block_names) * wl.shape.param_bytes
+    while n > wl.n_requests and weights + n * per_req > 140e9:
+        n -= wl.n_requests
     T = len(wl.chains)
     out = wl.req_output[0] if args.output is None else min(wl.req_output[0], 128)
     lw = dataclasses.replace(wl, req_tenant=[i % T for i in range(n)],
@@ -933,6 +942,80 @@ def live_leg(ctx, args, wl):
                 "scheduling": "arrivals prefilled on arrival (token budget "
                               f"{wl.max_batch_tokens}), then join the next lockstep decode step"})
     return rep
+
+
+def k7_roofline(ctx, rows, d, peaks):
+    """K7 (the cosine verdict kernel, be_cosine) timed alone at the speculative batch size:
+    algorithmic bytes 2 * rows * d * 2 (both bf16 inputs read once) per launch, launches cycling
+    over 32 input pairs (> L2), CUDA events on the launching stream."""
+    import torch
+    from paper_2404_18322_b200 import device as dev
+    stream = torch.cuda.ExternalStream(ctx.stream.value)
+    pairs = [(torch.randn(rows, d, device="cuda").to(torch.bfloat16),
+              torch.randn(rows, d, device="cuda").to(torch.bfloat16)) for _ in range(32)]
+    cos = torch.empty(rows, device="cuda")
+    acc = torch.empty(rows, device="cuda", dtype=torch.int32)
+    for a, b in pairs[:4]:
+        dev.cosine(ctx, a, b, 0.95, cos, acc)
+    ctx.sync()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    reps = 128
+    e0.record(stream)
+    for i in range(reps):
+        a, b = pairs[i % 32]
+        dev.cosine(ctx, a, b, 0.95, cos, acc)
+    e1.record(stream)
+    ctx.sync()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    byts = 2 * rows * d * 2
+    return {"kernel": "cosine_rows_kernel (K7)", "shape": f"{rows} rows x {d}", "bound": "hbm",
+            "us_per_launch": round(us, 2), "bytes_per_launch": byts,
+            "achieved": round(byts / (us * 1e-6) / 1e9, 1), "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": round(byts / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 4),
+            "note": "a 4 MB launch is latency-bound: the verdict costs a few us per speculative "
+                    "block run"}
+
+
+def spec_leg(ctx, args, wl, peaks, stream):
+    """Speculative execution inside the lockstep executor loop: the blocks the
+    reference's marking rule picks (pipeline.speculation_blocks = bh_policy_speculation_marks)
+    run with their 50%-FFN surrogate on a second stream feeding the next block early, K7
+    (cosine >= threshold) accepting rows, rejected rows re-running the next block. Tokens/s
+    with speculation against the plain step of the same runner, accept rate, K7 roofline."""
+    from paper_2404_18322_b200.pipeline import speculation_blocks
+    from paper_2404_18322_b200.runner import Runner
+    blocks, marked = speculation_blocks(wl)
+    out = {"marked_blocks": marked,
+           "speculated_blocks": [wl.block_names[b] for b in blocks],
+           "threshold": args.spec_threshold, "surrogate": "block with its FFN pruned to 50%"}
+    if not blocks:
+        out["note"] = "no marked block whose rows all continue to one block"
+        return out
+    run = Runner(ctx, wl, mode=1, use_graphs=True, spec_blocks=blocks,
+                 spec_threshold=args.spec_threshold)
+    try:
+        run.run()
+        for _ in range(3):
+            run.decode_step()
+        ctx.sync()
+        n = run.live
+        steps = max(3, min(args.steps, 10))
+        ms, _ = time_steps(run.decode_step, stream, steps, lambda: None)
+        st = run.spec_stats()
+    finally:
+        run.close()
+    rows = max(wl.rows_at_block()[b] for b in blocks)
+    out.update({"tokens_per_s": round(n * steps / (ms / 1e3), 2),
+                "ms_per_step": round(ms / steps, 4), "steps": steps,
+                "accept_rate": round(st["accept_rate"], 4) if st["accept_rate"] is not None
+                else None, "rows_verified": st["rows"],
+                "cos_mean": st["cos_mean"], "cos_min": st["cos_min"],
+                "k7": k7_roofline(ctx, rows, wl.shape.d_model, peaks),
+                "note": "one GPU: draft and verify share its SMs and HBM, so the speculative step "
+                        "streams the surrogate's weights on top of the block's - slower; the "
+                        "paper's gain needs the next block on another GPU"})
+    return out
 
 
 def run_config(wl, world):
@@ -964,6 +1047,10 @@ def main():
                          "choice (auto), chain positions cut into N pipeline stages, or one "
                          "replica of the zoo per GPU")
     ap.add_argument("--no-live", action="store_true", help="skip the live p95-latency leg")
+    ap.add_argument("--spec", dest="spec", action="store_true", default=None,
+                    help="add the speculative-execution leg (default: on for --config c5)")
+    ap.add_argument("--no-spec", dest="spec", action="store_false")
+    ap.add_argument("--spec-threshold", type=float, default=0.95)
     ap.add_argument("--qps", type=float, default=32.0,
                     help="live leg: Poisson arrival rate (requests/s)")
     ap.add_argument("--live-requests", type=int, default=None,

@@ -113,6 +113,17 @@ typedef struct {
   const char* const* block_lora_name; /* [n_blocks] adapter names of the LoRA variants
                                          (be_lora_load); LoRA variants of one base at a chain
                                          position decode in one launch (be_exec_lora_group_dev) */
+  /* speculation (§8 a14; scenario.cpp:502-548, 740-807): blocks marked for speculative
+   * execution (e.g. by bh_policy_speculation_marks). In a lockstep decode step, a marked block
+   * whose rows all continue to one next block runs as be_exec_speculative: its surrogate (the
+   * block with its FFN pruned to the first spec_keep fraction of channels)
+   * feeds the next block early on a second stream while the block itself verifies; K7 accepts
+   * a row when cos(draft, true) >= spec_threshold, rejected rows re-run the next block. Steps
+   * with speculation run without CUDA graphs (the verdict is read back on the host). */
+  int n_spec_blocks;
+  const int32_t* spec_blocks;
+  float spec_threshold; /* 0.95 in the paper */
+  float spec_keep;      /* surrogate FFN fraction, e.g. 0.5 */
 } bh_workload;
 
 typedef struct {
@@ -170,6 +181,45 @@ typedef struct {
   int graph_replayed;    /* 1 when the step ran as a CUDA graph replay */
 } bh_step_stats;
 int bh_runner_step_stats(const bh_runner* r, bh_step_stats* out);
+/* Speculation counters since creation: speculative block runs, rows verified, rows accepted,
+ * and the sum / minimum of the K7 cosines. */
+typedef struct {
+  int64_t runs, rows, accepted;
+  double cos_sum, cos_min;
+} bh_spec_stats;
+int bh_runner_spec_stats(const bh_runner* r, bh_spec_stats* out);
+
+/* ---- executor: the drop-in for Simulation::batch_duration_us (scenario.cpp:493) ----
+ * A host that forms batches itself (the reference Simulation) passes each popped ExecBatch to
+ * bh_executor_run_batch: the batch's block (loaded on first use from its id and component kinds,
+ * 'a' / 'f' per ComponentKind, zoo.hpp:12) runs on the GPU over the members' rows and
+ * block-local paged KV (page slots per (request, block) segment). Prefill members update their
+ * prompt rows in place; a chain-final prefill member's last prompt row becomes its decode row
+ * (the first token); decode members update their decode row in place (position =
+ * context_tokens - 1). Synchronous (the caller's event loop continues after the block ran). */
+typedef struct bh_executor bh_executor;
+typedef struct {
+  int d_model, n_heads, d_ff, max_pos;
+  int max_batch_tokens;
+  float init_scale;
+  uint64_t seed; /* weights "weights:<block>:...", prompts "inputs:req<id>" as bh_runner */
+} bh_executor_desc;
+typedef struct {
+  int32_t request_id;     /* QueueEntry::request_id, 1-based */
+  int32_t chain_step;
+  int32_t tokens;         /* prefill: prompt tokens; decode: 1 */
+  int32_t context_tokens; /* QueueEntry::context_tokens */
+  int32_t chain_final;    /* 1: the step is the request's last block */
+} bh_member;
+int bh_executor_create(be_ctx* ctx, const bh_executor_desc* d, int n_requests,
+                       const int32_t* req_prompt, const int32_t* req_output, bh_executor** out);
+int bh_executor_free(bh_executor* x);
+const char* bh_executor_last_error(const bh_executor* x);
+int bh_executor_run_batch(bh_executor* x, const char* block_id, const char* components, int phase,
+                          int n_members, const bh_member* members);
+/* decode = 1: the decode rows [n_requests][d]; 0: the prompt rows; bf16 to host. */
+int bh_executor_read_rows(bh_executor* x, int decode, void* host_out);
+int bh_executor_stats(const bh_executor* x, int64_t* batches, int64_t* tokens);
 
 /* ---- cluster: the executor loop over several GPUs with block placement (§8 a11 / a15 / e) ----
  * Blocks are placed on ranks (one GPU each); a token step is a fixed list of phases. In phase k

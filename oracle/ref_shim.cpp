@@ -6,6 +6,9 @@
 // zoo.cpp:78-88), migration planning (plan_migration, kv.cpp:16-58), percentiles
 // (metrics.cpp:30-38) and whole-simulation batch traces (Simulation::pump/on_batch_finish,
 // scenario.cpp:465-578).
+#include <dlfcn.h>
+
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <deque>
@@ -306,10 +309,89 @@ struct rs_sim {
   std::string report;
 };
 
+// The drop-in run (rs_sim_run_gpu): the same Simulation drives the product's batch executor
+// (bh_executor_run_batch, include/blockhost.h - the call that replaces batch_duration_us at
+// scenario.cpp:493) through the Engine's trace hook, which sees every kBatchFinish event before
+// its handler: each batch the reference formed runs on the GPU, in the reference's order, with
+// the reference's members. The product library is opened by path (dlopen), so this checker
+// carries no link dependency on it.
+struct GpuHook {
+  void* lib = nullptr;
+  void* ctx = nullptr;
+  void* exec = nullptr;
+  int (*run)(void*, const char*, const char*, int, int, const void*) = nullptr;
+  const char* (*err)(const void*) = nullptr;
+  std::vector<char> rows;  // decode rows read back at the end
+  int64_t batches = 0;
+};
+
+static void run_sim(rs_sim* h, int n_layers, int dim, int n_lora, int first_adapted,
+                    int n_requests, const int32_t* prompts, const int32_t* outputs,
+                    int max_batch_tokens, int64_t arrival_gap_us, GpuHook* gpu);
+
 rs_sim* rs_sim_run(int n_layers, int dim, int n_lora, int first_adapted, int n_requests,
                    const int32_t* prompts, const int32_t* outputs, int max_batch_tokens,
                    int64_t arrival_gap_us) {
   auto* h = new rs_sim();
+  run_sim(h, n_layers, dim, n_lora, first_adapted, n_requests, prompts, outputs,
+          max_batch_tokens, arrival_gap_us, nullptr);
+  return h;
+}
+
+// bh_executor_desc / bh_member of include/blockhost.h (same layout)
+struct rs_exec_desc {
+  int d_model, n_heads, d_ff, max_pos, max_batch_tokens;
+  float init_scale;
+  uint64_t seed;
+};
+struct rs_member {
+  int32_t request_id, chain_step, tokens, context_tokens, chain_final;
+};
+
+rs_sim* rs_sim_run_gpu(const char* product_lib, int device, int n_layers, int dim, int n_heads,
+                       int n_lora, int first_adapted, int n_requests, const int32_t* prompts,
+                       const int32_t* outputs, int max_batch_tokens, int64_t arrival_gap_us,
+                       uint64_t seed, float init_scale, void* decode_rows_out) {
+  auto* h = new rs_sim();
+  GpuHook g;
+  try {
+    g.lib = dlopen(product_lib, RTLD_NOW | RTLD_LOCAL);
+    if (g.lib == nullptr) throw std::runtime_error(std::string("dlopen: ") + dlerror());
+    auto sym = [&](const char* n) {
+      void* f = dlsym(g.lib, n);
+      if (f == nullptr) throw std::runtime_error(std::string("missing symbol ") + n);
+      return f;
+    };
+    auto ctx_create = reinterpret_cast<int (*)(int, void**)>(sym("be_ctx_create"));
+    auto ctx_destroy = reinterpret_cast<int (*)(void*)>(sym("be_ctx_destroy"));
+    auto ex_create = reinterpret_cast<int (*)(void*, const rs_exec_desc*, int, const int32_t*,
+                                              const int32_t*, void**)>(sym("bh_executor_create"));
+    auto ex_free = reinterpret_cast<int (*)(void*)>(sym("bh_executor_free"));
+    auto ex_read = reinterpret_cast<int (*)(void*, int, void*)>(sym("bh_executor_read_rows"));
+    g.run = reinterpret_cast<int (*)(void*, const char*, const char*, int, int, const void*)>(
+        sym("bh_executor_run_batch"));
+    g.err = reinterpret_cast<const char* (*)(const void*)>(sym("bh_executor_last_error"));
+    if (ctx_create(device, &g.ctx) != 0) throw std::runtime_error("be_ctx_create failed");
+    int max_ctx = 0;
+    for (int i = 0; i < n_requests; ++i) max_ctx = std::max(max_ctx, prompts[i] + outputs[i]);
+    rs_exec_desc d{dim, n_heads, 3 * dim, max_ctx + 16, max_batch_tokens, init_scale, seed};
+    if (ex_create(g.ctx, &d, n_requests, prompts, outputs, &g.exec) != 0)
+      throw std::runtime_error("bh_executor_create failed");
+    run_sim(h, n_layers, dim, n_lora, first_adapted, n_requests, prompts, outputs,
+            max_batch_tokens, arrival_gap_us, &g);
+    if (h->err.empty() && decode_rows_out != nullptr && ex_read(g.exec, 1, decode_rows_out) != 0)
+      h->err = std::string("read rows: ") + g.err(g.exec);
+    ex_free(g.exec);
+    ctx_destroy(g.ctx);
+  } catch (const std::exception& e) {
+    h->err = e.what();
+  }
+  return h;
+}
+
+static void run_sim(rs_sim* h, int n_layers, int dim, int n_lora, int first_adapted,
+                    int n_requests, const int32_t* prompts, const int32_t* outputs,
+                    int max_batch_tokens, int64_t arrival_gap_us, GpuHook* gpu) {
   try {
     Zoo zoo;
     std::vector<ComponentDescriptor> base;
@@ -409,10 +491,27 @@ rs_sim* rs_sim_run(int n_layers, int dim, int n_lora, int first_adapted, int n_r
       h->req_model.push_back((int)(r.app_id % sim.plan().served_models.size()));
     Simulation* sp = &sim;
     std::map<std::string, int> inst_index;
-    sim.engine().set_trace_hook([h, sp, &bidx, &inst_index](SimTime, std::uint64_t, EventKind kind) {
+    sim.engine().set_trace_hook([h, sp, &bidx, &inst_index, gpu, &pz](SimTime, std::uint64_t,
+                                                                      EventKind kind) {
       if (kind != EventKind::kBatchFinish) return;
       for (const auto& [dev, rb] : sp->running_) {
         const Instance* in = sp->pool().find(rb.instance_id);
+        if (gpu != nullptr) {
+          // the batch runs on the GPU now, before the reference advances its members
+          std::string comps;
+          for (const auto& c : pz.block_components(in->block_id))
+            comps += c.kind == ComponentKind::kAttention ? "a" : "f";
+          std::vector<rs_member> mem;
+          for (const auto& m : rb.batch.members) {
+            const auto& r = sp->live_.at(static_cast<std::uint64_t>(m.request_id));
+            mem.push_back({(int32_t)m.request_id, m.chain_step, m.tokens, m.context_tokens,
+                           m.chain_step + 1 == (int)r.chain->size() ? 1 : 0});
+          }
+          if (gpu->run(gpu->exec, in->block_id.c_str(), comps.c_str(),
+                       rb.batch.phase == Phase::kDecode ? 1 : 0, (int)mem.size(), mem.data()) != 0)
+            throw std::runtime_error(std::string("bh_executor_run_batch: ") + gpu->err(gpu->exec));
+          ++gpu->batches;
+        }
         auto it = inst_index.find(rb.instance_id);
         if (it == inst_index.end())
           it = inst_index.emplace(rb.instance_id, std::stoi(rb.instance_id.substr(1)) - 1).first;
@@ -429,7 +528,6 @@ rs_sim* rs_sim_run(int n_layers, int dim, int n_lora, int first_adapted, int n_r
   } catch (const std::exception& e) {
     h->err = e.what();
   }
-  return h;
 }
 void rs_sim_free(rs_sim* h) { delete h; }
 const char* rs_sim_error(const rs_sim* h) { return h->err.c_str(); }

@@ -32,6 +32,9 @@ def lib():
         L.rs_percentile.argtypes = [P, I, D, C.POINTER(D)]
         L.rs_sim_run.restype = P
         L.rs_sim_run.argtypes = [I, I, I, I, I, P, P, I, I64]
+        L.rs_sim_run_gpu.restype = P
+        L.rs_sim_run_gpu.argtypes = [C.c_char_p, I, I, I, I, I, I, I, P, P, I, I64, C.c_uint64,
+                                     C.c_float, P]
         for n, r, a in [("rs_sim_free", None, [P]), ("rs_sim_error", C.c_char_p, [P]),
                         ("rs_sim_report", C.c_char_p, [P]), ("rs_sim_n_blocks", I, [P]),
                         ("rs_sim_block_id", C.c_char_p, [P, I]),
@@ -124,6 +127,41 @@ def simulate(n_layers: int, dim: int, n_lora: int, first_adapted: int, prompts, 
         return blocks, kinds, chains, req_model, trace
     finally:
         L.rs_sim_free(h)
+
+
+def simulate_gpu(n_layers: int, dim: int, n_heads: int, n_lora: int, first_adapted: int,
+                 prompts, outputs, max_batch_tokens: int = 4096, seed: int = 1,
+                 init_scale: float = 0.02 * 3 ** 0.5, device: int = 0, product_lib=None):
+    """The reference Simulation (the same zoo and requests as simulate) driving the product's
+    batch executor (bh_executor_run_batch) through its Engine trace hook: every batch it forms
+    runs on the GPU. Returns (decode rows [n_requests][dim] as float32, batch trace)."""
+    import numpy as np
+    if product_lib is None:
+        product_lib = os.path.join(os.path.dirname(_HERE), "paper_2404_18322_b200",
+                                   "libblockexec.so")
+    p = np.ascontiguousarray(prompts, np.int32)
+    o = np.ascontiguousarray(outputs, np.int32)
+    rows = np.zeros((len(p), dim), np.uint16)
+    L = lib()
+    h = L.rs_sim_run_gpu(product_lib.encode(), device, n_layers, dim, n_heads, n_lora,
+                         first_adapted, len(p), p.ctypes.data, o.ctypes.data, max_batch_tokens,
+                         0, seed, init_scale, rows.ctypes.data)
+    try:
+        err = L.rs_sim_error(h).decode()
+        if err:
+            raise RuntimeError(err)
+        trace = []
+        rec = (C.c_int32 * 4)()
+        mem = (C.c_int32 * (3 * 65536))()
+        for i in range(L.rs_sim_n_batches(h)):
+            L.rs_sim_batch(h, i, rec, mem, 65536)
+            members = [(int(mem[3 * j]), int(mem[3 * j + 1]), int(mem[3 * j + 2]))
+                       for j in range(rec[3])]
+            trace.append((int(rec[0]), int(rec[1]), int(rec[2]), members))
+    finally:
+        L.rs_sim_free(h)
+    f32 = (rows.astype(np.uint32) << 16).view(np.float32)
+    return f32, trace
 
 
 def profile_component_us(path: str, cls: str, prefill: bool, batch: float, tokens: float) -> float:

@@ -88,6 +88,7 @@ class Runner {
   std::vector<bh_batch_rec> recs;
   std::vector<int32_t> m_req, m_step, m_ctx;
   bh_step_stats stats{};
+  const bh_spec_stats& spec_stats() const { return spec_stats_; }
 
  private:
   // --- executor loop pieces (scenario.cpp)
@@ -131,6 +132,16 @@ class Runner {
     return lora_base_[b] >= 0 ? 2 * (int)(kv_bpt_[b] / (4LL * d_)) : 0;  // n_att from KV bytes
   }
   std::vector<be_kv_pool*> pools_;
+  // speculation: surrogate block and its KV pool per marked block, the verify lane's workspace,
+  // [n_requests][d] scratch rows (draft, true, next) and the next block's row indices
+  std::vector<char> spec_;
+  std::vector<be_block*> sur_;
+  std::vector<be_kv_pool*> sur_pool_;
+  be_workspace* ws_verify_ = nullptr;
+  void* spec_buf_ = nullptr;
+  int32_t* spec_dst_ = nullptr;
+  float spec_thr_ = 0.95f;
+  bh_spec_stats spec_stats_{0, 0, 0, 0.0, 1.0};
   std::vector<int> chain_ptr_, chain_blocks_;
   std::vector<Request> reqs_;
   std::vector<std::string> inst_of_block_;
@@ -163,6 +174,9 @@ class Runner {
     std::vector<int32_t> lidx;   // lora: adapter slot per token (group index, -1 = the base)
   };
   std::vector<LaunchEntry> group_plans(const std::vector<PlannedBatch>& plans) const;
+  bool spec_pair(const std::vector<PlannedBatch>& plans, const LaunchEntry& a,
+                 const LaunchEntry& b) const;
+  void run_speculative(const PlannedBatch& pv, const PlannedBatch& pn);
   // one planned decode step: host bookkeeping done, metadata laid out, nothing on the device yet
   struct StepPlan {
     bool valid = false;
@@ -330,6 +344,35 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
     ck(cudaMalloc(&d_zero_idx_, (size_t)max_tok * sizeof(int32_t)), "lora idx");
     ck(cudaMemsetAsync(d_zero_idx_, 0, (size_t)max_tok * sizeof(int32_t), st_), "lora idx");
   }
+  spec_.assign(w.n_blocks, 0);
+  sur_.assign(w.n_blocks, nullptr);
+  sur_pool_.assign(w.n_blocks, nullptr);
+  if (w.n_spec_blocks > 0 && w.spec_blocks != nullptr) {
+    spec_thr_ = w.spec_threshold;
+    const float keep = w.spec_keep > 0.f && w.spec_keep < 1.f ? w.spec_keep : 0.5f;
+    for (int i = 0; i < w.n_spec_blocks; ++i) {
+      const int b = w.spec_blocks[i];
+      if (b < 0 || b >= w.n_blocks || lora_base_[b] >= 0 || kv_bpt_[b] == 0)
+        throw BeError(BE_ERR_INVALID, "runner: block " + std::to_string(b) + " cannot speculate");
+      if (spec_[b]) continue;
+      spec_[b] = 1;
+      // the surrogate: the block's own weights with the FFN cut to a channel prefix
+      be_block_desc sd = descs_[b];
+      sd.name = names_[b].c_str();
+      sd.components = comps_[b].empty() ? nullptr : comps_[b].c_str();
+      sd.ffn_src = descs_[b].d_ff;
+      sd.d_ff = std::max(64, (int)(descs_[b].d_ff * keep) / 64 * 64);
+      rc = be_block_load(ctx, &sd, &sur_[b]);
+      if (rc != BE_OK) throw BeError(rc, std::string("surrogate load: ") + be_last_error(ctx));
+      rc = be_kv_pool_create(ctx, sur_[b], np_of[b], &sur_pool_[b]);
+      if (rc != BE_OK) throw BeError(rc, std::string("surrogate kv pool: ") + be_last_error(ctx));
+    }
+    rc = be_workspace_create(ctx, d_, dff, H, max_tok, w.n_requests, pages_for(max_ctx_) + 1,
+                             &ws_verify_);
+    if (rc != BE_OK) throw BeError(rc, std::string("verify workspace: ") + be_last_error(ctx));
+    ck(cudaMalloc(&spec_buf_, (size_t)3 * w.n_requests * d_ * 2), "speculation rows");
+    ck(cudaMalloc(&spec_dst_, (size_t)w.n_requests * sizeof(int32_t)), "speculation rows");
+  }
   ck(cudaMalloc(&arena_, (size_t)w.n_requests * d_ * 2), "arena");
   ck(cudaMalloc(&parena_, (size_t)poff * d_ * 2), "prefill arena");
   prefill_rows_ = poff;
@@ -359,6 +402,13 @@ Runner::~Runner() {
   for (auto* l : loras_)
     if (l) be_lora_free(l);
   if (d_zero_idx_) cudaFree(d_zero_idx_);
+  for (auto* p : sur_pool_)
+    if (p) be_kv_pool_free(p);
+  for (auto* b : sur_)
+    if (b) be_block_free(b);
+  if (ws_verify_) be_workspace_free(ws_verify_);
+  if (spec_buf_) cudaFree(spec_buf_);
+  if (spec_dst_) cudaFree(spec_dst_);
 }
 
 int Runner::live() const {
@@ -863,6 +913,25 @@ void Runner::stage_and_launch(StepPlan& sp, const void* host_in) {
   };
   stats = sp.stats;
   stats.graph_replayed = 0;
+  bool any_spec = false;
+  for (size_t i = 0; i + 1 < entries.size() && !any_spec; ++i)
+    any_spec = spec_pair(plans, entries[i], entries[i + 1]);
+  if (any_spec) {
+    // speculative pairs are host-synchronous (the K7 verdict is read back): no graph
+    for (size_t i = 0; i < entries.size(); ++i) {
+      if (i + 1 < entries.size() && spec_pair(plans, entries[i], entries[i + 1])) {
+        run_speculative(plans[entries[i].plans[0]], plans[entries[i + 1].plans[0]]);
+        ++i;
+        continue;
+      }
+      launch_entry(plans, entries[i], reinterpret_cast<const be_token*>(meta_dev_ + sp.off_tok[i]),
+                   reinterpret_cast<const int32_t*>(meta_dev_ + sp.off_pt[i]),
+                   reinterpret_cast<const int32_t*>(meta_dev_ + sp.off_idx[i]));
+    }
+    gs.reset();
+    gs.sig.clear();
+    return;
+  }
   if (be_prof_active(ctx_)) {
     launch_all();  // per-launch event timing: plain launches, the captured graph is kept
     if (sp.sig != gs.sig) gs.reset();
@@ -933,6 +1002,64 @@ void Runner::decode_step(const void* host_in, void* host_out, int* n_batches, in
   if (host_out != nullptr) {
     copy_host_rows(sp.rows, false, host_out);
     ck(cudaStreamSynchronize(st_), "d2h sync");
+  }
+}
+
+// A speculative pair: a marked block's batch followed by a batch of one other block holding the
+// same rows in the same order (every member continues to that block), both plain launches.
+bool Runner::spec_pair(const std::vector<PlannedBatch>& plans, const LaunchEntry& a,
+                       const LaunchEntry& b) const {
+  if (a.plans.size() != 1 || b.plans.size() != 1) return false;
+  const PlannedBatch& pa = plans[a.plans[0]];
+  const PlannedBatch& pb = plans[b.plans[0]];
+  if (!spec_[pa.block] || pa.phase != Phase::kDecode || pb.phase != Phase::kDecode ||
+      loras_[pb.block] != nullptr || pa.toks.size() != pb.toks.size())
+    return false;
+  for (size_t i = 0; i < pa.toks.size(); ++i)
+    if (pa.toks[i].src_row != pb.toks[i].src_row) return false;
+  return true;
+}
+
+// be_exec_speculative over the pair (scenario.cpp:502-548 draft + early forward, 740-807
+// verification): rows go arena -> [draft | true] scratch rows 0..n-1 -> next -> scratch z ->
+// scattered back to their arena rows. The draft keeps its own KV pool (same slots).
+void Runner::run_speculative(const PlannedBatch& pv, const PlannedBatch& pn) {
+  const int n = static_cast<int>(pv.toks.size());
+  const size_t rows_bytes = (size_t)reqs_.size() * d_ * 2;
+  char* ydraft = static_cast<char*>(spec_buf_);
+  char* ytrue = ydraft + rows_bytes;
+  char* z = ytrue + rows_bytes;
+  std::vector<be_token> tv(pv.toks), tn(pn.toks);
+  std::vector<int32_t> dst(n);
+  for (int i = 0; i < n; ++i) {
+    dst[i] = tv[i].dst_row;
+    tv[i].dst_row = i;  // y rows 0..n-1: K7 compares row i of draft and true
+    tn[i].src_row = i;
+    tn[i].dst_row = i;
+  }
+  be_spec_stage verify{blocks_[pv.block], pools_[pv.block], ws_verify_, tv.data(), pv.n_rows,
+                       pv.stride, pv.pt.data()};
+  be_spec_stage draft{sur_[pv.block], sur_pool_[pv.block], ws_, tv.data(), pv.n_rows, pv.stride,
+                      pv.pt.data()};
+  be_spec_stage next{blocks_[pn.block], pools_[pn.block], ws_, tn.data(), pn.n_rows, pn.stride,
+                     pn.pt.data()};
+  std::vector<float> cosv(n);
+  std::vector<int32_t> acc(n);
+  int n_acc = 0;
+  int rc = be_exec_speculative(ctx_, &verify, &draft, &next, n, arena_, ydraft, ytrue, z,
+                               spec_thr_, cosv.data(), acc.data(), &n_acc);
+  if (rc != BE_OK) throw BeError(rc, std::string("speculative step: ") + be_last_error(ctx_));
+  ck(cudaMemcpyAsync(spec_dst_, dst.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st_),
+     "speculation rows");
+  rc = be_scatter_rows(ctx_, z, spec_dst_, n, d_, arena_, st_);
+  if (rc != BE_OK) throw BeError(rc, std::string("speculative scatter: ") + be_last_error(ctx_));
+  ck(cudaStreamSynchronize(st_), "speculation rows");  // dst staged from pageable memory
+  spec_stats_.runs += 1;
+  spec_stats_.rows += n;
+  spec_stats_.accepted += n_acc;
+  for (float c : cosv) {
+    spec_stats_.cos_sum += c;
+    spec_stats_.cos_min = std::min(spec_stats_.cos_min, (double)c);
   }
 }
 
@@ -1121,6 +1248,11 @@ extern "C" int bh_runner_clear_trace(bh_runner* h) {
   h->r->m_req.clear();
   h->r->m_step.clear();
   h->r->m_ctx.clear();
+  return BE_OK;
+}
+extern "C" int bh_runner_spec_stats(const bh_runner* h, bh_spec_stats* out) {
+  if (h == nullptr || out == nullptr) return BE_ERR_INVALID;
+  *out = h->r->spec_stats();
   return BE_OK;
 }
 extern "C" int bh_runner_step_stats(const bh_runner* h, bh_step_stats* out) {

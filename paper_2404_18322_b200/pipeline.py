@@ -111,7 +111,8 @@ def _profile_classes(path: str | None):
 
 
 def routing_policy(wl: Workload, n_devices: int, profiles: str | None = None,
-                   hbm_bytes: int = 180 * 10**9, instances: bool = True):
+                   hbm_bytes: int = 180 * 10**9, instances: bool = True,
+                   speculation: bool = False, spec_fraction: float = 0.10):
     """A bh_policy (include/blockpolicy.h) describing replica placement of `wl`: every block on
     each of n_devices GPUs of one NVLink server, priced by the measured B200 cost profiles
     (profiles/b200_profiles.json, scripts/make_profiles.py; §8(f) rank 2). Classes the profile
@@ -120,7 +121,7 @@ def routing_policy(wl: Workload, n_devices: int, profiles: str | None = None,
     s = wl.shape
     d = s.d_model
     prof = _profile_classes(profiles)
-    pol = Policy(adaptive=False, speculation=False)
+    pol = Policy(adaptive=False, speculation=speculation, spec_fraction=spec_fraction)
     att_bytes, ffn_bytes = 2 * 4 * d * d, 2 * 3 * d * s.d_ff
     for kind, wbytes, kv in (("attention", att_bytes, 4 * d), ("ffn", ffn_bytes, 0)):
         key = f"{kind}:{d}"
@@ -353,3 +354,28 @@ def ticks_needed(world: int, steps: int, warmup: int) -> int:
 
 def tokens_per_request_needed(world: int, total_ticks: int, n_micro: int) -> int:
     return math.ceil(total_ticks / n_micro) + 2
+
+
+def speculation_blocks(wl: Workload, spec_fraction: float = 0.10, us_per_row: float = 1.0):
+    """Blocks a lockstep decode step runs speculatively: the reference's marking rule
+    (bh_policy_speculation_marks = Scheduler::speculation_marks, scheduler.cpp:180-215: the top
+    ceil(fraction x instances) instances by queued cost, skipping blocks without a surrogate,
+    chain-final blocks and chain neighbours of marked ones) over the instances of one GPU, each
+    queue holding its per-block decode batch (queued cost = rows x us_per_row). Returns
+    (marked block indices the executor can speculate - every member continues to one block -,
+    all marked block names)."""
+    pol = routing_policy(wl, 1, instances=False, speculation=True, spec_fraction=spec_fraction)
+    rows = wl.rows_at_block()
+    for b, name in enumerate(wl.block_names):
+        pol.put_instance(f"r0.{name}", name, 0, ready=True, created_seq=b + 1,
+                         queue_len=rows[b], queued_cost_us=rows[b] * us_per_row,
+                         queued_cost_hwm=rows[b] * us_per_row)
+    marked = [iid.split(".", 1)[1] for iid in pol.speculation_marks()]
+    pol.close()
+    ok = []
+    for name in marked:
+        b = wl.block_names.index(name)
+        succ = {ch[ch.index(b) + 1] for ch in wl.chains if b in ch and ch.index(b) + 1 < len(ch)}
+        if len(succ) == 1:
+            ok.append(b)
+    return ok, marked

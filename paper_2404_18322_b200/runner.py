@@ -28,7 +28,14 @@ class WorkloadC(C.Structure):
                 ("req_prompt", C.c_void_p), ("req_output", C.c_void_p),
                 ("max_batch_tokens", C.c_int), ("mode", C.c_int), ("use_graphs", C.c_int),
                 ("seed", C.c_uint64), ("dry_run", C.c_int), ("plan_ahead", C.c_int),
-                ("block_lora_base", C.c_void_p), ("block_lora_name", C.c_void_p)]
+                ("block_lora_base", C.c_void_p), ("block_lora_name", C.c_void_p),
+                ("n_spec_blocks", C.c_int), ("spec_blocks", C.c_void_p),
+                ("spec_threshold", C.c_float), ("spec_keep", C.c_float)]
+
+
+class SpecStats(C.Structure):
+    _fields_ = [("runs", C.c_int64), ("rows", C.c_int64), ("accepted", C.c_int64),
+                ("cos_sum", C.c_double), ("cos_min", C.c_double)]
 
 
 _bound = False
@@ -55,6 +62,7 @@ def _bind():
         ("bh_runner_decode_group", I, [P, I, P, I, P, P, P]),
         ("bh_runner_step_stats", I, [P, P]),
         ("bh_runner_serve", I, [P, P, P, P]),
+        ("bh_runner_spec_stats", I, [P, P]),
     ]:
         fn = getattr(L, name)
         fn.restype, fn.argtypes = res, args
@@ -69,8 +77,10 @@ class Runner:
     """
 
     def __init__(self, ctx: Context | None, wl: Workload, mode: int = 1, use_graphs: bool = True,
-                 dry_run: bool = False, plan_ahead: bool = False):
-        """ctx None with dry_run=True runs the control plane alone (no GPU work)."""
+                 dry_run: bool = False, plan_ahead: bool = False, spec_blocks=None,
+                 spec_threshold: float = 0.95, spec_keep: float = 0.5):
+        """ctx None with dry_run=True runs the control plane alone (no GPU work).
+        spec_blocks: block indices whose decode runs speculatively (bh_workload.spec_blocks)."""
         _bind()
         self.ctx, self.wl = ctx, wl
         s = wl.shape
@@ -98,11 +108,14 @@ class Runner:
                 *[None if x is None else x[1].encode() for x in wl.block_lora])
             self._keep += [base, names]
             lora_base, lora_names = base.ctypes.data, C.cast(names, C.c_void_p)
+        spec = np.ascontiguousarray(list(spec_blocks or []) or [0], np.int32)
+        self._keep.append(spec)
         w = WorkloadC(len(wl.block_names), C.cast(descs, C.c_void_p), len(wl.chains),
                       k[1].ctypes.data, k[2].ctypes.data, wl.n_requests, k[3].ctypes.data,
                       k[4].ctypes.data, k[5].ctypes.data, wl.max_batch_tokens, mode,
                       1 if use_graphs else 0, wl.seed, 1 if dry_run else 0,
-                      1 if plan_ahead else 0, lora_base, lora_names)
+                      1 if plan_ahead else 0, lora_base, lora_names,
+                      len(spec_blocks or []), spec.ctypes.data, spec_threshold, spec_keep)
         h = C.c_void_p()
         rc = lib().bh_runner_create(ctx.h if ctx is not None else None, C.byref(w), C.byref(h))
         if rc != 0:
@@ -170,6 +183,14 @@ class Runner:
         s = StepStats()
         self._check(lib().bh_runner_step_stats(self.h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in StepStats._fields_}
+
+    def spec_stats(self) -> dict:
+        s = SpecStats()
+        self._check(lib().bh_runner_spec_stats(self.h, C.byref(s)))
+        d = {f: getattr(s, f) for f, _ in SpecStats._fields_}
+        d["accept_rate"] = d["accepted"] / d["rows"] if d["rows"] else None
+        d["cos_mean"] = d["cos_sum"] / d["rows"] if d["rows"] else None
+        return d
 
     def trace(self):
         """[(instance_idx, block_idx, phase, [(req, step, ctx), ...]), ...]"""
