@@ -464,11 +464,17 @@ __global__ void __launch_bounds__(192, CTAS)
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(sA + s * S::kABytes);
           const uint32_t b_addr = smem_u32(sB + s * S::kBBytes);
+#ifndef BE_EXP_NO_MMA  // experiments: data movement alone
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             umma_bf16(tacc, make_sdesc_k128(a_addr + k * 32), make_sdesc_k128(b_addr + k * 32),
                       idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
+#else
+          (void)a_addr;
+          (void)b_addr;
+          (void)tacc;
+#endif
           umma_commit(&empty[s]);
           if (kb == kb1 - 1) umma_commit(&tfull[a]);
         }
@@ -529,6 +535,14 @@ __global__ void __launch_bounds__(192, CTAS)
       tc_fence_after();
       if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
       __syncwarp();
+#ifdef BE_EXP_NO_EPI  // experiments: the mainloop alone (no partials, no fixup, no stores)
+      if (true) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
+        continue;
+      }
+#endif
       const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
       if (whole) {
 #pragma unroll 1
