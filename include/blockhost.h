@@ -124,6 +124,12 @@ typedef struct {
   const int32_t* spec_blocks;
   float spec_threshold; /* 0.95 in the paper */
   float spec_keep;      /* surrogate FFN fraction, e.g. 0.5 */
+  /* prefix groups (Request::prefix_group / prefix_tokens, workload.hpp:19-20; NULL = none):
+   * requests of a group share the first prefix_tokens prompt tokens (synthetic stream
+   * "inputs:prefix<group>"); at each block the first member to finish prefill donates its
+   * prefix pages and later members share them (create_kv_for_step, scenario.cpp:671-695). */
+  const int32_t* req_prefix_group;
+  const int32_t* req_prefix_tokens;
 } bh_workload;
 
 typedef struct {
@@ -159,6 +165,8 @@ int bh_runner_decode_group(bh_runner* r, int group, const int32_t* reqs, int n,
 int bh_runner_serve(bh_runner* r, const int64_t* arrival_us, int64_t* first_token_us,
                     int64_t* completion_us);
 int bh_runner_live_requests(const bh_runner* r);
+/* KV bookkeeping: bytes of pages in use and bytes saved by prefix sharing (KvStore). */
+int bh_runner_kv_bytes(const bh_runner* r, int64_t* used, int64_t* saved_by_sharing);
 int64_t bh_runner_tokens_generated(const bh_runner* r);
 /* Batch trace since creation. members: request ids, steps, context tokens (may be NULL). */
 int bh_runner_trace(const bh_runner* r, bh_batch_rec* recs, int cap, int* n_out,

@@ -327,7 +327,19 @@ struct GpuHook {
 
 static void run_sim(rs_sim* h, int n_layers, int dim, int n_lora, int first_adapted,
                     int n_requests, const int32_t* prompts, const int32_t* outputs,
-                    int max_batch_tokens, int64_t arrival_gap_us, GpuHook* gpu);
+                    int max_batch_tokens, int64_t arrival_gap_us, GpuHook* gpu,
+                    const int32_t* prefix_group = nullptr, const int32_t* prefix_tokens = nullptr);
+
+// The same run with prefix groups (Request::prefix_group / prefix_tokens, workload.hpp:19-20):
+// the report's kv.shared_bytes is the high-water mark of bytes saved by sharing.
+rs_sim* rs_sim_run_prefix(int n_layers, int dim, int n_lora, int first_adapted, int n_requests,
+                          const int32_t* prompts, const int32_t* outputs, int max_batch_tokens,
+                          const int32_t* prefix_group, const int32_t* prefix_tokens) {
+  auto* h = new rs_sim();
+  run_sim(h, n_layers, dim, n_lora, first_adapted, n_requests, prompts, outputs,
+          max_batch_tokens, 0, nullptr, prefix_group, prefix_tokens);
+  return h;
+}
 
 rs_sim* rs_sim_run(int n_layers, int dim, int n_lora, int first_adapted, int n_requests,
                    const int32_t* prompts, const int32_t* outputs, int max_batch_tokens,
@@ -391,7 +403,8 @@ rs_sim* rs_sim_run_gpu(const char* product_lib, int device, int n_layers, int di
 
 static void run_sim(rs_sim* h, int n_layers, int dim, int n_lora, int first_adapted,
                     int n_requests, const int32_t* prompts, const int32_t* outputs,
-                    int max_batch_tokens, int64_t arrival_gap_us, GpuHook* gpu) {
+                    int max_batch_tokens, int64_t arrival_gap_us, GpuHook* gpu,
+                    const int32_t* prefix_group, const int32_t* prefix_tokens) {
   try {
     Zoo zoo;
     std::vector<ComponentDescriptor> base;
@@ -459,6 +472,10 @@ static void run_sim(rs_sim* h, int n_layers, int dim, int n_lora, int first_adap
       r.arrival_us = arrival_gap_us * i;
       r.prompt_tokens = prompts[i];
       r.output_tokens = outputs[i];
+      if (prefix_group != nullptr) {
+        r.prefix_group = prefix_group[i];
+        r.prefix_tokens = prefix_tokens[i];
+      }
       reqs.push_back(r);
     }
     ScenarioConfig cfg;

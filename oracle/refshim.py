@@ -32,6 +32,8 @@ def lib():
         L.rs_percentile.argtypes = [P, I, D, C.POINTER(D)]
         L.rs_sim_run.restype = P
         L.rs_sim_run.argtypes = [I, I, I, I, I, P, P, I, I64]
+        L.rs_sim_run_prefix.restype = P
+        L.rs_sim_run_prefix.argtypes = [I, I, I, I, I, P, P, I, P, P]
         L.rs_sim_run_gpu.restype = P
         L.rs_sim_run_gpu.argtypes = [C.c_char_p, I, I, I, I, I, I, I, P, P, I, I64, C.c_uint64,
                                      C.c_float, P]
@@ -125,6 +127,36 @@ def simulate(n_layers: int, dim: int, n_lora: int, first_adapted: int, prompts, 
                        for j in range(rec[3])]
             trace.append((int(rec[0]), int(rec[1]), int(rec[2]), members))
         return blocks, kinds, chains, req_model, trace
+    finally:
+        L.rs_sim_free(h)
+
+
+def simulate_prefix(n_layers: int, dim: int, n_lora: int, first_adapted: int, prompts, outputs,
+                    prefix_group, prefix_tokens, max_batch_tokens: int = 4096):
+    """The reference Simulation with prefix groups: (report dict, batch trace)."""
+    import json
+    import numpy as np
+    p = np.ascontiguousarray(prompts, np.int32)
+    o = np.ascontiguousarray(outputs, np.int32)
+    g = np.ascontiguousarray(prefix_group, np.int32)
+    t = np.ascontiguousarray(prefix_tokens, np.int32)
+    L = lib()
+    h = L.rs_sim_run_prefix(n_layers, dim, n_lora, first_adapted, len(p), p.ctypes.data,
+                            o.ctypes.data, max_batch_tokens, g.ctypes.data, t.ctypes.data)
+    try:
+        err = L.rs_sim_error(h).decode()
+        if err:
+            raise RuntimeError(err)
+        rep = json.loads(L.rs_sim_report(h).decode())
+        trace = []
+        rec = (C.c_int32 * 4)()
+        mem = (C.c_int32 * (3 * 65536))()
+        for i in range(L.rs_sim_n_batches(h)):
+            L.rs_sim_batch(h, i, rec, mem, 65536)
+            members = [(int(mem[3 * j]), int(mem[3 * j + 1]), int(mem[3 * j + 2]))
+                       for j in range(rec[3])]
+            trace.append((int(rec[0]), int(rec[1]), int(rec[2]), members))
+        return rep, trace
     finally:
         L.rs_sim_free(h)
 

@@ -68,6 +68,16 @@ std::uint64_t KvStore::new_page(std::uint64_t request, const std::string& block,
   return id;
 }
 
+void KvStore::drop_reserved_front(std::uint64_t request, const std::string& block, int n) {
+  auto rit = reserved_.find({request, block});
+  if (rit == reserved_.end() || n <= 0) return;
+  auto& v = rit->second.slots;
+  const int k = std::min<int>(n, static_cast<int>(v.size()));
+  for (int i = 0; i < k; ++i) free_slot(rit->second.pool_key, rit->second.device, v[i]);
+  v.erase(v.begin(), v.begin() + k);
+  if (v.empty()) reserved_.erase(rit);
+}
+
 std::vector<int> KvStore::reserve_slots(std::uint64_t request, const std::string& block,
                                         const std::string& pool_key, int device,
                                         int total_pages) {

@@ -86,6 +86,9 @@ class KvStore {
   // chain end (append_decode_kv, scenario.cpp:697-719). To keep page ids bit-identical, physical
   // slots are reserved ahead of the bookkeeping and bound when the page id is created.
   // Returns the page-table row covering `total_pages` pages (existing, then reserved).
+  // Frees the first n slots reserved for (request, block): pages a prefix share supplied
+  // after the slots were reserved (their content was written, identical, into both).
+  void drop_reserved_front(std::uint64_t request, const std::string& block, int n);
   std::vector<int> reserve_slots(std::uint64_t request, const std::string& block,
                                  const std::string& pool_key, int device, int total_pages);
 

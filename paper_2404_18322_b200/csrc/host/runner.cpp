@@ -57,6 +57,8 @@ struct Request {
   int ctx = 0;       // context tokens (QueueEntry::context_tokens)
   bool done = false;
   int poff = 0;      // first row of its prompt in the prefill arena
+  int prefix_group = -1;
+  int prefix_tokens = 0;
 };
 
 struct PlannedBatch {
@@ -67,6 +69,7 @@ struct PlannedBatch {
   std::vector<int32_t> pt;  // [n_rows][stride]
   int n_rows = 0;
   int stride = 1;
+  std::vector<int> shared_pages;  // prefill: per member, prefix pages taken from a donor
 };
 
 class Runner {
@@ -81,6 +84,8 @@ class Runner {
   int live() const;
   std::int64_t generated() const { return tokens_generated_; }
   void* arena() { return arena_; }
+  std::int64_t kv_used() const { return kv_.used(0); }
+  std::int64_t kv_saved() const { return kv_.bytes_saved_by_sharing(); }
   int requests() const { return static_cast<int>(reqs_.size()); }
   void* prefill_arena() { return parena_; }
   std::int64_t prefill_rows() const { return prefill_rows_; }
@@ -95,7 +100,7 @@ class Runner {
   void dispatch(Request& r);
   void pump();
   void finish_running();
-  void advance_after_step(Request& r, int step);
+  void advance_after_step(Request& r, int step, int planned_shared = 0);
   void advance_from(Request& r, int step);
   std::string instance_for(int block);
   PlannedBatch plan(const std::string& inst_id, const Batch& b);
@@ -148,6 +153,9 @@ class Runner {
   std::vector<int> inst_index_;  // block -> instance creation index
   Pool pool_;
   KvStore kv_;
+  std::map<std::pair<int, int>, int> prefix_donors_;  // (prefix group, block) -> request id
+  bool prefix_share_ = true;
+  int prefix_donor(const Request& r, int block, int* want) const;
   be_workspace* ws_ = nullptr;
   void* arena_ = nullptr;   // decode rows [n_req][d]
   void* parena_ = nullptr;  // prefill rows [sum prompt][d]
@@ -228,6 +236,8 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   use_graphs_ = w.use_graphs != 0;
   plan_ahead_ = w.plan_ahead != 0;
   if (const char* g = std::getenv("BH_GROUP")) group_ = std::atoi(g) != 0;
+  // experiments / tests: prefix inputs without page sharing (every request its own donor)
+  if (const char* g = std::getenv("BH_PREFIX_SHARE")) prefix_share_ = std::atoi(g) != 0;
   max_batch_tokens_ = w.max_batch_tokens > 0 ? w.max_batch_tokens : 4096;
   d_ = w.blocks[0].d_model;
   for (int b = 0; b < w.n_blocks; ++b) {
@@ -258,6 +268,11 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
       throw BeError(BE_ERR_INVALID, "runner: bad request");
     r.ctx = r.prompt;
     r.poff = poff;
+    if (w.req_prefix_group != nullptr && w.req_prefix_tokens != nullptr &&
+        w.req_prefix_group[i] >= 0 && w.req_prefix_tokens[i] > 0) {
+      r.prefix_group = w.req_prefix_group[i];
+      r.prefix_tokens = std::min(w.req_prefix_tokens[i], r.prompt);
+    }
     poff += r.prompt;
     max_prompt = std::max(max_prompt, r.prompt);
     const int total = r.prompt + r.output;
@@ -381,6 +396,12 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
     rc = be_synth_rows(ctx, static_cast<char*>(parena_) + (size_t)r.poff * d_ * 2,
                        (int64_t)r.prompt * d_, w.seed, sid.c_str(), 1.7320508f, st_);
     if (rc != BE_OK) throw BeError(rc, "synthetic prompts");
+    if (r.prefix_group >= 0) {  // the group's common prefix
+      const std::string pid = "inputs:prefix" + std::to_string(r.prefix_group);
+      rc = be_synth_rows(ctx, static_cast<char*>(parena_) + (size_t)r.poff * d_ * 2,
+                         (int64_t)r.prefix_tokens * d_, w.seed, pid.c_str(), 1.7320508f, st_);
+      if (rc != BE_OK) throw BeError(rc, "synthetic prefixes");
+    }
   }
   ck(cudaStreamSynchronize(st_), "init");
 }
@@ -459,10 +480,25 @@ PlannedBatch Runner::plan(const std::string& inst_id, const Batch& b) {
     const int first = b.phase == Phase::kPrefill ? 0 : r.ctx - 1;
     const int count = b.phase == Phase::kPrefill ? r.prompt : 1;
     std::vector<int> row;
+    int shared = 0;
     if (kv_bpt_[block] > 0) {
       if (b.phase == Phase::kDecode && kv_.tokens(r.id, bn) != first)
         throw BeError(BE_ERR_STATE, "runner: kv segment out of step with the context");
-      row = kv_.reserve_slots(r.id, bn, bn, 0, pages_for(first + count));
+      int want = 0;
+      const int donor = b.phase == Phase::kPrefill && !kv_.has_segment(r.id, bn)
+                            ? prefix_donor(r, block, &want) : -1;
+      if (donor > 0) {
+        // the donor's whole prefix pages (share_prefix, kv.cpp): the prefill reads them and
+        // rewrites the same K/V into them (identical prefix tokens, identical bits)
+        const std::vector<int> ds = kv_.page_slots(donor, bn);
+        shared = std::min(std::min(want, kv_.tokens(donor, bn)) / kPageTokens, (int)ds.size());
+        row.assign(ds.begin(), ds.begin() + shared);
+        const std::vector<int> own =
+            kv_.reserve_slots(r.id, bn, bn, 0, pages_for(first + count) - shared);
+        row.insert(row.end(), own.begin(), own.end());
+      } else {
+        row = kv_.reserve_slots(r.id, bn, bn, 0, pages_for(first + count));
+      }
       std::copy(row.begin(), row.end(), pb.pt.begin() + (size_t)m * pb.stride);
     } else {
       row.assign(pages_for(first + count), 0);  // ffn-only block: no KV is written or read
@@ -482,8 +518,21 @@ PlannedBatch Runner::plan(const std::string& inst_id, const Batch& b) {
       t.pt_row = m;
       pb.toks.push_back(t);
     }
+    pb.shared_pages.push_back(shared);
   }
   return pb;
+}
+
+// create_kv_for_step's donor rule (scenario.cpp:679-692): the group's recorded donor at this
+// block, if it is another request whose segment already holds the prefix; -1 otherwise.
+int Runner::prefix_donor(const Request& r, int block, int* want) const {
+  if (r.prefix_group < 0 || r.prefix_tokens <= 0 || !prefix_share_) return -1;
+  *want = std::min(r.prefix_tokens, r.prompt);
+  auto it = prefix_donors_.find({r.prefix_group, block});
+  if (it == prefix_donors_.end() || it->second == r.id) return -1;
+  const std::string& bn = names_[block];
+  if (!kv_.has_segment(it->second, bn) || kv_.tokens(it->second, bn) < *want) return -1;
+  return it->second;
 }
 
 void Runner::launch(const PlannedBatch& pb, const be_token* d_tok, const int32_t* d_pt) {
@@ -581,17 +630,31 @@ void Runner::finish_running() {
   has_running_ = false;
   pool_.finish_batch(running_inst_, 0);
   const Batch b = running_;
-  for (const auto& m : b.members) advance_after_step(reqs_[m.request_id - 1], m.chain_step);
+  for (size_t i = 0; i < b.members.size(); ++i)
+    advance_after_step(reqs_[b.members[i].request_id - 1], b.members[i].chain_step,
+                       running_plan_.shared_pages[i]);
   pump();
 }
 
-void Runner::advance_after_step(Request& r, int step) {
+void Runner::advance_after_step(Request& r, int step, int planned_shared) {
   if (r.phase == Phase::kPrefill) {
     const int block = chain_block(r, step);
     const std::string& bn = names_[block];
     if (kv_bpt_[block] > 0 && !kv_.has_segment(r.id, bn)) {
+      // create_kv_for_step (scenario.cpp:671-695): share the donor's prefix or become the donor
+      int want = 0;
+      const int donor = prefix_donor(r, block, &want);
       kv_.create_segment(r.id, bn, 0, kv_bpt_[block]);
-      kv_.append_tokens(r.id, bn, r.prompt);
+      int covered = 0;
+      if (donor > 0) {
+        covered = kv_.share_prefix(r.id, donor, bn, want);
+      } else if (r.prefix_group >= 0) {
+        prefix_donors_[{r.prefix_group, block}] = r.id;
+      }
+      // a donor that finished in the same batch: the request wrote its own prefix pages too;
+      // the shared ones replace them
+      kv_.drop_reserved_front(r.id, bn, covered / kPageTokens - planned_shared);
+      kv_.append_tokens(r.id, bn, r.prompt - covered);
     }
   }
   advance_from(r, step);
@@ -810,7 +873,9 @@ Runner::StepPlan Runner::plan_step(int group, const std::vector<int>* members) {
     pool_.finish_batch(running_inst_, 0);
     account(running_plan_);
     ++batches_run_;
-    for (const auto& m : running_.members) advance_after_step(reqs_[m.request_id - 1], m.chain_step);
+    for (size_t i = 0; i < running_.members.size(); ++i)
+      advance_after_step(reqs_[running_.members[i].request_id - 1], running_.members[i].chain_step,
+                         running_plan_.shared_pages[i]);
   }
   sp.stats = stats;
   stats = saved;
@@ -1216,6 +1281,12 @@ extern "C" int bh_runner_serve(bh_runner* h, const int64_t* arrival_us, int64_t*
   if (h == nullptr || arrival_us == nullptr || first_token_us == nullptr || completion_us == nullptr)
     return BE_ERR_INVALID;
   return guard(h, [&] { h->r->serve(arrival_us, first_token_us, completion_us); });
+}
+extern "C" int bh_runner_kv_bytes(const bh_runner* h, int64_t* used, int64_t* saved) {
+  if (h == nullptr) return BE_ERR_INVALID;
+  if (used) *used = h->r->kv_used();
+  if (saved) *saved = h->r->kv_saved();
+  return BE_OK;
 }
 extern "C" int bh_runner_live_requests(const bh_runner* h) { return h ? h->r->live() : 0; }
 extern "C" int64_t bh_runner_tokens_generated(const bh_runner* h) { return h ? h->r->generated() : 0; }

@@ -30,7 +30,8 @@ class WorkloadC(C.Structure):
                 ("seed", C.c_uint64), ("dry_run", C.c_int), ("plan_ahead", C.c_int),
                 ("block_lora_base", C.c_void_p), ("block_lora_name", C.c_void_p),
                 ("n_spec_blocks", C.c_int), ("spec_blocks", C.c_void_p),
-                ("spec_threshold", C.c_float), ("spec_keep", C.c_float)]
+                ("spec_threshold", C.c_float), ("spec_keep", C.c_float),
+                ("req_prefix_group", C.c_void_p), ("req_prefix_tokens", C.c_void_p)]
 
 
 class SpecStats(C.Structure):
@@ -63,6 +64,7 @@ def _bind():
         ("bh_runner_step_stats", I, [P, P]),
         ("bh_runner_serve", I, [P, P, P, P]),
         ("bh_runner_spec_stats", I, [P, P]),
+        ("bh_runner_kv_bytes", I, [P, P, P]),
     ]:
         fn = getattr(L, name)
         fn.restype, fn.argtypes = res, args
@@ -110,12 +112,19 @@ class Runner:
             lora_base, lora_names = base.ctypes.data, C.cast(names, C.c_void_p)
         spec = np.ascontiguousarray(list(spec_blocks or []) or [0], np.int32)
         self._keep.append(spec)
+        pg = pt = None
+        if getattr(wl, "req_prefix_group", None) is not None:
+            pga = np.ascontiguousarray(wl.req_prefix_group, np.int32)
+            pta = np.ascontiguousarray(wl.req_prefix_tokens, np.int32)
+            self._keep += [pga, pta]
+            pg, pt = pga.ctypes.data, pta.ctypes.data
         w = WorkloadC(len(wl.block_names), C.cast(descs, C.c_void_p), len(wl.chains),
                       k[1].ctypes.data, k[2].ctypes.data, wl.n_requests, k[3].ctypes.data,
                       k[4].ctypes.data, k[5].ctypes.data, wl.max_batch_tokens, mode,
                       1 if use_graphs else 0, wl.seed, 1 if dry_run else 0,
                       1 if plan_ahead else 0, lora_base, lora_names,
-                      len(spec_blocks or []), spec.ctypes.data, spec_threshold, spec_keep)
+                      len(spec_blocks or []), spec.ctypes.data, spec_threshold, spec_keep,
+                      pg, pt)
         h = C.c_void_p()
         rc = lib().bh_runner_create(ctx.h if ctx is not None else None, C.byref(w), C.byref(h))
         if rc != 0:
@@ -183,6 +192,12 @@ class Runner:
         s = StepStats()
         self._check(lib().bh_runner_step_stats(self.h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in StepStats._fields_}
+
+    def kv_bytes(self) -> tuple[int, int]:
+        """(bytes of KV pages in use, bytes saved by prefix sharing)."""
+        u, sv = C.c_int64(0), C.c_int64(0)
+        self._check(lib().bh_runner_kv_bytes(self.h, C.byref(u), C.byref(sv)))
+        return u.value, sv.value
 
     def spec_stats(self) -> dict:
         s = SpecStats()

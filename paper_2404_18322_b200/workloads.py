@@ -28,6 +28,9 @@ class Workload:
     # per block: None, or (base block index, adapter name) for a LoRA variant that shares the
     # base's weights (the reference zoo's fused attention, attach "fuse"; gen_configs.py:88-106)
     block_lora: list | None = None
+    # per request: prefix group (-1 none) and shared prefix tokens (workload.hpp:19-20)
+    req_prefix_group: list | None = None
+    req_prefix_tokens: list | None = None
 
     @property
     def n_requests(self) -> int:

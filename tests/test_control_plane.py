@@ -421,3 +421,38 @@ def test_measured_b200_profiles_load_in_the_reference():
     # attention cost grows with context at a fixed batch (the KV read), as the kernels do
     dec = prof["classes"]["attention:4096"]["decode"]["us"]
     assert dec[-1][-1] > 2 * dec[-1][0]
+
+
+PREFIX_CASES = [
+    # n_layers, dim, n_lora, first_adapted, prompts, outputs, budget, prefix tokens
+    (4, 256, 2, 2, [48] * 8, [4] * 8, 4096, 40),         # one prefill batch: donor in-batch
+    (4, 256, 2, 2, [48, 20, 48, 33, 48, 16], [5, 3, 4, 2, 6, 3], 64, 33),  # across batches
+    (3, 512, 3, 1, [64, 70, 40, 64, 80, 17], [3, 3, 3, 3, 3, 3], 4096, 64),
+]
+
+
+@pytest.mark.parametrize("case", PREFIX_CASES)
+def test_prefix_sharing_matches_reference_simulation(case):
+    """Prefix groups (Request::prefix_group = the app's model, prefix_tokens): the executor loop
+    shares a donor's whole prefix pages exactly as create_kv_for_step (scenario.cpp:671-695) -
+    the batch trace is unchanged and the bytes saved equal the reference report's
+    kv.shared_bytes."""
+    from paper_2404_18322_b200.device import BlockShape
+    from paper_2404_18322_b200.runner import Runner
+    from paper_2404_18322_b200.workloads import Workload
+    n_layers, dim, n_lora, first, prompts, outputs, budget, ptok = case
+    blocks, kinds, chains, req_model, trace = R.simulate(n_layers, dim, n_lora, first, prompts,
+                                                         outputs, max_batch_tokens=budget)
+    groups = list(req_model)
+    toks = [ptok] * len(prompts)
+    rep, ptrace = R.simulate_prefix(n_layers, dim, n_lora, first, prompts, outputs, groups, toks,
+                                    max_batch_tokens=budget)
+    assert ptrace == trace
+    shape = BlockShape(1, dim, dim // 64, 3 * dim, max_pos=1024)
+    wl = Workload("prefix", shape, blocks, chains, req_model, prompts, outputs,
+                  max_batch_tokens=budget, block_comps=kinds, req_prefix_group=groups,
+                  req_prefix_tokens=toks)
+    run = Runner(None, wl, mode=0, dry_run=True)
+    run.run()
+    assert run.trace() == trace
+    assert run.kv_bytes()[1] == rep["kv"]["shared_bytes"] > 0
