@@ -103,11 +103,17 @@ template <int BN>
 __host__ __device__ constexpr int gemm_ctas() {
   return BN <= 64 ? BE_GEMM_CTAS : 1;
 }
+#ifndef BE_GEMM_MAX_STAGES
+#define BE_GEMM_MAX_STAGES 8
+#endif
+#ifndef BE_GEMM_RING_MAX_KB
+#define BE_GEMM_RING_MAX_KB 200
+#endif
 template <int BN>
 __host__ __device__ constexpr int gemm_stages_deep() {
-  const int ring_kb = gemm_ctas<BN>() > 1 ? BE_GEMM_RING_KB : 200;
+  const int ring_kb = gemm_ctas<BN>() > 1 ? BE_GEMM_RING_KB : BE_GEMM_RING_MAX_KB;
   const int s = (ring_kb * 1024) / GemmSmem<BN>::kStageBytes;
-  return s > 8 ? 8 : (s < 2 ? 2 : s);
+  return s > BE_GEMM_MAX_STAGES ? BE_GEMM_MAX_STAGES : (s < 2 ? 2 : s);
 }
 
 template <int BN>
