@@ -16,10 +16,6 @@
 
 namespace bx {
 
-#ifndef BE_GEMM_PF
-#define BE_GEMM_PF 0  // weight tiles prefetched into L2 beyond the ring (experiments)
-#endif
-constexpr int kGemmPF = BE_GEMM_PF;
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
@@ -428,16 +424,6 @@ __global__ void __launch_bounds__(192, CTAS)
         mbar_arrive_expect_tx(&full[i], stage_bytes);
         bulk_load(sA + i * S::kABytes, wtile(cw), S::kABytes, &full[i], kEvictFirst);
       }
-      // L2 lookahead: weight tiles kGemmPF iterations beyond the ring are prefetched into L2,
-      // so the bytes in flight per SM are not capped by the ring (a slot frees only when its
-      // MMA completes) and a refill finds its tile on chip
-      Cur cp = cw;
-      long long pf_next = pre;
-      auto prefetch_to = [&](long long upto) {
-        for (; pf_next < upto && pf_next < n_it; ++pf_next, step(cp))
-          prefetch_l2_bulk(wtile(cp), S::kABytes);
-      };
-      prefetch_to(pre + kGemmPF);
       pdl_wait();  // activations are produced by the previous kernel
       stamp(E, 2);
       tl_go(E.tl, E.tl_cap);
@@ -450,7 +436,6 @@ __global__ void __launch_bounds__(192, CTAS)
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         bulk_load(sA + s * S::kABytes, wtile(cw), S::kABytes, &full[s], kEvictFirst);
         tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, cw.kb * kBK, cw.n * BN, kEvictLast);
-        prefetch_to(i + 1 + kGemmPF);
         if (++s == STAGES) {
           s = 0;
           ph ^= 1u;

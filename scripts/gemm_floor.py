@@ -22,7 +22,8 @@ out = {"lib": os.environ.get("BE_LIB_PATH", "default")}
 for name, N, K in [("o", 4096, 4096), ("qkv", 12288, 4096), ("gate_up", 22016, 4096),
                    ("down", 4096, 11008)]:
     for M in (64, 16):
-        copies = max(2, int(3 * 126e6 / (N * K * 2)) + 1)
+        # BE_FLOOR_L2=1: one weight copy, re-read every launch (L2-resident when it fits)
+        copies = 1 if os.environ.get("BE_FLOOR_L2") else max(2, int(3 * 126e6 / (N * K * 2)) + 1)
         ws = [dev.pack_weight(ctx, (torch.rand(N, K, device="cuda", dtype=torch.bfloat16) - 0.5)
                               * 0.05) for _ in range(copies)]
         x = torch.randn(M, K, device="cuda").to(torch.bfloat16)

@@ -10,7 +10,7 @@
 
 using namespace bx;
 
-template <int N>
+template <int N, int NACC = 1>
 __global__ void __launch_bounds__(128, 1) mma_loop(int stages, int wait_each, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -39,9 +39,12 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int stages, int wait_each, un
     for (int s = 0; s < stages; ++s) {
       const unsigned long long ti = gtimer();
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        umma_bf16(tmem, make_sdesc_k128(a + k * 32), make_sdesc_k128(b + k * 32), idesc,
-                  (s > 0 || k > 0) ? 1u : 0u);
+      for (int k = 0; k < 4; ++k) {
+        // NACC accumulators side by side in TMEM, consecutive instructions alternating
+        const int acc = (s * 4 + k) % NACC;
+        umma_bf16(tmem + acc * N, make_sdesc_k128(a + k * 32), make_sdesc_k128(b + k * 32), idesc,
+                  (s * 4 + k >= NACC) ? 1u : 0u);
+      }
       if (wait_each || s == stages - 1) umma_commit(bar);
       if (wait_each) {
         mbar_wait(bar, ph);
@@ -59,14 +62,15 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int stages, int wait_each, un
   if (threadIdx.x < 32) tmem_free<256>(tmem);
 }
 
-template <int N>
+template <int N, int NACC = 1>
 void run(int sms, unsigned long long* d, unsigned long long* h) {
   const int smem = 16384 + N * 128 + 64 + 1024;
-  cudaFuncSetAttribute(mma_loop<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_loop<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  printf("accumulators %d\n", NACC);
   for (int wait_each = 0; wait_each < 2; ++wait_each) {
     const int stages = 2000;
-    mma_loop<N><<<sms, 128, smem>>>(stages, wait_each, d);
-    mma_loop<N><<<sms, 128, smem>>>(stages, wait_each, d);
+    mma_loop<N, NACC><<<sms, 128, smem>>>(stages, wait_each, d);
+    mma_loop<N, NACC><<<sms, 128, smem>>>(stages, wait_each, d);
     cudaDeviceSynchronize();
     cudaMemcpy(h, d, sms * 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     double tot = 0, lat = 0;
@@ -90,9 +94,12 @@ int main() {
   unsigned long long *d, *h = new unsigned long long[2 * sms];
   cudaMalloc(&d, 2 * sms * sizeof(unsigned long long));
   run<16>(sms, d, h);
-  run<32>(sms, d, h);
   run<64>(sms, d, h);
   run<128>(sms, d, h);
   run<256>(sms, d, h);
+  run<16, 2>(sms, d, h);
+  run<64, 2>(sms, d, h);
+  run<64, 4>(sms, d, h);
+  run<16, 4>(sms, d, h);
   return 0;
 }
