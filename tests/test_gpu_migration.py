@@ -75,6 +75,7 @@ def run_migration(ctx_src, ctx_dst, n_recompute):
     ctx_src.sync()
     ctx_dst.sync()
     out["ya"], out["yb"] = ya.float().cpu().numpy(), yb.float().cpu().numpy()
+    out["x"], out["x1"] = x.float().numpy(), x1.float().numpy()
     for o in {id(ws_a): ws_a, id(ws_b): ws_b}.values():
         o.free()
     a.free()
@@ -100,6 +101,14 @@ def check(out, n_recompute):
     assert np.array_equal(out["before_b"][untouched].view(np.uint32),
                           pb[untouched].view(np.uint32))
     assert rel_l2(out["yb"], out["ya"]) <= 1e-2
+    # the next token on the migrated cache against the fp32 oracle (prompt prefilled, then the
+    # decode row at position PROMPT)
+    from oracle import oracle as O
+    ob = O.OracleBlock(SHAPE, "m1", seed=4)
+    seq = ob.new_seq(PROMPT + 1)
+    ob.forward([seq], [0] * PROMPT, list(range(PROMPT)), out["x"])
+    y_ref = ob.forward([seq], [0], [PROMPT], out["x1"])
+    assert rel_l2(out["yb"], y_ref) <= 1e-2
 
 
 @pytest.mark.parametrize("rec_cp", [(0, 1), (3, 2), (2, 3), (1, 0)])

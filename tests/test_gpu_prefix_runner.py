@@ -44,11 +44,21 @@ def test_prefix_sharing_is_bit_transparent(ctx, mode):
         used_s, saved = shared.kv_bytes()
         used_p, saved_p = private.kv_bytes()
         assert saved > 0 and saved_p == 0 and used_s < used_p
+        outs = [rows(shared, n, d)]
         for _ in range(4):
             shared.decode_step()
             private.decode_step()
             ctx.sync()
-            assert np.array_equal(rows(shared, n, d), rows(private, n, d))
+            outs.append(rows(shared, n, d))
+            assert np.array_equal(outs[-1], rows(private, n, d))
+        # and the shared run against the fp32 oracle along the chains (prefix rows from the
+        # group's stream), teacher-forced per step as test_gpu_runner.py
+        from test_gpu_runner import oracle_chain
+        first_ref, ref = oracle_chain(wl, 4, outs[:-1])
+        for k, (g, r) in enumerate(zip([outs[0]] + outs[1:], [first_ref] + ref)):
+            rel = np.linalg.norm(g - r) / np.linalg.norm(r)
+            cos = ((g * r).sum(1) / np.linalg.norm(g, axis=1) / np.linalg.norm(r, axis=1)).min()
+            assert rel <= 2e-2 and cos >= 0.995, (k, rel, cos)
     else:  # the reference's event order, to completion
         shared.run()
         private.run()

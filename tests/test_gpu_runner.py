@@ -38,6 +38,11 @@ def oracle_chain(wl, n_steps, gpu_inputs):
     for r in range(wl.n_requests):
         p = wl.req_prompt[r]
         x = O.synth(p * s.d_model, wl.seed, f"inputs:req{r + 1}", 1.7320508).reshape(p, s.d_model)
+        pg = getattr(wl, "req_prefix_group", None)
+        if pg is not None and pg[r] >= 0:  # the group's common prefix (bh_workload.req_prefix_*)
+            t = min(wl.req_prefix_tokens[r], p)
+            x[:t] = O.synth(t * s.d_model, wl.seed, f"inputs:prefix{pg[r]}",
+                            1.7320508).reshape(t, s.d_model)
         for b in wl.chains[wl.req_tenant[r]]:
             seqs[(r, b)] = blocks[b].new_seq(max_tok)
             x = bf16_round(blocks[b].forward([seqs[(r, b)]], [0] * p, list(range(p)), x))
