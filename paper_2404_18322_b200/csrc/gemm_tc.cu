@@ -505,7 +505,13 @@ __global__ void __launch_bounds__(192, CTAS)
       const int f = m0 + q * 32 + lane;
       const int a = seg & 1;
       const uint32_t u = (uint32_t)(seg >> 1);
+#ifdef BE_EXP_NO_FIXUP  // experiments: owners finish their own share, no partials (wrong sums)
+      const bool owner_only = !(kb0 == 0 && kb1 == nkb) &&
+                              (int)blockIdx.x == R.cta_of((long long)tile * nkb);
+      const bool whole = (kb0 == 0 && kb1 == nkb) || owner_only;
+#else
       const bool whole = kb0 == 0 && kb1 == nkb;
+#endif
       const bool runs_epilogue = whole || (int)blockIdx.x == R.cta_of((long long)tile * nkb);
       float* rs = nullptr;
       if (E.ss_in != nullptr && runs_epilogue) {
@@ -536,8 +542,14 @@ __global__ void __launch_bounds__(192, CTAS)
       tc_fence_after();
       if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
       __syncwarp();
-#ifdef BE_EXP_NO_EPI  // experiments: the mainloop alone (no partials, no fixup, no stores)
+#if defined(BE_EXP_NO_EPI) || defined(BE_EXP_NO_EPI_MODE)
+      // experiments: the mainloop alone (no partials, no fixup, no stores), for every mode or
+      // for one epilogue mode only
+#ifdef BE_EXP_NO_EPI_MODE
+      if (MODE == BE_EXP_NO_EPI_MODE) {
+#else
       if (true) {
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
@@ -574,6 +586,10 @@ __global__ void __launch_bounds__(192, CTAS)
         int* ctr = E.counters + tile;
         if (E.trace != nullptr && warp == 2 && lane == 0)  // diagnostics: last segment's role
           E.trace[blockIdx.x * 8 + 6] = (int)blockIdx.x == c_first ? 1000000 + n_contrib : 2000000;
+#ifdef BE_EXP_NO_FIXUP
+        if (true) {
+        } else
+#endif
         if ((int)blockIdx.x != c_first) {
           float4* slot = part4(blockIdx.x) + row;
 #pragma unroll 1
