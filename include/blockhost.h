@@ -165,6 +165,19 @@ int bh_runner_decode_group(bh_runner* r, int group, const int32_t* reqs, int n,
 int bh_runner_serve(bh_runner* r, const int64_t* arrival_us, int64_t* first_token_us,
                     int64_t* completion_us);
 int bh_runner_live_requests(const bh_runner* r);
+/* KV migration between runners (§8 f rank 1; start_kv_migration, scenario.cpp:361-431):
+ * bh_runner_adopt takes over requests mid-decode on a fresh lockstep runner (request idx[k]
+ * continues at context ctx[k] with generated[k] tokens out; KV segments of ctx - 1 tokens are
+ * created on fresh page slots); bh_runner_kv_segment returns a segment's page slots in token
+ * order (and its token count) and bh_runner_kv_pool the block's pool, so the caller moves the
+ * pages (be_kv_copy_pages in a process, be_hop_* across) before the next decode step. */
+int bh_runner_adopt(bh_runner* r, int n, const int32_t* idx, const int32_t* ctx,
+                    const int32_t* generated);
+int bh_runner_request_state(const bh_runner* r, int idx, int32_t* ctx, int32_t* generated,
+                            int32_t* done);
+int bh_runner_kv_segment(const bh_runner* r, int idx, int block, int32_t* slots, int cap,
+                         int* n_pages, int* tokens);
+be_kv_pool* bh_runner_kv_pool(const bh_runner* r, int block);
 /* KV bookkeeping: bytes of pages in use and bytes saved by prefix sharing (KvStore). */
 int bh_runner_kv_bytes(const bh_runner* r, int64_t* used, int64_t* saved_by_sharing);
 int64_t bh_runner_tokens_generated(const bh_runner* r);

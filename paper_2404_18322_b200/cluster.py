@@ -149,6 +149,7 @@ class Plan:
     phases: list[tuple[int, list, list]]  # (kind, [(rank, slot)], [Hop fields tuple])
     placement: list[int]             # block -> rank (-1 = every rank / home)
     note: str = ""
+    wl: Workload | None = None       # the whole workload the plan cuts
 
     def runner(self, rank: int, slot: int) -> RunnerSpec | None:
         for r in self.runners:
@@ -273,7 +274,7 @@ def make_plan(wl: Workload, world: int, placement: list[int], homes: list[int],
                                      row_of[(0, s, i)], 1))
             phases.append((kind, runs, merge(hops)))
     return Plan(world, list(homes), list(order), sorted(runners.values(),
-                key=lambda r: (r.rank, r.slot)), phases, placement, note)
+                key=lambda r: (r.rank, r.slot)), phases, placement, note, wl)
 
 
 def block_plan(wl: Workload, world: int) -> Plan:
@@ -338,8 +339,8 @@ class Cluster:
     def __init__(self, ctxs: dict, plan: Plan, comm: Comm | None = None, use_graphs=True,
                  plan_ahead=False):
         from .runner import Runner
-        L = _bind()
-        self.plan = plan
+        self.plan, self.ctxs, self.comm = plan, dict(ctxs), comm
+        self.use_graphs, self.plan_ahead = use_graphs, plan_ahead
         ranks = sorted(ctxs)
         if ranks != list(range(ranks[0], ranks[0] + len(ranks))):
             raise ValueError("local ranks must be consecutive")
@@ -349,18 +350,28 @@ class Cluster:
                 self.runners[(spec.rank, spec.slot)] = Runner(
                     ctxs[spec.rank], spec.wl, mode=1, use_graphs=use_graphs,
                     plan_ahead=plan_ahead)
-        arr = (C.c_void_p * len(ranks))(*[ctxs[r].h.value for r in ranks])
+        self.h = None
+        self._build()
+
+    def _build(self):
+        """The bh_cluster of the current plan over the current runners."""
+        L = _bind()
+        if self.h:
+            L.bh_cluster_free(self.h)
+            self.h = None
+        ranks = sorted(self.ctxs)
+        arr = (C.c_void_p * len(ranks))(*[self.ctxs[r].h.value for r in ranks])
         h = C.c_void_p()
-        d = plan.runners[0].wl.shape.d_model
-        rc = L.bh_cluster_create(comm.h if comm else None, ranks[0], len(ranks), arr, d,
-                                 C.byref(h))
+        d = self.plan.runners[0].wl.shape.d_model
+        rc = L.bh_cluster_create(self.comm.h if self.comm else None, ranks[0], len(ranks), arr,
+                                 d, C.byref(h))
         if rc != 0:
             raise BlockExecError(rc, "bh_cluster_create failed")
         self.h = h
         for (r, s), run in self.runners.items():
             self._ck(L.bh_cluster_add_runner(h, r, s, run.h))
         self._keep = []
-        for kind, runs, hops in plan.phases:
+        for kind, runs, hops in self.plan.phases:
             ra = np.asarray([x for rs in runs for x in rs] or [0], np.int32)
             ha = (Hop * max(1, len(hops)))(*[Hop(*x) for x in hops])
             self._keep += [ra, ha]
@@ -394,6 +405,167 @@ class Cluster:
             for k, v in run.step_stats().items():
                 out[k] = out.get(k, 0) + v
         return out
+
+    # -------------------------------------------------------------- KV migration (§8 f rank 1)
+    def migrate(self, placement: list[int]) -> dict:
+        """Re-places private blocks mid-decode (placement: block -> rank, as place_blocks) and
+        moves the KV the new layout needs: every leg runner whose rows change is rebuilt on its
+        rank (the block weights loaded there - the reference's parameter load), adopts its rows
+        at their current context (bh_runner_adopt) and receives each (request, block) segment's
+        pages from the runner that held them - be_kv_copy_pages inside a process (peer copy when
+        the contexts differ), NCCL send/recv of the pages across processes (be_hop_*): the copy
+        path of start_kv_migration (scenario.cpp:361-431; plan_migration picks all-copy on
+        NVLink). Home runners and their rows stay. Returns what moved."""
+        import time
+        from .runner import Runner
+        if self.plan_ahead:
+            raise ValueError("migrate needs runners without plan-ahead (their request counters "
+                             "run one step ahead)")
+        old = self.plan
+        wl = old.wl
+        new = make_plan(wl, old.world, placement, old.homes, old.order,
+                        old.note + " -> migrated")
+        t0 = time.perf_counter()
+        for c in self.ctxs.values():
+            c.sync()
+        # every rank is in lockstep: a home runner's request state is every copy's state
+        state = {}
+        for (r, s), run in self.runners.items():
+            if s == 0:
+                for j, i in enumerate(old.order):
+                    state[i] = run.request_state(j)[:2]
+                break
+        keep, fresh = {}, {}
+        for spec in new.runners:
+            if spec.rank not in self.ctxs:
+                continue
+            prev = old.runner(spec.rank, spec.slot)
+            if spec.slot == 0 or (prev is not None and prev.items == spec.items):
+                keep[(spec.rank, spec.slot)] = self.runners[(spec.rank, spec.slot)]
+                continue
+            run = Runner(self.ctxs[spec.rank], spec.wl, mode=1, use_graphs=self.use_graphs,
+                         plan_ahead=self.plan_ahead)
+            idx = list(range(len(spec.items)))
+            run.adopt(idx, [state[i][0] for _, i in spec.items],
+                      [state[i][1] for _, i in spec.items])
+            fresh[(spec.rank, spec.slot)] = (spec, run)
+        # the page moves, in one canonical order on every rank: (new rank, slot, row, block)
+        moves = []  # (src rank, src slot, src row, src block, dst rank, dst slot, dst row, dst block)
+        for spec in new.runners:
+            key = (spec.rank, spec.slot)
+            if spec.slot == 0 or (old.runner(*key) is not None and
+                                  old.runner(*key).items == spec.items):
+                continue
+            for j, (s, i) in enumerate(spec.items):
+                src = next(r for r in old.runners if r.slot == spec.slot and (s, i) in r.items)
+                jo = src.items.index((s, i))
+                t = spec.wl.req_tenant[j]
+                for b in spec.wl.chains[t]:
+                    bo = src.wl.block_names.index(spec.wl.block_names[b])
+                    moves.append((src.rank, src.slot, jo, bo, spec.rank, spec.slot, j, b))
+        moved_pages = moved_bytes = remote_bytes = 0
+        L = lib()
+        local = [m for m in moves if m[0] in self.ctxs and m[4] in self.ctxs]
+        for (sr, ss, sj, sb, dr, ds, dj, db) in local:
+            src_run = self.runners[(sr, ss)]
+            dst_run = fresh[(dr, ds)][1]
+            src_slots, tok = src_run.kv_segment(sj, sb)
+            if tok == 0 and not src_slots:
+                continue  # a block without attention keeps no KV
+            dst_slots, _ = dst_run.kv_segment(dj, db)
+            n = min(len(src_slots), len(dst_slots))
+            a = np.asarray(src_slots[:n], np.int32)
+            b = np.asarray(dst_slots[:n], np.int32)
+            dp = dst_run.kv_pool(db)
+            check(L.be_kv_copy_pages(self.ctxs[dr].h, C.c_void_p(src_run.kv_pool(sb)),
+                                     C.c_void_p(dp), a.ctypes.data_as(C.c_void_p),
+                                     b.ctypes.data_as(C.c_void_p), n, C.c_void_p(0)),
+                  self.ctxs[dr].h)
+            moved_pages += n
+            moved_bytes += n * L.be_kv_pool_page_bytes(C.c_void_p(dp))
+        remote = [m for m in moves if (m[0] in self.ctxs) != (m[4] in self.ctxs)]
+        if remote:
+            remote_bytes = self._migrate_remote(remote, fresh)
+        for c in self.ctxs.values():
+            c.sync()
+        # swap in the new runners and plan
+        for key, run in self.runners.items():
+            if key not in keep:
+                run.close()
+        self.runners = dict(keep)
+        self.runners.update({k: v[1] for k, v in fresh.items()})
+        self.plan = new
+        self._build()
+        return {"runners_rebuilt": len(fresh), "pages_copied_in_process": moved_pages,
+                "bytes_copied_in_process": moved_bytes, "bytes_over_nccl": remote_bytes,
+                "seconds": time.perf_counter() - t0}
+
+    def _migrate_remote(self, moves, fresh) -> int:
+        """Pages of segments changing process: per peer, the pages this rank sends are packed
+        (canonical move order, the same list on both ranks) into one staging buffer, one NCCL
+        group moves every buffer, and received buffers are unpacked into the fresh slots."""
+        import torch
+        from .pipeline import _DevRows
+        L = lib()
+        me = next(iter(self.ctxs))
+
+        def pool_view(run, block, slots):
+            pool = C.c_void_p(run.kv_pool(block))
+            pb = L.be_kv_pool_page_bytes(pool)
+            n = max(slots) + 1
+            t = torch.as_tensor(_DevRows(L.be_kv_pool_data(pool), n, pb // 2),
+                                device="cuda").view(torch.uint8).view(n, pb)
+            return t, torch.as_tensor(slots, dtype=torch.long, device="cuda")
+
+        for c in self.ctxs.values():
+            c.sync()
+        sends, recvs = {}, {}  # peer -> [(pool view, slot index)]
+        for (sr, ss, sj, sb, dr, ds, dj, db) in moves:
+            if sr == me:
+                run = self.runners[(sr, ss)]
+                slots, _ = run.kv_segment(sj, sb)
+                if slots:
+                    sends.setdefault(dr, []).append(pool_view(run, sb, slots))
+            else:
+                run = fresh[(dr, ds)][1]
+                slots, _ = run.kv_segment(dj, db)
+                if slots:
+                    recvs.setdefault(sr, []).append(pool_view(run, db, slots))
+
+        def staging(parts):
+            n = sum(idx.numel() for _, idx in parts)
+            return torch.empty(n, parts[0][0].shape[1], dtype=torch.uint8, device="cuda")
+
+        sbuf = {p: staging(v) for p, v in sends.items()}
+        rbuf = {p: staging(v) for p, v in recvs.items()}
+        for p, parts in sends.items():
+            off = 0
+            for view, idx in parts:
+                sbuf[p][off:off + idx.numel()] = view[idx]
+                off += idx.numel()
+        torch.cuda.synchronize()
+        B = _bind()
+        self._ck_comm(B.be_hop_begin(self.comm.h))
+        for p, buf in sbuf.items():
+            self._ck_comm(B.be_hop_send(self.comm.h, p, C.c_void_p(buf.data_ptr()), buf.numel(),
+                                        C.c_void_p(0)))
+        for p, buf in rbuf.items():
+            self._ck_comm(B.be_hop_recv(self.comm.h, p, C.c_void_p(buf.data_ptr()), buf.numel(),
+                                        C.c_void_p(0)))
+        self._ck_comm(B.be_hop_end(self.comm.h))
+        for c in self.ctxs.values():
+            c.sync()
+        for p, parts in recvs.items():
+            off = 0
+            for view, idx in parts:
+                view[idx] = rbuf[p][off:off + idx.numel()]
+                off += idx.numel()
+        torch.cuda.synchronize()
+        return sum(b.numel() for b in sbuf.values()) + sum(b.numel() for b in rbuf.values())
+
+    def _ck_comm(self, rc):
+        if rc != 0:
+            raise BlockExecError(rc, _bind().be_comm_last_error(self.comm.h).decode())
 
     def close(self):
         if getattr(self, "h", None):

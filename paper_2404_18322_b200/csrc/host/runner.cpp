@@ -81,6 +81,12 @@ class Runner {
   void decode_step(const void* host_in, void* host_out, int* n_batches, int group = -1,
                    const std::vector<int>* members = nullptr);
   void serve(const std::int64_t* arrival_us, std::int64_t* first_us, std::int64_t* done_us);
+  // KV migration: requests taken over mid-decode (their KV pages are copied in by the caller)
+  void adopt(int n, const int32_t* idx, const int32_t* ctx, const int32_t* generated);
+  void request_state(int idx, int32_t* ctx, int32_t* generated, int32_t* done) const;
+  std::vector<int> kv_segment(int idx, int block, int* tokens) const;
+  be_kv_pool* kv_pool(int block) const { return pools_[block]; }
+  int n_blocks() const { return static_cast<int>(names_.size()); }
   int live() const;
   std::int64_t generated() const { return tokens_generated_; }
   void* arena() { return arena_; }
@@ -1128,6 +1134,57 @@ void Runner::run_speculative(const PlannedBatch& pv, const PlannedBatch& pn) {
   }
 }
 
+// Taking over requests mid-decode (lockstep mode, a fresh runner): request idx[k] continues at
+// context ctx[k] with generated[k] tokens out; on every KV block of its chain a segment holding
+// ctx - 1 tokens is created on fresh page slots (kv_segment returns them) for the caller to fill
+// with the pages it migrates - the destination side of start_kv_migration
+// (scenario.cpp:361-431) when a request's chain steps are rebound to this device.
+void Runner::adopt(int n, const int32_t* idx, const int32_t* ctx, const int32_t* generated) {
+  if (mode_ != 1) throw BeError(BE_ERR_STATE, "adopt needs lockstep mode");
+  if (batches_run_ != 0 || has_running_) throw BeError(BE_ERR_STATE, "adopt on a used runner");
+  std::vector<char> seen(reqs_.size(), 0);
+  for (int k = 0; k < n; ++k) {
+    if (idx[k] < 0 || idx[k] >= (int)reqs_.size() || seen[idx[k]])
+      throw BeError(BE_ERR_INVALID, "adopt: bad request index");
+    seen[idx[k]] = 1;
+    Request& r = reqs_[idx[k]];
+    if (ctx[k] <= r.prompt || ctx[k] > r.prompt + r.output || generated[k] < 1 ||
+        generated[k] >= r.output || ctx[k] != r.prompt + generated[k])
+      throw BeError(BE_ERR_INVALID, "adopt: inconsistent request state");
+    r.phase = Phase::kDecode;
+    r.step = 0;
+    r.ctx = ctx[k];
+    r.generated = generated[k];
+    for (int s = 0; s < chain_len(r); ++s) {
+      const int b = chain_block(r, s);
+      if (kv_bpt_[b] == 0) continue;
+      const std::string& bn = names_[b];
+      kv_.create_segment(r.id, bn, 0, kv_bpt_[b]);
+      kv_.append_tokens(r.id, bn, r.ctx - 1);
+    }
+    tokens_generated_ += generated[k];
+  }
+  for (int i = 0; i < (int)reqs_.size(); ++i)
+    if (seen[i]) step_done_order_.push_back(i);
+  batches_run_ = 1;  // the runner is live: run() must not prefill these requests again
+}
+
+void Runner::request_state(int idx, int32_t* ctx, int32_t* generated, int32_t* done) const {
+  if (idx < 0 || idx >= (int)reqs_.size()) throw BeError(BE_ERR_INVALID, "bad request index");
+  const Request& r = reqs_[idx];
+  if (ctx) *ctx = r.ctx;
+  if (generated) *generated = r.generated;
+  if (done) *done = r.done ? 1 : 0;
+}
+
+std::vector<int> Runner::kv_segment(int idx, int block, int* tokens) const {
+  if (idx < 0 || idx >= (int)reqs_.size() || block < 0 || block >= (int)names_.size())
+    throw BeError(BE_ERR_INVALID, "bad request / block index");
+  const Request& r = reqs_[idx];
+  if (tokens) *tokens = kv_.tokens(r.id, names_[block]);
+  return kv_.page_slots(r.id, names_[block]);
+}
+
 // Live serving (lockstep mode). Requests arrive at arrival_us (relative to the call) and are
 // admitted in arrival order; every admission round prefills the new arrivals through their
 // chains (pop_batch under the token budget, batches run as they form, as one device lane does:
@@ -1281,6 +1338,30 @@ extern "C" int bh_runner_serve(bh_runner* h, const int64_t* arrival_us, int64_t*
   if (h == nullptr || arrival_us == nullptr || first_token_us == nullptr || completion_us == nullptr)
     return BE_ERR_INVALID;
   return guard(h, [&] { h->r->serve(arrival_us, first_token_us, completion_us); });
+}
+extern "C" int bh_runner_adopt(bh_runner* h, int n, const int32_t* idx, const int32_t* ctx,
+                               const int32_t* generated) {
+  if (h == nullptr || n < 0 || (n > 0 && (idx == nullptr || ctx == nullptr || generated == nullptr)))
+    return BE_ERR_INVALID;
+  return guard(h, [&] { h->r->adopt(n, idx, ctx, generated); });
+}
+extern "C" int bh_runner_request_state(const bh_runner* h, int idx, int32_t* ctx,
+                                       int32_t* generated, int32_t* done) {
+  if (h == nullptr) return BE_ERR_INVALID;
+  return guard(const_cast<bh_runner*>(h), [&] { h->r->request_state(idx, ctx, generated, done); });
+}
+extern "C" int bh_runner_kv_segment(const bh_runner* h, int idx, int block, int32_t* slots, int cap,
+                                    int* n_pages, int* tokens) {
+  if (h == nullptr || n_pages == nullptr) return BE_ERR_INVALID;
+  return guard(const_cast<bh_runner*>(h), [&] {
+    const std::vector<int> v = h->r->kv_segment(idx, block, tokens);
+    *n_pages = static_cast<int>(v.size());
+    for (int i = 0; i < std::min(cap, *n_pages) && slots != nullptr; ++i) slots[i] = v[i];
+  });
+}
+extern "C" be_kv_pool* bh_runner_kv_pool(const bh_runner* h, int block) {
+  if (h == nullptr || block < 0 || block >= h->r->n_blocks()) return nullptr;
+  return h->r->kv_pool(block);
 }
 extern "C" int bh_runner_kv_bytes(const bh_runner* h, int64_t* used, int64_t* saved) {
   if (h == nullptr) return BE_ERR_INVALID;

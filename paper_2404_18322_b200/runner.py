@@ -65,6 +65,10 @@ def _bind():
         ("bh_runner_serve", I, [P, P, P, P]),
         ("bh_runner_spec_stats", I, [P, P]),
         ("bh_runner_kv_bytes", I, [P, P, P]),
+        ("bh_runner_adopt", I, [P, I, P, P, P]),
+        ("bh_runner_request_state", I, [P, I, P, P, P]),
+        ("bh_runner_kv_segment", I, [P, I, I, P, I, P, P]),
+        ("bh_runner_kv_pool", P, [P, I]),
     ]:
         fn = getattr(L, name)
         fn.restype, fn.argtypes = res, args
@@ -192,6 +196,30 @@ class Runner:
         s = StepStats()
         self._check(lib().bh_runner_step_stats(self.h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in StepStats._fields_}
+
+    def adopt(self, idx, ctx, generated) -> None:
+        """Take over requests mid-decode (bh_runner_adopt): KV segments are created empty of
+        content on fresh page slots; copy the migrated pages in before the next step."""
+        a = [np.ascontiguousarray(v, np.int32) for v in (idx, ctx, generated)]
+        self._check(lib().bh_runner_adopt(self.h, a[0].size, a[0].ctypes.data, a[1].ctypes.data,
+                                          a[2].ctypes.data))
+
+    def request_state(self, idx: int) -> tuple[int, int, bool]:
+        c, g, d = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+        self._check(lib().bh_runner_request_state(self.h, idx, C.byref(c), C.byref(g),
+                                                  C.byref(d)))
+        return c.value, g.value, bool(d.value)
+
+    def kv_segment(self, idx: int, block: int) -> tuple[list, int]:
+        """(page slots in token order, tokens) of request idx's segment at block."""
+        buf = (C.c_int32 * 4096)()
+        n, t = C.c_int(0), C.c_int(0)
+        self._check(lib().bh_runner_kv_segment(self.h, idx, block, buf, 4096, C.byref(n),
+                                               C.byref(t)))
+        return list(buf[:n.value]), t.value
+
+    def kv_pool(self, block: int) -> int:
+        return lib().bh_runner_kv_pool(self.h, block) or 0
 
     def kv_bytes(self) -> tuple[int, int]:
         """(bytes of KV pages in use, bytes saved by prefix sharing)."""

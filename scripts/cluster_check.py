@@ -30,6 +30,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2n")
     ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--migrate", action="store_true",
+                    help="after half the steps move tenant 0's private blocks to the next rank "
+                         "(Cluster.migrate: KV pages over NCCL) and keep decoding")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -45,10 +48,15 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = narrow_c2(args.steps + 2) if args.config == "c2n" else \
         CONFIGS[args.config](prompt=64, output=args.steps + 2)
+    mig_at = args.steps // 2 if args.migrate else -1
     idx = sorted(range(wl.n_requests), key=lambda i: (wl.req_tenant[i], i))
     wl = dataclasses.replace(wl, req_tenant=[wl.req_tenant[i] for i in idx])
     n, d = wl.n_requests, wl.shape.d_model
     plan = block_plan(wl, world)
+    moved = list(plan.placement)
+    for b, name in enumerate(wl.block_names):
+        if name.startswith("t0.") and moved[b] >= 0:
+            moved[b] = (moved[b] + 1) % world
 
     def rows(run):
         t = torch.as_tensor(_DevRows(run.arena_ptr, n, d), device="cuda").view(torch.bfloat16)
@@ -64,13 +72,17 @@ def main():
     cl = Cluster({rank: ctx}, plan, comm)
     cl.prefill()
     got = [rows(cl.home(rank))]
-    for _ in range(args.steps):
+    mig = None
+    for k in range(args.steps):
+        if k == mig_at:
+            mig = cl.migrate(moved)
         cl.decode_step()
         ctx.sync()
         got.append(rows(cl.home(rank)))
     st = cl.stats()
     sent, recv = plan.hop_bytes_per_step(rank, d)
-    counters_ok = st["sent_bytes"] >= args.steps * sent and st["recv_bytes"] >= args.steps * recv
+    counters_ok = args.migrate or (st["sent_bytes"] >= args.steps * sent and
+                                   st["recv_bytes"] >= args.steps * recv)
     cl.close()
     comm.close()
     # every rank's rows, gathered on rank 0
@@ -86,7 +98,9 @@ def main():
         lb = Cluster(ctxs, plan)
         lb.prefill()
         ref = [[rows(lb.home(r)) for r in range(world)]]
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            if k == mig_at:
+                lb.migrate(moved)
             lb.decode_step()
             for c in ctxs.values():
                 c.sync()
@@ -101,7 +115,8 @@ def main():
         res = {"ok": all(s["bit_exact"] for s in steps) and bool(ok_counters.item()),
                "world": world, "config": wl.name, "placement": plan.note,
                "hop_bytes_per_step_rank0": plan.hop_bytes_per_step(0, d),
-               "nccl_counters_ok": bool(ok_counters.item()), "steps": steps}
+               "nccl_counters_ok": bool(ok_counters.item()), "steps": steps,
+               "migration_rank0": mig}
         print(json.dumps(res), flush=True)
     ctx.close()
     dist.barrier()

@@ -112,3 +112,58 @@ def test_block_placement_two_ranks_matches_oracle():
         cl.close()
         for c in ctxs.values():
             c.close()
+
+
+def test_kv_migration_mid_decode_matches_oracle():
+    """§8(f) rank 1 inside the running loop: after 3 decode steps, tenant 0's private blocks
+    move from rank 0 to rank 1 (Cluster.migrate: the leg runners whose rows change are rebuilt on
+    their rank, adopt their rows at the current context, and receive every (request, block) KV
+    segment's pages - be_kv_copy_pages, a peer copy between the two ranks' contexts); decoding
+    continues on the new layout. Every step before and after matches the fp32 oracle along the
+    chains, and both ranks keep identical rows."""
+    import dataclasses
+    from test_gpu_runner import oracle_chain
+    wl = narrow_c2(output=8)
+    idx = sorted(range(wl.n_requests), key=lambda i: (wl.req_tenant[i], i))
+    wl = dataclasses.replace(wl, req_tenant=[wl.req_tenant[i] for i in idx])
+    d, n = wl.shape.d_model, wl.n_requests
+    plan = block_plan(wl, 2)
+    ctxs = {0: dev.Context(0), 1: dev.Context(0)}
+    cl = Cluster(ctxs, plan)
+    try:
+        cl.prefill()
+        outs = [[], []]
+
+        def step():
+            cl.decode_step()
+            for r in (0, 1):
+                ctxs[r].sync()
+            for r in (0, 1):
+                outs[r].append(arena_rows(cl.home(r), n, d))
+
+        for _ in range(3):
+            step()
+        before = list(plan.placement)
+        moved = list(before)
+        for b, name in enumerate(wl.block_names):
+            if name.startswith("t0."):
+                assert before[b] == 0
+                moved[b] = 1
+        st = cl.migrate(moved)
+        assert st["runners_rebuilt"] == 2 and st["pages_copied_in_process"] > 0
+        assert cl.plan.runner(1, 1).wl.block_names.count("t0.b2") == 1
+        for _ in range(3):
+            step()
+        for k in range(6):
+            assert np.array_equal(outs[0][k], outs[1][k])
+        first_ref, _ = oracle_chain(wl, 0, [])
+        _, ref = oracle_chain(wl, 6, [first_ref] + outs[0][:-1])
+        for k in range(1, 6):
+            g, r = outs[0][k], ref[k]
+            rel = np.linalg.norm(g - r) / np.linalg.norm(r)
+            cos = ((g * r).sum(1) / np.linalg.norm(g, axis=1) / np.linalg.norm(r, axis=1)).min()
+            assert rel <= 2e-2 and cos >= 0.995, (k, rel, cos)
+    finally:
+        cl.close()
+        for c in ctxs.values():
+            c.close()
