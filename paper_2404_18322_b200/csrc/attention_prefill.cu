@@ -36,9 +36,11 @@ struct PrefillAttnParams {
   int* tiles;                 // [rows + 1] tile start rows, then the count at tiles[rows]
 };
 
-// One CTA, up to 1024 threads: row r starts a tile if r == 0 or its (pt_row, pos / 64) differs
-// from row r-1's; starts are compacted in order (block-wide scan in chunks).
-__global__ void tile_index_kernel(const int* __restrict__ tok, int rows, int* __restrict__ tiles) {
+// One CTA, up to 1024 threads: row r starts a tile if r == 0 or its (pt_row, pos >> shift)
+// differs from row r-1's (64-row tiles here, 128 for the tcgen05 kernel); starts are compacted in
+// order (block-wide scan in chunks).
+__global__ void tile_index_kernel(const int* __restrict__ tok, int rows, int* __restrict__ tiles,
+                                  int shift) {
   __shared__ int warp_sums[32];
   __shared__ int base;
   if (threadIdx.x == 0) base = 0;
@@ -48,9 +50,9 @@ __global__ void tile_index_kernel(const int* __restrict__ tok, int rows, int* __
     const int r = r0 + threadIdx.x;
     int start = 0;
     if (r < rows) {
-      const int key_pt = tok[(size_t)r * 5 + 4], key_p = tok[(size_t)r * 5 + 3] >> 6;
+      const int key_pt = tok[(size_t)r * 5 + 4], key_p = tok[(size_t)r * 5 + 3] >> shift;
       start = r == 0 || tok[(size_t)(r - 1) * 5 + 4] != key_pt ||
-              (tok[(size_t)(r - 1) * 5 + 3] >> 6) != key_p;
+              (tok[(size_t)(r - 1) * 5 + 3] >> shift) != key_p;
     }
     // inclusive scan of `start` over the block
     int v = start;
@@ -298,10 +300,15 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnParams P) 
   }
 }
 
+cudaError_t launch_tile_index(const int* tok, int rows, int* tiles, int shift, cudaStream_t stream) {
+  tile_index_kernel<<<1, 1024, 0, stream>>>(tok, rows, tiles, shift);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_attention_prefill(const PrefillAttnParams& P, int head_dim, int num_sms,
                                      cudaStream_t stream) {
   if (P.rows <= 0) return cudaSuccess;
-  tile_index_kernel<<<1, 1024, 0, stream>>>(P.tok, P.rows, P.tiles);
+  tile_index_kernel<<<1, 1024, 0, stream>>>(P.tok, P.rows, P.tiles, 6);
   const int grid = num_sms * 4;
   auto run = [&](auto kern, int hd) {
     const int smem = 2 * 2 * 64 * (hd + 8) * 2;  // [K,V][2 buffers][64][hd + 8] bf16

@@ -74,6 +74,20 @@ struct PrefillAttnParams {
   __nv_bfloat16* out;
   int* tiles;
 };
+struct PrefillTcParams {
+  const int* page_table;
+  int pt_stride;
+  const int* tok;
+  int rows;
+  int H;
+  int layer, n_layers;
+  float scale_log2;
+  __nv_bfloat16* out;
+  const int* tiles;
+};
+cudaError_t launch_attention_prefill_tc(const PrefillTcParams& P, const CUtensorMap& map_q,
+                                        const CUtensorMap& map_kv, int num_sms,
+                                        cudaStream_t stream);
 cudaError_t launch_attention_prefill(const PrefillAttnParams&, int head_dim, int num_sms,
                                      cudaStream_t);
 }  // namespace bx
@@ -94,7 +108,8 @@ struct be_ctx {
   int* gemm_counters = nullptr;
   int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
   int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
-  int prefill_tc = 1;     // tensor-core prefill attention (BE_PREFILL_TC=0: the per-row kernel)
+  int prefill_tc = 1;     // prefill attention: 1 tcgen05 (hd 128; mma.sync for hd 64), 2 mma.sync,
+                          // 0 the per-row decode kernel (BE_PREFILL_TC)
   int attn_splits_force = 0;  // decode attention split-K count (BE_ATTN_SPLITS=1..16; 0 = auto)
   // per-launch event timing of exec_batch kernels (be_prof_enable); off on the hot path
   struct ProfRec {
@@ -143,6 +158,10 @@ struct be_kv_pool {
   long long page_elems = 0;
   long long layer_elems = 0;
   int n_layers = 0, n_heads = 0, head_dim = 0;
+  // 5-D TMA map [page*layers + layer][K|V][head][16 tokens][hd], box {64, 16, 1, 1, 1}: the
+  // tcgen05 prefill attention's K / V page loads (encoded on first use)
+  CUtensorMap m_kv{};
+  bool has_m_kv = false;
 };
 
 // LoRA adapter of a block's attention components: per attention layer
@@ -181,6 +200,8 @@ struct be_workspace {
   size_t pt_capacity = 0;
   // TMA maps of the B operands by BN (16..256)
   std::map<int, CUtensorMap> m_xb, m_attn, m_h;
+  CUtensorMap m_q{};        // q rows, box {64, 128}: the tcgen05 prefill attention's Q tiles
+  bool has_m_q = false;
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -295,7 +316,7 @@ extern "C" int be_ctx_create(int device, be_ctx** out) {
   ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   if (const char* g = getenv("BE_GEMM_GRID")) ctx->gemm_grid_cap = atoi(g);
   if (const char* p = getenv("BE_PDL")) ctx->use_pdl = atoi(p) != 0;
-  if (const char* p = getenv("BE_PREFILL_TC")) ctx->prefill_tc = atoi(p) != 0;
+  if (const char* p = getenv("BE_PREFILL_TC")) ctx->prefill_tc = atoi(p);
   if (const char* p = getenv("BE_ATTN_SPLITS")) {
     const int v = atoi(p);
     ctx->attn_splits_force = v < 0 ? 0 : v > 16 ? 16 : v;
@@ -960,7 +981,41 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     if (ap.tl != nullptr && splits > 1) tl_slot(ctx, BE_K_ATTENTION);  // combine's slot = tl + 1
     {
       ProfScope ps(ctx, st, BE_K_ATTENTION, ntok, H, hd, 0, 0);
-      if (phase == BE_PHASE_PREFILL && n_grp == 1 && ctx->prefill_tc) {
+      if (phase == BE_PHASE_PREFILL && n_grp == 1 && ctx->prefill_tc == 1 && hd == 128) {
+        // prompt rows on tcgen05: S and O in TMEM, Q / K / V tiles by TMA
+        if (!ws->has_m_q) {
+          if (make_map(ctx, &ws->m_q, ws->q, ws->max_tok, (uint64_t)H * hd, 128) != BE_OK)
+            return BE_ERR_CUDA;
+          ws->has_m_q = true;
+        }
+        if (!pool->has_m_kv) {
+          cuuint64_t dims[5] = {(cuuint64_t)hd, 16, (cuuint64_t)H, 2,
+                                (cuuint64_t)pool->n_pages * pool->n_layers};
+          cuuint64_t strides[4] = {(cuuint64_t)hd * 2, (cuuint64_t)16 * hd * 2,
+                                   (cuuint64_t)H * 16 * hd * 2, (cuuint64_t)pool->layer_elems * 2};
+          cuuint32_t box[5] = {64, 16, 1, 1, 1};
+          cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+          const CUresult r = ctx->encode(&pool->m_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                                         pool->base, dims, strides, box, estr,
+                                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (r != CUDA_SUCCESS) return fail(ctx, BE_ERR_CUDA, "kv pool tensor map (%d)", (int)r);
+          pool->has_m_kv = true;
+        }
+        bx::PrefillTcParams pt{};
+        pt.page_table = d_pt;
+        pt.pt_stride = pt_stride;
+        pt.tok = tok;
+        pt.rows = ntok;
+        pt.H = H;
+        pt.layer = l;
+        pt.n_layers = pool->n_layers;
+        pt.scale_log2 = ap.scale_log2;
+        pt.out = ws->attn;
+        pt.tiles = ws->prefill_tiles;
+        e = bx::launch_attention_prefill_tc(pt, ws->m_q, pool->m_kv, ctx->num_sms, st);
+      } else if (phase == BE_PHASE_PREFILL && n_grp == 1 && ctx->prefill_tc) {
         // prompt rows: query tiles share K/V tiles on tensor cores
         bx::PrefillAttnParams pp{};
         pp.q = ws->q;
