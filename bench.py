@@ -628,7 +628,6 @@ def run_cluster(args, world, rank, local):
                "ms_per_step": round(e_ms / args.steps, 4)}
     launches = int(stats["launches"])
     cl.close()
-    comm.close()
     replicas = None
     if not args.no_replicas:
         run = Runner(ctx, wl, mode=1, use_graphs=True, plan_ahead=True)
@@ -645,6 +644,9 @@ def run_cluster(args, world, rank, local):
                     + rst["act_bytes"],
                     "layout": "every GPU holds every block and serves its own request mix"}
         run.close()
+    spec = None
+    if args.spec or (args.spec is None and args.config == "c5"):
+        spec = cluster_spec_leg(args, wl, plan, ctx, comm, world, rank, stream, mx)
     if rank == 0:
         hbm = peaks["hbm_gbs"]
         ms_step = ms / args.steps
@@ -664,14 +666,59 @@ def run_cluster(args, world, rank, local):
                               "achieved": round(step_bytes_max / (ms_step / 1e3) / 1e9, 1),
                               "peak": hbm, "unit": "GB/s",
                               "frac": round(step_bytes_max / (ms_step / 1e3) / 1e9 / hbm, 4)},
-            "replicas": replicas, "e2e": e2e, "cpu_baseline": None,
+            "replicas": replicas, "speculation": spec, "e2e": e2e, "cpu_baseline": None,
             "gpu_launches": launches * args.steps, "clocks": clk,
             "prefill_s": round(prefill_s, 2),
             "note": "gpu_launches: this rank's kernels (NCCL's send/recv kernels not counted)",
         }
         print(json.dumps(line), flush=True)
+    comm.close()
     ctx.close()
     dist.destroy_process_group()
+
+
+def cluster_spec_leg(args, wl, plan, ctx, comm, world, rank, stream, mx):
+    """Speculative execution in the block-placed cluster (C5 = configs[4] on N GPUs): the blocks
+    the reference's marking rule picks are shared blocks, present on every rank, so each rank's
+    home runner drafts them with the 50%-FFN surrogate on its second stream, feeds the next block
+    early and verifies with K7 on its own GPU; private blocks and hops as in the plain cluster.
+    Tokens/s against the plain cluster step of the same run; accept counts summed over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2404_18322_b200.cluster import Cluster
+    from paper_2404_18322_b200.pipeline import speculation_blocks
+    blocks, marked = speculation_blocks(wl)
+    out = {"marked_blocks": marked, "speculated_blocks": [wl.block_names[b] for b in blocks],
+           "threshold": args.spec_threshold, "surrogate": "block with its FFN pruned to 50%"}
+    if not blocks:
+        out["note"] = "no marked block whose rows all continue to one block"
+        return out
+    cl = Cluster({rank: ctx}, plan, comm, use_graphs=True, spec_blocks=blocks,
+                 spec_threshold=args.spec_threshold)
+    try:
+        cl.prefill()
+        for _ in range(3):
+            cl.decode_step()
+        ctx.sync()
+        n = cl.home(rank).live
+        steps = max(3, min(args.steps, 10))
+        ms, _ = time_steps(cl.decode_step, stream, steps, dist.barrier)
+        ms = mx(ms)
+        st = cl.spec_stats()
+    finally:
+        cl.close()
+    t = torch.tensor([float(st["rows"]), float(st["accepted"]), float(st["cos_sum"])],
+                     device="cuda", dtype=torch.float64)
+    dist.all_reduce(t)
+    rows, acc, cos_sum = (float(x) for x in t.tolist())
+    out.update({"tokens_per_s": round(n * world * steps / (ms / 1e3), 2),
+                "ms_per_step": round(ms / steps, 4), "steps": steps,
+                "accept_rate": round(acc / rows, 4) if rows else None,
+                "rows_verified_all_ranks": int(rows),
+                "cos_mean": cos_sum / rows if rows else None,
+                "note": "every rank drafts and verifies its own rows of the shared blocks on its "
+                        "GPU; accept counts summed over ranks"})
+    return out
 
 
 def run_ours(args, world, rank, local):

@@ -337,21 +337,46 @@ class Cluster:
     for the ranks of this process (one with a communicator; any number without)."""
 
     def __init__(self, ctxs: dict, plan: Plan, comm: Comm | None = None, use_graphs=True,
-                 plan_ahead=False):
+                 plan_ahead=False, spec_blocks=None, spec_threshold: float = 0.95):
+        """spec_blocks: blocks of plan.wl (global indices) whose decode runs speculatively
+        (bh_workload.spec_blocks); every leg runner holding one speculates on it, the draft and
+        its verification on that runner's GPU (a marked block's successor is in the same leg:
+        the shared blocks the reference's marking rule picks are on every home rank)."""
         from .runner import Runner
         self.plan, self.ctxs, self.comm = plan, dict(ctxs), comm
         self.use_graphs, self.plan_ahead = use_graphs, plan_ahead
+        self.spec_names = {plan.wl.block_names[b] for b in (spec_blocks or [])}
+        self.spec_threshold = spec_threshold
         ranks = sorted(ctxs)
         if ranks != list(range(ranks[0], ranks[0] + len(ranks))):
             raise ValueError("local ranks must be consecutive")
         self.runners = {}
         for spec in plan.runners:
             if spec.rank in ctxs:
-                self.runners[(spec.rank, spec.slot)] = Runner(
-                    ctxs[spec.rank], spec.wl, mode=1, use_graphs=use_graphs,
-                    plan_ahead=plan_ahead)
+                self.runners[(spec.rank, spec.slot)] = self._runner(spec)
         self.h = None
         self._build()
+
+    def _runner(self, spec: RunnerSpec):
+        from .runner import Runner
+        local = [b for b, n in enumerate(spec.wl.block_names) if n in self.spec_names]
+        return Runner(self.ctxs[spec.rank], spec.wl, mode=1, use_graphs=self.use_graphs,
+                      plan_ahead=self.plan_ahead, spec_blocks=local or None,
+                      spec_threshold=self.spec_threshold)
+
+    def spec_stats(self) -> dict:
+        """Speculation counters summed over this process's runners (bh_runner_spec_stats)."""
+        out = {}
+        for run in self.runners.values():
+            for k, v in run.spec_stats().items():
+                if k == "cos_min":
+                    out[k] = min(out.get(k, 1.0), v) if run.spec_stats()["rows"] else out.get(k)
+                elif k not in ("accept_rate", "cos_mean"):
+                    out[k] = out.get(k, 0) + v
+        rows = out.get("rows", 0)
+        out["accept_rate"] = out["accepted"] / rows if rows else None
+        out["cos_mean"] = out["cos_sum"] / rows if rows else None
+        return out
 
     def _build(self):
         """The bh_cluster of the current plan over the current runners."""
@@ -443,8 +468,7 @@ class Cluster:
             if spec.slot == 0 or (prev is not None and prev.items == spec.items):
                 keep[(spec.rank, spec.slot)] = self.runners[(spec.rank, spec.slot)]
                 continue
-            run = Runner(self.ctxs[spec.rank], spec.wl, mode=1, use_graphs=self.use_graphs,
-                         plan_ahead=self.plan_ahead)
+            run = self._runner(spec)
             idx = list(range(len(spec.items)))
             run.adopt(idx, [state[i][0] for _, i in spec.items],
                       [state[i][1] for _, i in spec.items])

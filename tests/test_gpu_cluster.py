@@ -167,3 +167,47 @@ def test_kv_migration_mid_decode_matches_oracle():
         cl.close()
         for c in ctxs.values():
             c.close()
+
+
+@pytest.mark.parametrize("thr", [2.0, -2.0])
+def test_block_placement_with_speculation(thr):
+    """C5 (configs[4]) in the block-placed cluster: the marked shared blocks speculate on every
+    home rank (Cluster(spec_blocks=...)), private blocks and hops as in the plain plan.
+    Threshold 2 rejects every row, so the steps equal the plain cluster's within bf16 rounding;
+    -2 accepts every row. Both ranks' rows stay identical, and each rank's home runner verifies
+    all its rows at every marked block of every step."""
+    import dataclasses
+    from test_gpu_spec_runner import narrow_c5
+    from paper_2404_18322_b200.pipeline import speculation_blocks
+    wl = narrow_c5()
+    idx = sorted(range(wl.n_requests), key=lambda i: (wl.req_tenant[i], i))
+    wl = dataclasses.replace(wl, req_tenant=[wl.req_tenant[i] for i in idx])
+    d, n = wl.shape.d_model, wl.n_requests
+    blocks, _ = speculation_blocks(wl)
+    assert blocks
+    plan = block_plan(wl, 2)
+    ctxs = {0: dev.Context(0), 1: dev.Context(0)}
+    pctxs = {0: dev.Context(0), 1: dev.Context(0)}
+    cl = Cluster(ctxs, plan, spec_blocks=blocks, spec_threshold=thr)
+    plain = Cluster(pctxs, plan)
+    try:
+        cl.prefill()
+        plain.prefill()
+        for k in range(4):
+            cl.decode_step()
+            plain.decode_step()
+            for c in list(ctxs.values()) + list(pctxs.values()):
+                c.sync()
+            g0, g1 = arena_rows(cl.home(0), n, d), arena_rows(cl.home(1), n, d)
+            p0 = arena_rows(plain.home(0), n, d)
+            assert np.isfinite(g0).all() and np.array_equal(g0, g1)
+            rel = np.linalg.norm(g0 - p0) / np.linalg.norm(p0)
+            assert rel <= (2e-2 if thr > 1 else 0.5), (k, rel)
+        st = cl.spec_stats()
+        assert st["runs"] == 4 * len(blocks) * 2 and st["rows"] == 4 * len(blocks) * 2 * n
+        assert st["accepted"] == (0 if thr > 1 else st["rows"])
+    finally:
+        cl.close()
+        plain.close()
+        for c in list(ctxs.values()) + list(pctxs.values()):
+            c.close()
