@@ -263,6 +263,56 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& E, int f, int t0
   }
 }
 
+// kQKV epilogue of one 16-token chunk with the chunk's RoPE (cos, sin) already in registers and
+// its (position, KV slot) pairs in shared memory (prefill, whole tiles): same arithmetic and
+// stores as epilogue_chunk<kQKV>, no per-token branches before the stores.
+__device__ __forceinline__ void qkv_chunk_rr(const EpiParams& E, int f, int t0, float (&v)[16],
+                                             const float* rs, const float2 (&cs)[16],
+                                             const int2* meta) {
+  const int lane = threadIdx.x & 31;
+  const bool odd = (lane & 1) != 0;
+  const int nvalid = E.ntok - t0 < 16 ? E.ntok - t0 : 16;
+  const int d = E.d_model;
+  const int sec = f / d;
+  const int fi = f - sec * d;
+  const int head = fi / E.head_dim;
+  const int e = fi - head * E.head_dim;
+  if (rs != nullptr) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] *= rs[i];
+  }
+  if (sec < 2) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float other = __shfl_xor_sync(0xffffffffu, v[i], 1);
+      v[i] = odd ? v[i] * cs[i].x + other * cs[i].y : v[i] * cs[i].x - other * cs[i].y;
+    }
+  }
+  const int ee = e & ~1;
+  const int H = d / E.head_dim;
+  __nv_bfloat16* kvp = E.n_grp > 1 ? E.kvgrp[t0 / E.grp_rows] : E.kv_pool;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[2 * p] : v[2 * p + 1], 1);
+    const float lo = odd ? recv : v[2 * p];
+    const float hi = odd ? v[2 * p + 1] : recv;
+    const int ti = 2 * p + (odd ? 1 : 0);
+    if (ti >= nvalid) continue;
+    if (sec == 0) {
+      *reinterpret_cast<uint32_t*>(E.out + (size_t)(t0 + ti) * E.ldo + (fi & ~1)) =
+          pack_bf16x2(lo, hi);
+    } else {
+      const int slot = meta[ti].y;
+      if (slot >= 0) {
+        const long long page = slot >> 4;
+        const size_t idx = (size_t)(page * E.page_elems + (long long)E.layer * E.layer_elems) +
+                           ((size_t)((sec - 1) * H + head) * 16 + (slot & 15)) * E.head_dim + ee;
+        *reinterpret_cast<uint32_t*>(kvp + idx) = pack_bf16x2(lo, hi);
+      }
+    }
+  }
+}
+
 // rs[j] = 1/sqrt(sum_g ss[n0 + j][g] / d + eps) for the BN tokens of a tile; warp q of the four
 // epilogue warps takes tokens q, q+4, ...; each lane sums groups lane, lane+32, ... then the warp
 // reduces in a fixed order (bit-reproducible).
@@ -328,7 +378,7 @@ template <int BN, int STAGES, int CTAS, int MODE, bool RR>
 __global__ void __launch_bounds__(192, CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
-                   EpiParams E) {
+                   int rr_gm, EpiParams E) {
   using S = GemmSmem<BN>;
   constexpr uint32_t kTmemCols = tmem_cols<2 * BN>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -345,6 +395,9 @@ __global__ void __launch_bounds__(192, CTAS)
   float* rs_smem = reinterpret_cast<float*>(tmem_holder + 4);  // [2][BN] per-token rstd
   float* lu_smem = rs_smem + 2 * BN;                           // k*Lora: [BN][r] u slices
   int* li_smem = reinterpret_cast<int*>(lu_smem + BN * kLoraRank);  // k*Lora: [BN] adapters
+  // RR kQKV (never a LoRA mode): [2][BN] (position, KV slot) of the tile's tokens, staged under
+  // the mainloop, in the LoRA u region
+  int2* meta_smem = reinterpret_cast<int2*>(lu_smem);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -359,6 +412,22 @@ __global__ void __launch_bounds__(192, CTAS)
   const long long it_end = RR ? (long long)n_my_tiles * nkb : R.begin(blockIdx.x + 1);
   // real tile of a (virtual) tile index of this CTA's range
   auto real_tile = [&](int vt) { return RR ? (int)blockIdx.x + vt * (int)gridDim.x : vt; };
+  // (m, n) of a tile. Stream-K: m fastest. RR: grouped raster - bands of rr_gm weight tiles,
+  // token tiles within a band, m fastest inside it - so the ~148 tiles in flight share a few
+  // weight tiles AND a few token tiles in L2 (m fastest over all m would re-stream the whole
+  // weight matrix from HBM once per token tile).
+  auto tile_mn = [&](int tile, int& m, int& n) {
+    if (!RR) {
+      m = tile % m_tiles;
+      n = tile / m_tiles;
+      return;
+    }
+    const int band = tile / (rr_gm * n_tiles);
+    const int r = tile - band * rr_gm * n_tiles;
+    const int w = m_tiles - band * rr_gm < rr_gm ? m_tiles - band * rr_gm : rr_gm;
+    n = r / w;
+    m = band * rr_gm + (r - n * w);
+  };
 
   if (threadIdx.x == 0) {
     stamp(E, 0);
@@ -396,15 +465,15 @@ __global__ void __launch_bounds__(192, CTAS)
       };
       const int vt0 = (int)(it_begin / nkb);
       const int tile0 = real_tile(vt0);
-      Cur cw{tile0, (int)(it_begin - (long long)vt0 * nkb), tile0 % m_tiles, tile0 / m_tiles};
+      Cur cw{tile0, (int)(it_begin - (long long)vt0 * nkb), 0, 0};
+      tile_mn(tile0, cw.m, cw.n);
       Cur cb = cw;
       auto step = [&](Cur& c) {
         if (++c.kb == nkb) {
           c.kb = 0;
           if constexpr (RR) {
             c.tile += (int)gridDim.x;
-            c.m = c.tile % m_tiles;
-            c.n = c.tile / m_tiles;
+            tile_mn(c.tile, c.m, c.n);
           } else {
             ++c.tile;
             if (++c.m == m_tiles) {
@@ -419,10 +488,12 @@ __global__ void __launch_bounds__(192, CTAS)
         return wb + ((size_t)c.m * nkb + c.kb) * (kBM * kBK);
       };
       constexpr uint32_t stage_bytes = S::kStageBytes;
+      // weights: streamed once (evict first) unless RR's band shares them across token tiles
+      constexpr uint64_t kWPolicy = RR ? kEvictLast : kEvictFirst;
       // weights first: nothing upstream writes them, so they stream under the previous kernel
       for (int i = 0; i < pre; ++i, step(cw)) {
         mbar_arrive_expect_tx(&full[i], stage_bytes);
-        bulk_load(sA + i * S::kABytes, wtile(cw), S::kABytes, &full[i], kEvictFirst);
+        bulk_load(sA + i * S::kABytes, wtile(cw), S::kABytes, &full[i], kWPolicy);
       }
       pdl_wait();  // activations are produced by the previous kernel
       stamp(E, 2);
@@ -434,7 +505,7 @@ __global__ void __launch_bounds__(192, CTAS)
       for (long long i = pre; i < n_it; ++i, step(cw)) {
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_arrive_expect_tx(&full[s], stage_bytes);
-        bulk_load(sA + s * S::kABytes, wtile(cw), S::kABytes, &full[s], kEvictFirst);
+        bulk_load(sA + s * S::kABytes, wtile(cw), S::kABytes, &full[s], kWPolicy);
         tma_load_2d(&map_x, &full[s], sB + s * S::kBBytes, cw.kb * kBK, cw.n * BN, kEvictLast);
         if (++s == STAGES) {
           s = 0;
@@ -500,7 +571,8 @@ __global__ void __launch_bounds__(192, CTAS)
       const long long left = it_end - it;
       const int kb1 = (int)((nkb - kb0) < left ? nkb : kb0 + left);
       it += kb1 - kb0;
-      const int m_tile = tile % m_tiles, n_tile = tile / m_tiles;
+      int m_tile, n_tile;
+      tile_mn(tile, m_tile, n_tile);
       const int m0 = m_tile * kBM, n0 = n_tile * BN;
       const int f = m0 + q * 32 + lane;
       const int a = seg & 1;
@@ -513,6 +585,18 @@ __global__ void __launch_bounds__(192, CTAS)
       const bool whole = kb0 == 0 && kb1 == nkb;
 #endif
       const bool runs_epilogue = whole || (int)blockIdx.x == R.cta_of((long long)tile * nkb);
+      if constexpr (RR && MODE == kQKV) {
+        // the tile's token positions / KV slots for the RoPE and KV stores below (one L2 round
+        // trip per tile instead of one per 16-token chunk); double-buffered like rs
+        int2* meta = meta_smem + (seg & 1) * BN;
+        for (int k = threadIdx.x - 64; k < BN; k += 128) {
+          const int t = n0 + k;
+          meta[k] = t < E.ntok ? make_int2(__ldg(E.tok + (size_t)t * 5 + 3),
+                                           __ldg(E.tok + (size_t)t * 5 + 2))
+                               : make_int2(0, -1);
+        }
+        if (E.ss_in == nullptr) named_bar_sync(2, 128);
+      }
       float* rs = nullptr;
       if (E.ss_in != nullptr && runs_epilogue) {
         // the norm statistics of this tile's tokens, computed under the mainloop
@@ -557,7 +641,34 @@ __global__ void __launch_bounds__(192, CTAS)
       }
 #endif
       const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN);
-      if (whole) {
+      if (RR && MODE == kQKV) {
+        // prefill QKV: the next chunk's RoPE (cos, sin) loads are in flight while this chunk
+        // is rotated and stored
+        const int2* meta = meta_smem + (seg & 1) * BN;
+        const bool rope = f / E.d_model < 2;  // q / k rows (warp-uniform)
+        const int e2 = ((f % E.d_model) % E.head_dim) >> 1;
+        float2 csa[16], csb[16];
+        auto load_cs = [&](int c0, float2 (&cs)[16]) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int pos = meta[c0 + i].x;
+            cs[i] = __ldg(E.rope + (size_t)(pos > 0 ? pos : 0) * (E.head_dim >> 1) + e2);
+          }
+        };
+        if (rope) load_cs(0, csa);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          if (n0 + c0 >= E.ntok) break;
+          float acc[16];
+          if (rope && c0 + 16 < BN && n0 + c0 + 16 < E.ntok) load_cs(c0 + 16, csb);
+          tmem_ld16(t_lane + c0, acc);
+          qkv_chunk_rr(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr, csa, meta + c0);
+          if (c0 + 16 >= BN || n0 + c0 + 16 >= E.ntok) break;
+          if (rope && c0 + 32 < BN && n0 + c0 + 32 < E.ntok) load_cs(c0 + 32, csa);
+          tmem_ld16(t_lane + c0 + 16, acc);
+          qkv_chunk_rr(E, f, n0 + c0 + 16, acc, rs ? rs + c0 + 16 : nullptr, csb, meta + c0 + 16);
+        }
+      } else if (whole) {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           if (n0 + c0 >= E.ntok) break;
@@ -719,7 +830,8 @@ static cudaError_t launch_bn_rr(const GemmLaunch& L, cudaStream_t stream) {
   constexpr int CTAS = gemm_ctas<BN>();  // resident CTAs per SM the register budget allows
   constexpr int smem = STAGES * GemmSmem<BN>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
                        2 * BN * 4 /*rstd*/ +
-                       (MODE >= kQKVLora ? BN * (kLoraRank + 1) * 4 : 0) /*LoRA u, adapters*/;
+                       (MODE >= kQKVLora ? BN * (kLoraRank + 1) * 4 : 0) /*LoRA u, adapters*/ +
+                       (RR && MODE == kQKV ? 2 * BN * 8 : 0) /*token metadata*/;
   auto kern = gemm_sk_kernel<BN, STAGES, CTAS, MODE, RR>;
   static unsigned long long configured = 0;  // per device: the attribute is device state
   int dev = 0;
@@ -741,7 +853,13 @@ static cudaError_t launch_bn_rr(const GemmLaunch& L, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = L.pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, L.w_packed, *L.map_x, L.K, m_tiles, n_tiles,
+  // RR band width in weight tiles (BE_GEMM_RR_GM: experiments; 0 = all of them, m fastest)
+  static const int kRRGm = [] {
+    const char* e = getenv("BE_GEMM_RR_GM");
+    return e ? atoi(e) : 16;
+  }();
+  const int rr_gm = kRRGm > 0 && kRRGm < m_tiles ? kRRGm : m_tiles;
+  return cudaLaunchKernelEx(&cfg, kern, L.w_packed, *L.map_x, L.K, m_tiles, n_tiles, rr_gm,
                             L.epi);
 }
 
