@@ -33,7 +33,8 @@ struct PrefillAttnParams {
   int H;
   float scale_log2;
   __nv_bfloat16* out;         // [rows][H*hd]
-  int* tiles;                 // [rows + 1] tile start rows, then the count at tiles[rows]
+  int* tiles;                 // [rows + 2] tile start rows, the count at tiles[rows], a work
+                              // counter at tiles[rows + 1]
 };
 
 // One CTA, up to 1024 threads: row r starts a tile if r == 0 or its (pt_row, pos >> shift)
@@ -79,7 +80,10 @@ __global__ void tile_index_kernel(const int* __restrict__ tok, int rows, int* __
     if (threadIdx.x == blockDim.x - 1) base += before + start;
     __syncthreads();
   }
-  if (threadIdx.x == 0) tiles[rows] = base;
+  if (threadIdx.x == 0) {
+    tiles[rows] = base;
+    tiles[rows + 1] = 0;  // work counter of the tcgen05 kernel's dynamic item queue
+  }
 }
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {

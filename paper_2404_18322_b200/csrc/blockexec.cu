@@ -192,7 +192,7 @@ struct be_workspace {
   size_t splitws_elems = 0;
   int* counters = nullptr;
   int n_counters = 0;
-  int* prefill_tiles = nullptr;  // [max_tok + 1] query tiles of the tensor-core prefill attention
+  int* prefill_tiles = nullptr;  // [max_tok + 2] query tiles of the tensor-core prefill attention
   float* attn_part = nullptr;
   size_t attn_part_elems = 0;
   be_token* d_tokens = nullptr;
@@ -580,7 +580,7 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
   ok &= cudaMalloc(&w->splitws, w->splitws_elems * sizeof(float)) == cudaSuccess;
   w->n_counters = 1 << 16;
   ok &= cudaMalloc(&w->counters, w->n_counters * sizeof(int)) == cudaSuccess;
-  ok &= cudaMalloc(&w->prefill_tiles, (T + 1) * sizeof(int)) == cudaSuccess;
+  ok &= cudaMalloc(&w->prefill_tiles, (T + 2) * sizeof(int)) == cudaSuccess;
   const size_t part_rows = T < 1024 ? T : 1024;
   w->attn_part_elems = part_rows * H * 16 * (128 + 2);
   ok &= cudaMalloc(&w->attn_part, w->attn_part_elems * sizeof(float)) == cudaSuccess;
