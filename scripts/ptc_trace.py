@@ -1,6 +1,6 @@
 """Phase timeline of the tcgen05 prefill attention (library built with -DBE_EXP_PTC_TRACE):
-per kv iteration of CTAs 0..3 (thread 0), the ns spent waiting for K, for S = Q K^T, in the
-softmax, at the CTA barrier + waiting for V, and for O += P V.
+per kv iteration of CTAs 0..3 (thread 0), the ns spent waiting for S = Q K^T (and the P V
+before it), in the softmax, at the CTA barrier + waiting for V, issuing P V and the next S.
   BE_LIB_PATH=scripts/variants/libblockexec_ptctrace.so python scripts/ptc_trace.py"""
 import ctypes as C
 import os
@@ -34,14 +34,13 @@ buf = np.zeros((4, 64, 6), np.uint64)
 f = lib().be_exp_ptc_trace
 f.argtypes = [C.c_void_p]
 assert f(buf.ctypes.data) == 0
-names = ["wait_K", "S", "softmax", "bar+wait_V", "PV", "to_next"]
+names = ["wait_S", "softmax", "bar+wait_V", "issue PV+S"]
+cols = [(0, 2), (2, 3), (3, 4), (4, 5)]
 for c in range(4):
     tr = buf[c].astype(np.int64)
-    valid = tr[:, 5] > 0
-    tr = tr[valid]
-    d_ = np.diff(tr, axis=1)
+    tr = tr[tr[:, 5] > 0]
     nxt = tr[1:, 0] - tr[:-1, 5]
     print(f"cta {c}: {len(tr)} iterations; median ns:",
-          {names[i]: int(np.median(d_[:, i])) for i in range(5)},
+          {n: int(np.median(tr[:, b] - tr[:, a])) for n, (a, b) in zip(names, cols)},
           "next-iter gap", int(np.median(nxt)) if len(nxt) else None,
           "total us", round((tr[-1, 5] - tr[0, 0]) / 1e3, 1))
