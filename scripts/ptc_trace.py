@@ -30,12 +30,12 @@ y = torch.empty_like(x)
 for _ in range(2):
     dev.exec_batch(ctx, blk, pool, ws, dev.PHASE_PREFILL, toks, pt, x, y)
 ctx.sync()
-buf = np.zeros((4, 64, 6), np.uint64)
+buf = np.zeros((4, 64, 9), np.uint64)
 f = lib().be_exp_ptc_trace
 f.argtypes = [C.c_void_p]
 assert f(buf.ctypes.data) == 0
-names = ["wait_S", "softmax", "bar+wait_V", "issue PV+S"]
-cols = [(0, 2), (2, 3), (3, 4), (4, 5)]
+names = ["wait_S", "softmax", "bar+wait_V", "issue PV+S", "tmem_ld", "max", "exp+pack", "st+rest"]
+cols = [(0, 2), (2, 3), (3, 4), (4, 5), (2, 6), (6, 7), (7, 8), (8, 3)]
 for c in range(4):
     tr = buf[c].astype(np.int64)
     tr = tr[tr[:, 5] > 0]
