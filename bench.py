@@ -407,6 +407,9 @@ def profile_step(ctx, run, wl, stream, peaks, peaks_kind):
               key=lambda k: fam[k]["ms"])
     a = fam[top]
     traffic = load_traffic().get(top)
+    if traffic and abs(traffic.get("algorithmic_bytes_per_launch", 0) - a["bytes"] / a["launches"]) \
+            > 0.01 * a["bytes"] / a["launches"]:
+        traffic = None  # captured on another workload (the ncu capture is of C2's step)
     roofline = {"bound": "hbm", "kernel": {"gemm": "gemm_sk_kernel (all projections)",
                                            "attention": "attn_decode_kernel"}.get(top, top),
                 "achieved": a["achieved_gbs"], "peak": hbm, "unit": "GB/s", "frac": a["frac"],

@@ -76,6 +76,8 @@ class Runner {
  public:
   Runner(be_ctx* ctx, const bh_workload& w);
   ~Runner();
+  Runner(const Runner&) = delete;
+  Runner& operator=(const Runner&) = delete;
   void run(int max_batches);
   // group -1 / members null: every live request; else one micro-batch (own CUDA graph)
   void decode_step(const void* host_in, void* host_out, int* n_batches, int group = -1,
@@ -136,6 +138,8 @@ class Runner {
   std::vector<int> lora_base_;
   std::vector<be_lora*> loras_;
   std::vector<char> own_block_;
+  void init(const bh_workload& w);  // the constructor's body
+  void release();                    // frees every device / host resource held so far
   int32_t* d_zero_idx_ = nullptr;  // adapter index 0 for every row of a single-variant launch
   int wbase(int b) const { return lora_base_[b] >= 0 ? lora_base_[b] : b; }
   // a LoRA launch adds two shrink kernels per attention component
@@ -231,7 +235,19 @@ class Runner {
   size_t meta_cap_ = 0;
 };
 
+// A construction that fails part-way (e.g. out of device memory for the next pool) frees what
+// it allocated before rethrowing: the destructor does not run for a throwing constructor.
 Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
+  try {
+    init(w);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+void Runner::init(const bh_workload& w) {
+  be_ctx* ctx = ctx_;
   if (w.n_blocks <= 0 || w.n_tenants <= 0 || w.n_requests <= 0 || !w.blocks || !w.chain_ptr ||
       !w.chain_blocks || !w.req_tenant || !w.req_prompt || !w.req_output)
     throw BeError(BE_ERR_INVALID, "runner: incomplete workload");
@@ -412,9 +428,11 @@ Runner::Runner(be_ctx* ctx, const bh_workload& w) : ctx_(ctx) {
   ck(cudaStreamSynchronize(st_), "init");
 }
 
-Runner::~Runner() {
+Runner::~Runner() { release(); }
+
+void Runner::release() {
   for (auto& kv : graphs_) kv.second.reset();
-  if (!dry_) cudaStreamSynchronize(st_);
+  if (!dry_ && st_ != nullptr) cudaStreamSynchronize(st_);
   for (int k = 0; k < 2; ++k) {
     if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
     if (meta_ev_[k]) cudaEventDestroy(meta_ev_[k]);
@@ -423,7 +441,8 @@ Runner::~Runner() {
   if (arena_) cudaFree(arena_);
   if (parena_) cudaFree(parena_);
   if (ws_) be_workspace_free(ws_);
-  for (auto* p : pools_) be_kv_pool_free(p);
+  for (auto* p : pools_)
+    if (p) be_kv_pool_free(p);
   for (size_t b = 0; b < blocks_.size(); ++b)
     if (own_block_[b] && blocks_[b]) be_block_free(blocks_[b]);
   for (auto* l : loras_)
