@@ -211,3 +211,45 @@ def test_block_placement_with_speculation(thr):
         plain.close()
         for c in list(ctxs.values()) + list(pctxs.values()):
             c.close()
+
+
+def test_block_placement_eight_ranks_loopback():
+    """The driver's 8-GPU shape on one GPU: block_plan at world 8 puts C2's four tenants' private
+    blocks on ranks 0-3 (ranks 4-7 hold shared blocks only and send every private leg away);
+    eight contexts in this process, hops as device copies. Every rank's rows follow the fp32
+    oracle along the chains (checked for rank 0, which hosts a private block, and rank 7, which
+    sends all its private legs away). Ranks are not bit-identical here: a guest batch of 32
+    prompts spans several GEMM token tiles whose stream-K k-splits differ, so the same request
+    on two ranks may be summed in another order."""
+    import dataclasses
+    from test_gpu_runner import oracle_chain
+    wl = narrow_c2(output=5)
+    idx = sorted(range(wl.n_requests), key=lambda i: (wl.req_tenant[i], i))
+    wl = dataclasses.replace(wl, req_tenant=[wl.req_tenant[i] for i in idx])
+    d, n = wl.shape.d_model, wl.n_requests
+    plan = block_plan(wl, 8)
+    assert {p for p in plan.placement if p >= 0} == {0, 1, 2, 3}
+    ctxs = {r: dev.Context(0) for r in range(8)}
+    cl = Cluster(ctxs, plan)
+    try:
+        cl.prefill()
+        outs = {0: [], 7: []}
+        for _ in range(4):
+            cl.decode_step()
+            for c in ctxs.values():
+                c.sync()
+            for r in outs:
+                outs[r].append(arena_rows(cl.home(r), n, d))
+        first_ref, _ = oracle_chain(wl, 0, [])
+        for r, got in outs.items():
+            _, ref = oracle_chain(wl, 4, [first_ref] + got[:-1])
+            for k in range(1, 4):
+                g, o = got[k], ref[k]
+                rel = np.linalg.norm(g - o) / np.linalg.norm(o)
+                cos = ((g * o).sum(1) / np.linalg.norm(g, axis=1) / np.linalg.norm(o, axis=1)).min()
+                assert rel <= 2e-2 and cos >= 0.995, (r, k, rel, cos)
+        assert cl.stats()["local_bytes"] > 0
+    finally:
+        cl.close()
+        for c in ctxs.values():
+            c.close()
