@@ -186,6 +186,7 @@ struct be_workspace {
   bf16* attn = nullptr;
   bf16* h = nullptr;
   float* ss = nullptr;  // [max_tok][d / 32] sums of squares of the residual stream (fused RMSNorm)
+  float* rstd = nullptr;  // [max_tok] its per-token rstd, reduced once for round-robin GEMMs
   float* lora_u = nullptr;  // [max_tok][3 * kLoraRank] LoRA shrink outputs
   int32_t* d_lora_idx = nullptr;  // [max_tok] adapter per token (be_exec_lora_batch staging)
   float* splitws = nullptr;
@@ -574,6 +575,7 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
   ok &= cudaMalloc(&w->attn, T * d * sizeof(bf16)) == cudaSuccess;
   ok &= cudaMalloc(&w->h, T * dff * sizeof(bf16)) == cudaSuccess;
   ok &= cudaMalloc(&w->ss, T * (d / 32) * sizeof(float)) == cudaSuccess;
+  ok &= cudaMalloc(&w->rstd, T * sizeof(float)) == cudaSuccess;
   ok &= cudaMalloc(&w->lora_u, T * 3 * bx::kLoraRank * sizeof(float)) == cudaSuccess;
   ok &= cudaMalloc(&w->d_lora_idx, T * sizeof(int32_t)) == cudaSuccess;
   w->splitws_elems = (size_t)16 << 20;  // 64 MB of fp32 split-K partials (L2 sized)
@@ -616,7 +618,7 @@ extern "C" int be_workspace_create(be_ctx* ctx, int d, int dff, int H, int max_t
 extern "C" int be_workspace_free(be_workspace* w) {
   if (w == nullptr) return BE_ERR_INVALID;
   cudaSetDevice(w->ctx->device);
-  void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->ss, w->splitws, w->counters, w->prefill_tiles,
+  void* ptrs[] = {w->X, w->Xb, w->q, w->attn, w->h, w->ss, w->rstd, w->splitws, w->counters, w->prefill_tiles,
                   w->attn_part, w->d_tokens, w->d_pt, w->lora_u, w->d_lora_idx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -780,8 +782,15 @@ int run_gemm(be_ctx* ctx, be_workspace* ws, const bf16* w_packed, const CUtensor
   L.pdl = ctx->use_pdl;
   epi.ws = ws->splitws;
   epi.counters = ws->counters;
+  cudaError_t e = cudaSuccess;
+  if (p.rr && epi.ss_in != nullptr && epi.n_grp <= 1) {
+    // prefill: every weight tile of a token tile needs the same per-token rstd - reduce once
+    e = bx::launch_rstd(epi.ss_in, epi.ss_groups, ntok, epi.norm_eps, ws->rstd, st);
+    if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "rstd: %s", cudaGetErrorString(e));
+    epi.rs_in = ws->rstd;
+  }
   L.epi = epi;
-  cudaError_t e = bx::launch_gemm(L, st);
+  e = bx::launch_gemm(L, st);
   if (e != cudaSuccess)
     return fail(ctx, BE_ERR_CUDA, "gemm N=%d K=%d ntok=%d: %s", N, K, ntok, cudaGetErrorString(e));
   return BE_OK;

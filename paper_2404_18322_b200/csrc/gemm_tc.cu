@@ -599,9 +599,15 @@ __global__ void __launch_bounds__(192, CTAS)
       }
       float* rs = nullptr;
       if (E.ss_in != nullptr && runs_epilogue) {
-        // the norm statistics of this tile's tokens, computed under the mainloop
+        // the norm statistics of this tile's tokens, computed under the mainloop (or reduced
+        // once per token by launch_rstd for round-robin launches)
         rs = rs_smem + (seg & 1) * BN;
-        tile_rstd<BN>(E, n0, q, rs);
+        if (E.rs_in != nullptr) {
+          for (int k = threadIdx.x - 64; k < BN; k += 128)
+            rs[k] = n0 + k < E.ntok ? __ldg(E.rs_in + n0 + k) : 0.f;
+        } else {
+          tile_rstd<BN>(E, n0, q, rs);
+        }
         named_bar_sync(2, 128);
       }
       if constexpr (MODE >= kQKVLora) {
@@ -897,6 +903,29 @@ cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream) {
     case kResidOutLora: return launch_mode<kResidOutLora>(L, stream);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// one warp per token, the same lane split, float4 sums and butterfly order as tile_rstd
+__global__ void __launch_bounds__(256) rstd_kernel(const float* __restrict__ ss, int G, int ntok,
+                                                   float eps, float* __restrict__ rstd) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= ntok) return;
+  const int G4 = G >> 2;
+  const float4* p = reinterpret_cast<const float4*>(ss + (size_t)t * G);
+  const float4 a = lane < G4 ? __ldcg(p + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 b = lane + 32 < G4 ? __ldcg(p + lane + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float s = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) rstd[t] = rsqrtf(s * (1.0f / (float)(G * 32)) + eps);
+}
+
+cudaError_t launch_rstd(const float* ss, int groups, int ntok, float eps, float* rstd,
+                        cudaStream_t stream) {
+  if (ntok <= 0) return cudaSuccess;
+  rstd_kernel<<<(ntok + 7) / 8, 256, 0, stream>>>(ss, groups, ntok, eps, rstd);
+  return cudaGetLastError();
 }
 
 int gemm_pick_bn(int ntok) {

@@ -39,6 +39,7 @@ struct EpiParams {
   // kResid epilogue) writes per-(token, 32-feature group) sums of squares ss[t][g]; a GEMM with
   // ss_in reduces them to rstd[t] = 1/sqrt(sum/d + eps) before its first accumulator is ready
   const float* ss_in;      // [ntok][ss_groups] or nullptr (no norm)
+  const float* rs_in;      // [ntok] rstd already reduced (round-robin launches), or nullptr
   float* ss_out;           // kResid: [ntok][ss_groups] written for the next component, or nullptr
   int ss_groups;           // d_model / 32
   float norm_eps;
@@ -142,6 +143,10 @@ struct GemmPlan {
 
 // Launches on `stream`; returns cudaError_t.
 cudaError_t launch_gemm(const GemmLaunch& L, cudaStream_t stream);
+// rstd[t] = 1/sqrt(sum_g ss[t][g] / (32 G) + eps) for ntok tokens, in tile_rstd's exact order
+// (prefill: the round-robin GEMM tiles of one token tile would otherwise each reduce it again)
+cudaError_t launch_rstd(const float* ss, int groups, int ntok, float eps, float* rstd,
+                        cudaStream_t stream);
 
 // BN for a token count; persistent grid and workspace need for the stream-K schedule.
 int gemm_pick_bn(int ntok);
