@@ -7,8 +7,10 @@
 // end inside a tile; such partial tiles meet in an fp32 workspace (L2-resident) and the last
 // contributor to arrive runs the fused epilogue (no CTA ever waits on another).
 //
-// Warp roles (192 threads): warp 0 = TMA producer (one elected lane), warp 1 = MMA issuer (one
-// elected lane) + TMEM allocator, warps 2..5 = epilogue (warp w drains TMEM lanes 32*(w%4)..).
+// Warp roles (320 threads): warp 0 = TMA producer (one elected lane), warp 1 = MMA issuer (one
+// elected lane) + TMEM allocator, warps 2..9 = epilogue: warp w drains TMEM lanes 32*(w%4)..
+// (the lane quarter a warp may access), warps w and w+4 splitting the tile's token columns, so
+// two epilogue warps per SM sub-partition hide each other's latencies.
 // Two TMEM accumulators ping-pong so the MMA of the next tile overlaps the epilogue of this one.
 // Programmatic dependent launch: weight tiles (which no earlier kernel writes) are requested
 // before griddepcontrol.wait, so the weight stream starts under the previous kernel's tail.
@@ -313,9 +315,9 @@ __device__ __forceinline__ void qkv_chunk_rr(const EpiParams& E, int f, int t0, 
   }
 }
 
-// rs[j] = 1/sqrt(sum_g ss[n0 + j][g] / d + eps) for the BN tokens of a tile; warp q of the four
-// epilogue warps takes tokens q, q+4, ...; each lane sums groups lane, lane+32, ... then the warp
-// reduces in a fixed order (bit-reproducible).
+// rs[j] = 1/sqrt(sum_g ss[n0 + j][g] / d + eps) for the BN tokens of a tile; epilogue warp ew of
+// kEpiWarps takes tokens ew, ew + kEpiWarps, ...; each lane sums groups lane, lane+32, ... then
+// the warp reduces in a fixed order (bit-reproducible).
 // All loads are issued before any reduction (one L2 round trip): a token's groups are read as
 // float4s, lane l taking float4s l and l + 32 (ss_groups <= 256, i.e. d_model <= 8192).
 template <int BN>
@@ -324,7 +326,7 @@ __device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, flo
   const int G = E.ss_groups;
   const int G4 = G >> 2;
   const float inv_d = 1.0f / (float)(G * 32);
-  constexpr int J = BN / 4;  // tokens per warp
+  constexpr int J = (BN + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
   // wide tiles (BN > 64) in rounds of 16 tokens: all 64 at once would exceed the register file
   constexpr int JC = J < 16 ? J : 16;
 #pragma unroll 1
@@ -332,9 +334,10 @@ __device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, flo
     float s[JC];
 #pragma unroll
     for (int jj = 0; jj < JC; ++jj) {
-      const int t = n0 + q + 4 * (j0 + jj);
+      const int tt = q + kEpiWarps * (j0 + jj);
+      const int t = n0 + tt;
       const float4* p = reinterpret_cast<const float4*>(E.ss_in + (size_t)t * G);
-      const bool ok = t < E.ntok;
+      const bool ok = tt < BN && t < E.ntok;
       const float4 a = (ok && lane < G4) ? __ldcg(p + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 b = (ok && lane + 32 < G4) ? __ldcg(p + lane + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
       s[jj] = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
@@ -347,8 +350,8 @@ __device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, flo
     if (lane == 0) {
 #pragma unroll
       for (int jj = 0; jj < JC; ++jj) {
-        const int tt = q + 4 * (j0 + jj);
-        rs[tt] = n0 + tt < E.ntok ? rsqrtf(s[jj] * inv_d + E.norm_eps) : 0.f;
+        const int tt = q + kEpiWarps * (j0 + jj);
+        if (tt < BN) rs[tt] = n0 + tt < E.ntok ? rsqrtf(s[jj] * inv_d + E.norm_eps) : 0.f;
       }
     }
   }
@@ -375,7 +378,7 @@ struct SkRange {
 // flight share a few token tiles and all weight tiles stay L2-resident; the per-CTA iteration
 // range [it_begin, it_end) is then virtual (its own tiles back to back).
 template <int BN, int STAGES, int CTAS, int MODE, bool RR>
-__global__ void __launch_bounds__(192, CTAS)
+__global__ void __launch_bounds__(64 + 32 * kEpiWarps, CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
                    int rr_gm, EpiParams E) {
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(192, CTAS)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     mbar_init(fixbar, 1);
     fence_barrier_init();
@@ -560,9 +563,17 @@ __global__ void __launch_bounds__(192, CTAS)
       kb0 = 0;  // later segments start at a tile's first k-block
     }
   } else {
-    // ---------------- epilogue warps 2..5
+    // ---------------- epilogue warps 2..9
     pdl_wait();
+    constexpr int kEpiThreads = 32 * kEpiWarps;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 2;  // epilogue warp 0..kEpiWarps-1
+    // the tile's token columns split between the warps sharing a lane quarter (16-column chunks)
+    constexpr int kHalves = BN >= 16 * (kEpiWarps / 4) ? kEpiWarps / 4 : 1;
+    constexpr int CW = BN / kHalves;
+    const int half = ew / 4;
+    const int cb = half < kHalves ? half * CW : BN;  // this warp's columns [cb, ce)
+    const int ce = half < kHalves ? cb + CW : BN;
     int seg = 0;
     for (long long it = it_begin; it < it_end; ++seg) {
       const int vt = (int)((unsigned)it / (unsigned)nkb);  // it < 2^31
@@ -589,13 +600,13 @@ __global__ void __launch_bounds__(192, CTAS)
         // the tile's token positions / KV slots for the RoPE and KV stores below (one L2 round
         // trip per tile instead of one per 16-token chunk); double-buffered like rs
         int2* meta = meta_smem + (seg & 1) * BN;
-        for (int k = threadIdx.x - 64; k < BN; k += 128) {
+        for (int k = threadIdx.x - 64; k < BN; k += kEpiThreads) {
           const int t = n0 + k;
           meta[k] = t < E.ntok ? make_int2(__ldg(E.tok + (size_t)t * 5 + 3),
                                            __ldg(E.tok + (size_t)t * 5 + 2))
                                : make_int2(0, -1);
         }
-        if (E.ss_in == nullptr) named_bar_sync(2, 128);
+        if (E.ss_in == nullptr) named_bar_sync(2, kEpiThreads);
       }
       float* rs = nullptr;
       if (E.ss_in != nullptr && runs_epilogue) {
@@ -603,29 +614,29 @@ __global__ void __launch_bounds__(192, CTAS)
         // once per token by launch_rstd for round-robin launches)
         rs = rs_smem + (seg & 1) * BN;
         if (E.rs_in != nullptr) {
-          for (int k = threadIdx.x - 64; k < BN; k += 128)
+          for (int k = threadIdx.x - 64; k < BN; k += kEpiThreads)
             rs[k] = n0 + k < E.ntok ? __ldg(E.rs_in + n0 + k) : 0.f;
         } else {
-          tile_rstd<BN>(E, n0, q, rs);
+          tile_rstd<BN>(E, n0, ew, rs);
         }
-        named_bar_sync(2, 128);
+        named_bar_sync(2, kEpiThreads);
       }
       if constexpr (MODE >= kQKVLora) {
         if (runs_epilogue) {
           // the tile's LoRA u slices (its 128 rows lie in one q / k / v segment) and adapters
-          named_bar_sync(3, 128);  // the previous tile's readers are done with the buffer
-          const int et = threadIdx.x - 64;  // epilogue thread 0..127
+          named_bar_sync(3, kEpiThreads);  // the previous tile's readers are done with the buffer
+          const int et = threadIdx.x - 64;  // epilogue thread
           const int sg = m0 / E.lora_seg;
           float4* lu4 = reinterpret_cast<float4*>(lu_smem);
-          for (int k = et; k < BN * (kLoraRank / 4); k += 128) {
+          for (int k = et; k < BN * (kLoraRank / 4); k += kEpiThreads) {
             const int tt = k / (kLoraRank / 4), qq = k % (kLoraRank / 4);
             lu4[k] = n0 + tt < E.ntok
                          ? __ldg(reinterpret_cast<const float4*>(
                                E.lora_u + (size_t)(n0 + tt) * E.lora_ustride + sg * kLoraRank) + qq)
                          : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          for (int k = et; k < BN; k += 128) li_smem[k] = n0 + k < E.ntok ? __ldg(E.lora_idx + n0 + k) : -1;
-          named_bar_sync(3, 128);
+          for (int k = et; k < BN; k += kEpiThreads) li_smem[k] = n0 + k < E.ntok ? __ldg(E.lora_idx + n0 + k) : -1;
+          named_bar_sync(3, kEpiThreads);
         }
       }
       mbar_wait(&tfull[a], u & 1u);
@@ -661,22 +672,22 @@ __global__ void __launch_bounds__(192, CTAS)
             cs[i] = __ldg(E.rope + (size_t)(pos > 0 ? pos : 0) * (E.head_dim >> 1) + e2);
           }
         };
-        if (rope) load_cs(0, csa);
+        if (rope && cb < ce && n0 + cb < E.ntok) load_cs(cb, csa);
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = cb; c0 < ce; c0 += 32) {
           if (n0 + c0 >= E.ntok) break;
           float acc[16];
-          if (rope && c0 + 16 < BN && n0 + c0 + 16 < E.ntok) load_cs(c0 + 16, csb);
+          if (rope && c0 + 16 < ce && n0 + c0 + 16 < E.ntok) load_cs(c0 + 16, csb);
           tmem_ld16(t_lane + c0, acc);
           qkv_chunk_rr(E, f, n0 + c0, acc, rs ? rs + c0 : nullptr, csa, meta + c0);
-          if (c0 + 16 >= BN || n0 + c0 + 16 >= E.ntok) break;
-          if (rope && c0 + 32 < BN && n0 + c0 + 32 < E.ntok) load_cs(c0 + 32, csa);
+          if (c0 + 16 >= ce || n0 + c0 + 16 >= E.ntok) break;
+          if (rope && c0 + 32 < ce && n0 + c0 + 32 < E.ntok) load_cs(c0 + 32, csa);
           tmem_ld16(t_lane + c0 + 16, acc);
           qkv_chunk_rr(E, f, n0 + c0 + 16, acc, rs ? rs + c0 + 16 : nullptr, csb, meta + c0 + 16);
         }
       } else if (whole) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
+        for (int c0 = cb; c0 < ce; c0 += 16) {
           if (n0 + c0 >= E.ntok) break;
           float acc[16];
           tmem_ld16(t_lane + c0, acc);
@@ -710,7 +721,7 @@ __global__ void __launch_bounds__(192, CTAS)
         if ((int)blockIdx.x != c_first) {
           float4* slot = part4(blockIdx.x) + row;
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
+          for (int c0 = cb; c0 < ce; c0 += 16) {
             if (n0 + c0 >= E.ntok) break;
             float acc[16];
             tmem_ld16(t_lane + c0, acc);
@@ -719,9 +730,9 @@ __global__ void __launch_bounds__(192, CTAS)
               __stcg(slot + ((c0 >> 2) + j) * kBM,
                      make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
           }
-          // the CTA barrier orders the 128 threads' stores before one release at GPU scope
+          // the CTA barrier orders the epilogue threads' stores before one release at GPU scope
           // (release is cumulative; no sequentially-consistent fence on the hot path)
-          named_bar_sync(1, 128);
+          named_bar_sync(1, kEpiThreads);
           if (warp == 2 && lane == 0)
             asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
         } else {
@@ -733,17 +744,20 @@ __global__ void __launch_bounds__(192, CTAS)
             *ctr = 0;  // reset for the next launch / graph replay (ordered by kernel boundary)
           }
           __syncwarp();
-          named_bar_sync(1, 128);  // everyone's loads are ordered after the acquire
+          named_bar_sync(1, kEpiThreads);  // everyone's loads are ordered after the acquire
           if constexpr (BN <= 64) {
             // whole tile in registers; the contributors' partials are staged into the ring
             // (idle now: this is the CTA's last segment and its MMAs are complete) by bulk
             // copies, every partial of a round in flight at once - one L2 round trip per round
             // instead of one per contributor - and summed from shared memory in contributor
             // order (deterministic)
-            float acc[BN];
+            float acc[CW];  // this warp's columns [cb, cb + CW) (a warp past kHalves has none)
+            const bool mine = half < kHalves;
+            if (mine) {
 #pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 16)
-              tmem_ld16(t_lane + c0, *reinterpret_cast<float(*)[16]>(acc + c0));
+              for (int c = 0; c < CW; c += 16)
+                tmem_ld16(t_lane + cb + c, *reinterpret_cast<float(*)[16]>(acc + c));
+            }
             constexpr int kPartBytes = BN * kBM * 4;
             constexpr int kPerRound = STAGES * S::kStageBytes / kPartBytes;
             static_assert(kPerRound >= 1, "ring smaller than one partial tile");
@@ -762,10 +776,10 @@ __global__ void __launch_bounds__(192, CTAS)
               }
               mbar_wait(fixbar, fph);
               fph ^= 1u;
-              for (int j = 0; j < nr; ++j) {
-                const float4* p = staged + (size_t)j * (kPartBytes / 16) + row;
+              for (int j = 0; mine && j < nr; ++j) {
+                const float4* p = staged + (size_t)j * (kPartBytes / 16) + row + (cb / 4) * kBM;
 #pragma unroll
-                for (int k = 0; k < BN / 4; ++k) {
+                for (int k = 0; k < CW / 4; ++k) {
                   const float4 v = p[k * kBM];
                   acc[4 * k] += v.x;
                   acc[4 * k + 1] += v.y;
@@ -773,17 +787,17 @@ __global__ void __launch_bounds__(192, CTAS)
                   acc[4 * k + 3] += v.w;
                 }
               }
-              if (o0 + kPerRound < n_contrib) named_bar_sync(1, 128);  // the ring is reused
+              if (o0 + kPerRound < n_contrib) named_bar_sync(1, kEpiThreads);  // ring reused
             }
 #pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-              if (n0 + c0 >= E.ntok) break;
-              epilogue_chunk<MODE>(E, f, n0 + c0, *reinterpret_cast<float(*)[16]>(acc + c0),
-                                   rs ? rs + c0 : nullptr, lu_smem, li_smem, n0);
+            for (int c = 0; c < CW; c += 16) {
+              if (!mine || n0 + cb + c >= E.ntok) break;
+              epilogue_chunk<MODE>(E, f, n0 + cb + c, *reinterpret_cast<float(*)[16]>(acc + c),
+                                   rs ? rs + cb + c : nullptr, lu_smem, li_smem, n0);
             }
           } else {
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
+          for (int c0 = cb; c0 < ce; c0 += 16) {
             if (n0 + c0 >= E.ntok) break;
             float acc[16];
             tmem_ld16(t_lane + c0, acc);  // the owner's share is contributor 0
@@ -851,7 +865,7 @@ static cudaError_t launch_bn_rr(const GemmLaunch& L, cudaStream_t stream) {
   const int n_tiles = (L.epi.ntok + BN - 1) / BN;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(L.grid, 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
+  cfg.blockDim = dim3(64 + 32 * kEpiWarps, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

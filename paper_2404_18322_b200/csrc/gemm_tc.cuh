@@ -80,6 +80,7 @@ struct EpiParams {
   LoraTable lora_b;
 };
 
+constexpr int kEpiWarps = 8;  // epilogue warps per CTA (two per TMEM lane quarter)
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 
