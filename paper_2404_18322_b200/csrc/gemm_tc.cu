@@ -7,10 +7,11 @@
 // end inside a tile; such partial tiles meet in an fp32 workspace (L2-resident) and the last
 // contributor to arrive runs the fused epilogue (no CTA ever waits on another).
 //
-// Warp roles (320 threads): warp 0 = TMA producer (one elected lane), warp 1 = MMA issuer (one
-// elected lane) + TMEM allocator, warps 2..9 = epilogue: warp w drains TMEM lanes 32*(w%4)..
-// (the lane quarter a warp may access), warps w and w+4 splitting the tile's token columns, so
-// two epilogue warps per SM sub-partition hide each other's latencies.
+// Warp roles (64 + 32 * epi_warps<BN>() threads): warp 0 = TMA producer (one elected lane), warp
+// 1 = MMA issuer (one elected lane) + TMEM allocator, warps 2.. = epilogue: warp w drains TMEM
+// lanes 32*(w%4).. (the lane quarter a warp may access), the warps sharing a quarter splitting
+// the tile's token columns, so several epilogue warps per SM sub-partition hide each other's
+// latencies (the owners' fixup + epilogue is each decode launch's exposed tail).
 // Two TMEM accumulators ping-pong so the MMA of the next tile overlaps the epilogue of this one.
 // Programmatic dependent launch: weight tiles (which no earlier kernel writes) are requested
 // before griddepcontrol.wait, so the weight stream starts under the previous kernel's tail.
@@ -316,7 +317,7 @@ __device__ __forceinline__ void qkv_chunk_rr(const EpiParams& E, int f, int t0, 
 }
 
 // rs[j] = 1/sqrt(sum_g ss[n0 + j][g] / d + eps) for the BN tokens of a tile; epilogue warp ew of
-// kEpiWarps takes tokens ew, ew + kEpiWarps, ...; each lane sums groups lane, lane+32, ... then
+// epi_warps<BN>() takes tokens ew, ew + epi_warps<BN>(), ...; each lane sums groups lane, lane+32, ... then
 // the warp reduces in a fixed order (bit-reproducible).
 // All loads are issued before any reduction (one L2 round trip): a token's groups are read as
 // float4s, lane l taking float4s l and l + 32 (ss_groups <= 256, i.e. d_model <= 8192).
@@ -326,6 +327,7 @@ __device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, flo
   const int G = E.ss_groups;
   const int G4 = G >> 2;
   const float inv_d = 1.0f / (float)(G * 32);
+  constexpr int kEpiWarps = epi_warps<BN>();
   constexpr int J = (BN + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
   // wide tiles (BN > 64) in rounds of 16 tokens: all 64 at once would exceed the register file
   constexpr int JC = J < 16 ? J : 16;
@@ -378,7 +380,7 @@ struct SkRange {
 // flight share a few token tiles and all weight tiles stay L2-resident; the per-CTA iteration
 // range [it_begin, it_end) is then virtual (its own tiles back to back).
 template <int BN, int STAGES, int CTAS, int MODE, bool RR>
-__global__ void __launch_bounds__(64 + 32 * kEpiWarps, CTAS)
+__global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
                    int rr_gm, EpiParams E) {
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, CTAS)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], epi_warps<BN>());
     }
     mbar_init(fixbar, 1);
     fence_barrier_init();
@@ -563,13 +565,14 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, CTAS)
       kb0 = 0;  // later segments start at a tile's first k-block
     }
   } else {
-    // ---------------- epilogue warps 2..9
+    // ---------------- epilogue warps 2 .. 1 + epi_warps<BN>()
     pdl_wait();
+    constexpr int kEpiWarps = epi_warps<BN>();
     constexpr int kEpiThreads = 32 * kEpiWarps;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int ew = warp - 2;  // epilogue warp 0..kEpiWarps-1
     // the tile's token columns split between the warps sharing a lane quarter (16-column chunks)
-    constexpr int kHalves = BN >= 16 * (kEpiWarps / 4) ? kEpiWarps / 4 : 1;
+    constexpr int kHalves = BN / 16 < kEpiWarps / 4 ? BN / 16 : kEpiWarps / 4;
     constexpr int CW = BN / kHalves;
     const int half = ew / 4;
     const int cb = half < kHalves ? half * CW : BN;  // this warp's columns [cb, ce)
@@ -865,7 +868,7 @@ static cudaError_t launch_bn_rr(const GemmLaunch& L, cudaStream_t stream) {
   const int n_tiles = (L.epi.ntok + BN - 1) / BN;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(L.grid, 1, 1);
-  cfg.blockDim = dim3(64 + 32 * kEpiWarps, 1, 1);
+  cfg.blockDim = dim3(64 + 32 * epi_warps<BN>(), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
