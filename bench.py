@@ -852,7 +852,10 @@ def run_ours(args, world, rank, local):
             roofline["note"] = ("achieved: the family's launches bracketed by CUDA events on "
                                 "the runner's stream (one extra step, no graph, no PDL overlap)")
         except Exception as exc:  # diagnostics only
-            prof["families"]["_in_step_timeline"] = {"error": str(exc)}
+            msg = str(exc)
+            prof["families"]["_in_step_timeline"] = (
+                {"skipped": "a second runner of this config does not fit beside the measured one"}
+                if "out of device memory" in msg else {"error": msg})
     kr = kernel_rooflines(ctx, wl, peaks) if rank == 0 and args.isolated else {}
     live = spec = None
     if world == 1 and not args.no_live:
