@@ -82,7 +82,10 @@ std::vector<int> KvStore::reserve_slots(std::uint64_t request, const std::string
                                         const std::string& pool_key, int device,
                                         int total_pages) {
   std::vector<int> row = page_slots(request, block);
-  auto& r = reserved_[{request, block}];
+  auto rit = reserved_.find({request, block});
+  if (rit == reserved_.end() && static_cast<int>(row.size()) >= total_pages)
+    return row;  // nothing reserved and nothing to reserve (the common decode step)
+  auto& r = rit != reserved_.end() ? rit->second : reserved_[{request, block}];
   if (r.slots.empty()) {
     r.pool_key = pool_key;
     r.device = device;
@@ -262,6 +265,7 @@ std::vector<int> KvStore::page_slots(std::uint64_t request, const std::string& b
   std::vector<int> out;
   const Segment* s = find(request, block);
   if (!s) return out;
+  out.reserve(s->page_ids.size());
   for (std::uint64_t id : s->page_ids) out.push_back(pages_.at(id).slot);
   return out;
 }

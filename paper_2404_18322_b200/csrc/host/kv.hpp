@@ -8,6 +8,7 @@
 #pragma once
 #include <cstdint>
 #include <map>
+#include <unordered_map>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -123,7 +124,7 @@ class KvStore {
   };
   std::map<std::pair<std::uint64_t, std::string>, Reserved> reserved_;
   std::map<std::pair<std::uint64_t, std::string>, Segment> segments_;
-  std::map<std::uint64_t, Page> pages_;
+  std::unordered_map<std::uint64_t, Page> pages_;  // looked up by id only (never iterated)
   std::map<std::pair<std::string, int>, SlotPool> pools_;
   std::map<int, std::int64_t> used_;
   std::map<int, std::int64_t> capacity_;
