@@ -127,6 +127,18 @@ int KvStore::append_tokens(std::uint64_t request, const std::string& block, int 
   return added;
 }
 
+bool KvStore::append_if_present(std::uint64_t request, const std::string& block, int n) {
+  if (n < 0) throw KvError("negative token append");
+  auto it = segments_.find({request, block});
+  if (it == segments_.end()) return false;
+  Segment& s = it->second;
+  s.tokens += n;
+  const int need = pages_for(s.tokens);
+  while (static_cast<int>(s.page_ids.size()) < need)
+    s.page_ids.push_back(new_page(request, block, s, s.device));
+  return true;
+}
+
 int KvStore::share_prefix(std::uint64_t request, std::uint64_t from, const std::string& block,
                           int tokens) {
   Segment& dst = seg(request, block);

@@ -62,6 +62,8 @@ class KvStore {
                       std::int64_t bytes_per_token, const std::string& pool_key = "");
   bool has_segment(std::uint64_t request, const std::string& block) const;
   int append_tokens(std::uint64_t request, const std::string& block, int n);
+  // append_tokens on the segment if it exists (one lookup); false when there is none
+  bool append_if_present(std::uint64_t request, const std::string& block, int n);
   int share_prefix(std::uint64_t request, std::uint64_t from, const std::string& block,
                    int tokens);
   void release(std::uint64_t request, const std::string& block);

@@ -714,10 +714,7 @@ void Runner::advance_from(Request& r, int step) {
     return;
   }
   // decode token done: one more token on every segment of the chain
-  for (int s = 0; s < chain_len(r); ++s) {
-    const std::string& bn = names_[chain_block(r, s)];
-    if (kv_.has_segment(r.id, bn)) kv_.append_tokens(r.id, bn, 1);
-  }
+  for (int s = 0; s < chain_len(r); ++s) kv_.append_if_present(r.id, names_[chain_block(r, s)], 1);
   r.generated += 1;
   ++tokens_generated_;
   r.ctx += 1;
