@@ -120,7 +120,7 @@ class Runner {
   int chain_block(const Request& r, int step) const { return chain_blocks_[chain_ptr_[r.tenant] + step]; }
 
   be_ctx* ctx_;
-  cudaStream_t st_;
+  cudaStream_t st_ = nullptr;
   bool dry_ = false;  // control plane only
   std::vector<std::string> comps_;
   std::vector<std::int64_t> kv_bpt_;  // per block
