@@ -859,7 +859,10 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
   if (e != cudaSuccess) return fail(ctx, BE_ERR_CUDA, "gather: %s", cudaGetErrorString(e));
 
   const int max_pages = pt_stride;
-  const int splits = attn_splits(ctx, ntok, H, max_pages);
+  int splits = attn_splits(ctx, ntok, H, max_pages);
+  // a forced split count (tests / experiments) applies where its partials fit (decode sizes)
+  if (ctx->attn_splits_force > 0 && (size_t)ntok * H * splits * (hd + 2) > ws->attn_part_elems)
+    splits = 1;
   if ((size_t)ntok * H * splits * (hd + 2) > ws->attn_part_elems && splits > 1)
     return fail(ctx, BE_ERR_INVALID, "attention partial buffer too small");
 
