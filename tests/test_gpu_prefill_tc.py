@@ -60,9 +60,12 @@ def rel(a, b):
 
 @pytest.mark.parametrize("prompts,start", [([300, 17, 129, 1, 256], 0), ([90, 200], 40),
                                            ([700], 0)])
-def test_tcgen05_prefill_matches_other_kernels_and_oracle(prompts, start):
+@pytest.mark.parametrize("mode", [1, 3])
+def test_tcgen05_prefill_matches_other_kernels_and_oracle(prompts, start, mode):
+    """mode 1: the warp-specialised kernel (one CTA per SM, S double-buffered); 3: two CTAs per
+    SM."""
     from oracle import oracle as O
-    tc = run(1, prompts, start)
+    tc = run(mode, prompts, start)
     ref = run(2, prompts, start)
     rowk = run(0, prompts, start)
     for (x1, y1, _), (x2, y2, _), (x3, y3, _) in zip(tc, ref, rowk):
