@@ -111,9 +111,9 @@ struct be_ctx {
   int* gemm_counters = nullptr;
   int gemm_grid_cap = 0;  // 0 = one persistent CTA per SM (BE_GEMM_GRID overrides)
   int use_pdl = 1;        // programmatic dependent launch of GEMMs (BE_PDL=0 disables)
-  int prefill_tc = 1;     // prefill attention (BE_PREFILL_TC): 1 tcgen05 warp-specialised, one
-                          // CTA per SM (hd 128; mma.sync for hd 64), 3 tcgen05 two CTAs per SM,
-                          // 2 mma.sync, 0 the per-row decode kernel
+  int prefill_tc = 1;     // prefill attention (BE_PREFILL_TC): 1 tcgen05, two CTAs per SM (hd
+                          // 128; mma.sync for hd 64), 4 tcgen05 warp-specialised one CTA per SM
+                          // (experiment: slower), 2 mma.sync, 0 the per-row decode kernel
   int attn_splits_force = 0;  // decode attention split-K count (BE_ATTN_SPLITS=1..16; 0 = auto)
   // per-launch event timing of exec_batch kernels (be_prof_enable); off on the hot path
   struct ProfRec {
@@ -997,7 +997,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
     if (ap.tl != nullptr && splits > 1) tl_slot(ctx, BE_K_ATTENTION);  // combine's slot = tl + 1
     {
       ProfScope ps(ctx, st, BE_K_ATTENTION, ntok, H, hd, 0, 0);
-      if (phase == BE_PHASE_PREFILL && n_grp == 1 && (ctx->prefill_tc == 1 || ctx->prefill_tc == 3) &&
+      if (phase == BE_PHASE_PREFILL && n_grp == 1 && (ctx->prefill_tc == 1 || ctx->prefill_tc == 4) &&
           hd == 128) {
         // prompt rows on tcgen05: S and O in TMEM, Q / K / V tiles by TMA
         if (!ws->has_m_q) {
@@ -1031,7 +1031,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
         pt.scale_log2 = ap.scale_log2;
         pt.out = ws->attn;
         pt.tiles = ws->prefill_tiles;
-        e = ctx->prefill_tc == 1
+        e = ctx->prefill_tc == 4
                 ? bx::launch_attention_prefill_pipe(pt, ws->m_q, pool->m_kv, ctx->num_sms, st)
                 : bx::launch_attention_prefill_tc(pt, ws->m_q, pool->m_kv, ctx->num_sms, st);
       } else if (phase == BE_PHASE_PREFILL && n_grp == 1 && ctx->prefill_tc) {

@@ -60,10 +60,10 @@ def rel(a, b):
 
 @pytest.mark.parametrize("prompts,start", [([300, 17, 129, 1, 256], 0), ([90, 200], 40),
                                            ([700], 0)])
-@pytest.mark.parametrize("mode", [1, 3])
+@pytest.mark.parametrize("mode", [1, 4])
 def test_tcgen05_prefill_matches_other_kernels_and_oracle(prompts, start, mode):
-    """mode 1: the warp-specialised kernel (one CTA per SM, S double-buffered); 3: two CTAs per
-    SM."""
+    """mode 1: two CTAs per SM (the default); 4: the warp-specialised kernel (one CTA per SM, S
+    double-buffered in TMEM, loader and MMA warps)."""
     from oracle import oracle as O
     tc = run(mode, prompts, start)
     ref = run(2, prompts, start)
