@@ -630,6 +630,20 @@ def run_cluster(args, world, rank, local):
                "d2h_bytes_per_step": int(hout.numel() * 2),
                "ms_per_step": round(e_ms / args.steps, 4)}
     launches = int(stats["launches"])
+    roofline = None
+    if rank == 0 and not args.no_roofline:
+        # the dominant kernel family of this rank's home runner (the shared blocks over its own
+        # rows), one extra step of that runner with every launch bracketed by CUDA events; the
+        # cluster is closed right after, so its desynchronised state is never used again
+        try:
+            home_wl = plan.runner(rank, 0).wl
+            roofline = profile_step(ctx, home, home_wl, stream, peaks, peaks_kind)["roofline"]
+            roofline["note"] = ("rank 0's home runner (shared blocks over its own rows): launches "
+                                "bracketed by CUDA events on its stream (no graph, no PDL overlap)")
+            roofline["traffic"] = None
+            roofline["traffic_source"] = None
+        except Exception as exc:  # diagnostics only
+            roofline = {"error": str(exc)}
     cl.close()
     replicas = None
     if not args.no_replicas:
@@ -664,7 +678,7 @@ def run_cluster(args, world, rank, local):
             "config_detail": {"placement": plan.note, "processes": "one per GPU",
                               "hop_bytes_per_step_rank0": {"nccl_sent": sent,
                                                            "nccl_recv": recv}},
-            "roofline": None,
+            "roofline": roofline,
             "step_roofline": {"bound": "hbm", "bytes_per_step_max_gpu": step_bytes_max,
                               "achieved": round(step_bytes_max / (ms_step / 1e3) / 1e9, 1),
                               "peak": hbm, "unit": "GB/s",
