@@ -94,23 +94,52 @@ def shared_blocks(wl: Workload) -> set[int]:
     return {b for b, ts in seen.items() if len(ts) > 1}
 
 
-def place_blocks(wl: Workload, world: int, hbm_bytes: int = 180 * 10**9) -> list[int]:
-    """Block -> rank (-1: an instance on every rank). Private blocks by the reference's locality
-    rule (bh_policy_choose_device = Scheduler::choose_device, scheduler.cpp:262-314), in chain
-    order, each placement charged to its device's ledger before the next choice."""
+def place_blocks(wl: Workload, world: int, hbm_bytes: int = 180 * 10**9,
+                 trace: list | None = None) -> list[int]:
+    """Block -> rank (-1: an instance on every rank).
+    Shared blocks follow the reference's scale-out (bh_policy_scale_decisions =
+    Scheduler::scale_decisions, scheduler.cpp:227-260): each starts as one instance on rank 0
+    holding the decode queue of every rank's requests (weak scaling: world x the config's rows);
+    an instance whose queued work exceeds one GPU's rows is hot and gets a replica on the device
+    choose_device(most free) picks, the queue splitting over the replicas, until none is hot - on
+    a server with room that is every rank. Private blocks by the locality rule
+    (bh_policy_choose_device, scheduler.cpp:262-314), in chain order, each placement charged to
+    its device's ledger before the next choice. `trace` (optional) receives the scale-out
+    decisions as (round, instance, device)."""
     from .pipeline import routing_policy
     if world == 1:
         return [-1] * len(wl.block_names)  # one GPU holds every block: no leg ever leaves it
     shared = shared_blocks(wl)
-    pol = routing_policy(wl, world, instances=False, hbm_bytes=hbm_bytes)
+    rows = wl.n_requests  # each rank's decode rows per step
+    pol = routing_policy(wl, world, instances=False, hbm_bytes=hbm_bytes, scale_queue_us=rows)
     used = [0] * world
     seq = 0
-    for b in sorted(shared):
+    replicas = {b: [0] for b in sorted(shared)}
+    for b in replicas:
+        used[0] += wl.shape.param_bytes
+    for rnd in range(world):
         for dev in range(world):
-            seq += 1
-            pol.put_instance(f"r{dev}.{wl.block_names[b]}", wl.block_names[b], dev, ready=True,
-                             created_seq=seq)
-            used[dev] += wl.shape.param_bytes
+            pol.set_ledger(dev, used[dev])
+        for b, devs in replicas.items():
+            for dev in devs:
+                seq += 1
+                pol.put_instance(f"r{dev}.{wl.block_names[b]}", wl.block_names[b], dev,
+                                 ready=True, created_seq=seq, queue_len=world * rows // len(devs),
+                                 queued_cost_us=world * rows / len(devs))
+        decisions = pol.scale_decisions()
+        if not decisions:
+            break
+        for inst, dev in decisions:
+            b = wl.block_names.index(inst.split(".", 1)[1])
+            if dev not in replicas[b]:
+                replicas[b].append(dev)
+                used[dev] += wl.shape.param_bytes
+                if trace is not None:
+                    trace.append((rnd, inst, dev))
+    for b, devs in replicas.items():
+        if len(devs) != world:
+            raise ValueError(f"{wl.name}: scale-out left block {wl.block_names[b]} on ranks "
+                             f"{sorted(devs)} only (the plan needs shared blocks on every rank)")
     for dev in range(world):
         pol.set_ledger(dev, used[dev])
     place = [-1] * len(wl.block_names)

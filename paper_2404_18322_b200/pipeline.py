@@ -112,7 +112,8 @@ def _profile_classes(path: str | None):
 
 def routing_policy(wl: Workload, n_devices: int, profiles: str | None = None,
                    hbm_bytes: int = 180 * 10**9, instances: bool = True,
-                   speculation: bool = False, spec_fraction: float = 0.10):
+                   speculation: bool = False, spec_fraction: float = 0.10,
+                   scale_queue_us: int = 0):
     """A bh_policy (include/blockpolicy.h) describing replica placement of `wl`: every block on
     each of n_devices GPUs of one NVLink server, priced by the measured B200 cost profiles
     (profiles/b200_profiles.json, scripts/make_profiles.py; §8(f) rank 2). Classes the profile
@@ -121,7 +122,8 @@ def routing_policy(wl: Workload, n_devices: int, profiles: str | None = None,
     s = wl.shape
     d = s.d_model
     prof = _profile_classes(profiles)
-    pol = Policy(adaptive=False, speculation=speculation, spec_fraction=spec_fraction)
+    pol = Policy(adaptive=False, speculation=speculation, spec_fraction=spec_fraction,
+                 scale_queue_us=scale_queue_us)
     att_bytes, ffn_bytes = 2 * 4 * d * d, 2 * 3 * d * s.d_ff
     for kind, wbytes, kv in (("attention", att_bytes, 4 * d), ("ffn", ffn_bytes, 0)):
         key = f"{kind}:{d}"

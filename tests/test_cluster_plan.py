@@ -184,3 +184,22 @@ def test_prefill_phases_move_prompt_rows():
     assert all(h[4] == ARENA_DECODE for h in pre[1])
     rows = sum(h[8] for h in pre[0]) // 32
     assert rows == 2 * wl.n_requests  # every request of both ranks reaches its private leg
+
+
+def test_shared_blocks_replicated_by_the_reference_scale_out():
+    """place_blocks replicates the shared blocks through bh_policy_scale_decisions (the
+    reference's Scheduler::scale_decisions): one instance per shared block on rank 0 holding
+    every rank's decode queue is hot; each round adds replicas on the most-free devices until
+    every rank holds one (weak scaling: each replica then serves one rank's rows)."""
+    from paper_2404_18322_b200.cluster import place_blocks, shared_blocks
+    from paper_2404_18322_b200.workloads import CONFIGS
+    wl = CONFIGS["c2"](prompt=64, output=8)
+    shared = shared_blocks(wl)
+    for world in (2, 4, 8):
+        trace = []
+        place = place_blocks(wl, world, trace=trace)
+        assert all(place[b] == -1 for b in shared)
+        assert len(trace) == len(shared) * (world - 1)
+        for b in shared:
+            devs = sorted(d for _, inst, d in trace if inst.endswith("." + wl.block_names[b]))
+            assert devs == list(range(1, world))
