@@ -31,6 +31,28 @@ __device__ __forceinline__ void stamp(const EpiParams& E, int idx) {
     E.trace[blockIdx.x * 8 + idx] = t;
   }
 }
+#ifdef BE_EXP_RR_TRACE  // experiments (scripts/rr_trace.py): per-tile stamps of CTA 0 in
+                        // round-robin launches of the epilogue mode named by the macro's value
+__device__ unsigned long long g_rr_trace[64][6];
+__device__ unsigned long long g_rr_ld[64];
+__device__ __forceinline__ void rr_stamp(int seg, int k) {
+  if (blockIdx.x == 0 && seg < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_rr_trace[seg][k] = t;
+  }
+}
+extern "C" int be_exp_rr_trace(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_rr_trace, sizeof(g_rr_trace));
+}
+extern "C" int be_exp_rr_ld(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_rr_ld, sizeof(g_rr_ld));
+}
+#define RR_STAMP(seg, k) \
+  if (RR && MODE == BE_EXP_RR_TRACE) rr_stamp(seg, k)
+#else
+#define RR_STAMP(seg, k)
+#endif
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -532,8 +554,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
       const int kb1 = (int)((nkb - kb0) < left ? nkb : kb0 + left);
       const int a = seg & 1;
       const uint32_t u = (uint32_t)(seg >> 1);
+      if (lane == 0) RR_STAMP(seg, 0);
       mbar_wait(&tempty[a], (u & 1u) ^ 1u);
       tc_fence_after();
+      if (lane == 0) RR_STAMP(seg, 1);
       const uint32_t tacc = tmem_base + (uint32_t)(a * BN);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[s], ph);
@@ -553,7 +577,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
           (void)tacc;
 #endif
           umma_commit(&empty[s]);
-          if (kb == kb1 - 1) umma_commit(&tfull[a]);
+          if (kb == kb1 - 1) {
+            umma_commit(&tfull[a]);
+            RR_STAMP(seg, 5);
+          }
         }
         __syncwarp();
         if (++s == STAGES) {
@@ -642,8 +669,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
           named_bar_sync(3, kEpiThreads);
         }
       }
+      if (warp == 2 && lane == 0) RR_STAMP(seg, 2);
       mbar_wait(&tfull[a], u & 1u);
       tc_fence_after();
+      if (warp == 2 && lane == 0) RR_STAMP(seg, 3);
       if (warp == 2 && lane == 0) stamp(E, 4);  // overwritten: the last segment's accumulator
       __syncwarp();
 #if defined(BE_EXP_NO_EPI) || defined(BE_EXP_NO_EPI_MODE)
@@ -832,6 +861,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
       }
       tc_fence_before();
       __syncwarp();
+      if (warp == 2 && lane == 0) RR_STAMP(seg, 4);
       if (lane == 0) mbar_arrive(&tempty[a]);
     }
     if (warp == 2 && lane == 0) stamp(E, 5);

@@ -42,6 +42,6 @@ tr = buf.astype(np.int64)
 tr = tr[tr[:, 5] > 0]
 t0 = tr[0, 0]
 print(f"{len(tr)} tiles of CTA 0 (us from its first tile)")
-print(" tile  mma_wait_acc  mma(start->commit)  epi_wait_acc  epilogue  (of which TMEM loads)")
+print(" tile  mma_wait_acc  mma(start->commit)  epi_wait_acc  epilogue  (warp 2)")
 for i, r in enumerate(tr):
-    print(f"{i:5d} {(r[1]-r[0])/1e3:12.2f} {(r[5]-r[1])/1e3:18.2f} {(r[3]-r[2])/1e3:13.2f} {(r[4]-r[3])/1e3:9.2f} {ld[i]/1e3:9.2f}")
+    print(f"{i:5d} {(r[1]-r[0])/1e3:12.2f} {(r[5]-r[1])/1e3:18.2f} {(r[3]-r[2])/1e3:13.2f} {(r[4]-r[3])/1e3:9.2f}")
