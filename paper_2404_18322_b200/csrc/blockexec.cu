@@ -831,6 +831,19 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
   // grouped blocks stream their own weights per n-tile (BN = rows per block); LoRA variants of one
   // base share its weights, so their rows form one matrix streamed once
   const int bn = n_grp > 1 && lora == nullptr ? grp_rows : bx::gemm_pick_bn(ntok);
+  // narrow GEMMs (O, down: N = d, <= 40 weight tiles) at 129-256 rows: 128-token tiles halve the
+  // split-tile partials (128 KB at 256 tokens) the stream-K owners must read; wide GEMMs keep
+  // 256-token tiles (one weight stream). Prefill widths (round-robin) are unaffected.
+  static const bool kNarrowBn128 = [] {
+    const char* e = getenv("BE_GEMM_NARROW_BN128");
+    return e ? atoi(e) != 0 : true;
+  }();
+  auto bn_narrow = [&](int N) {
+    return kNarrowBn128 && n_grp == 1 && lora == nullptr && bn == 256 && ntok <= 256 &&
+                   N / bx::kBM <= 40
+               ? 128
+               : bn;
+  };
   const int wcopies = lora != nullptr ? 1 : n_grp;  // weight streams per GEMM (byte accounting)
   if (n_grp > 1) {
     if (n_grp > bx::kMaxGroup || ntok % n_grp != 0 || (grp_rows != 16 && grp_rows != 32 && grp_rows != 64))
@@ -921,7 +934,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
         ed.tl_cap = ctx->tl_cap;
         ProfScope ps(ctx, st, BE_K_GEMM_DOWN, ntok, d, F, gemm_bytes(d, F, ntok) + 2.0 * (wcopies - 1) * (d) * (F),
                      2.0 * (d) * (F) * ntok);
-        rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn], d, F, ntok, bn, ed, st);
+        rc = run_gemm(ctx, ws, L.wd, &ws->m_h[bn_narrow(d)], d, F, ntok, bn_narrow(d), ed, st);
       }
       if (rc != BE_OK) return rc;
       continue;
@@ -1088,7 +1101,7 @@ int exec_dev(be_ctx* ctx, int n_grp, be_block* const* blks, be_kv_pool* const* p
         eo.tl_cap = ctx->tl_cap;
         ProfScope ps(ctx, st, BE_K_GEMM_O, ntok, d, d, gemm_bytes(d, d, ntok) + 2.0 * (wcopies - 1) * (d) * (d),
                      2.0 * (d) * (d) * ntok);
-      rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn], d, d, ntok, bn, eo, st);
+      rc = run_gemm(ctx, ws, L.wo, &ws->m_attn[bn_narrow(d)], d, d, ntok, bn_narrow(d), eo, st);
     }
     if (rc != BE_OK) return rc;
   }

@@ -21,7 +21,7 @@ ctx = dev.Context(0)
 out = {"lib": os.environ.get("BE_LIB_PATH", "default")}
 for name, N, K in [("o", 4096, 4096), ("qkv", 12288, 4096), ("gate_up", 22016, 4096),
                    ("down", 4096, 11008)]:
-    for M in (64, 16):
+    for M in [int(m) for m in os.environ.get("BE_FLOOR_M", "64,16").split(",")]:
         # BE_FLOOR_L2=1: one weight copy, re-read every launch (L2-resident when it fits)
         copies = 1 if os.environ.get("BE_FLOOR_L2") else max(2, int(3 * 126e6 / (N * K * 2)) + 1)
         ws = [dev.pack_weight(ctx, (torch.rand(N, K, device="cuda", dtype=torch.bfloat16) - 0.5)
@@ -35,7 +35,8 @@ for name, N, K in [("o", 4096, 4096), ("qkv", 12288, 4096), ("gate_up", 22016, 4
               ctx.h)
         mb = 2 * (N * K + M * K + M * N) / 1e6
         out[f"{name}_m{M}"] = {"us": round(us.value, 2), "MB": round(mb, 1),
-                               "GBps": round(mb * 1e3 / us.value, 0)}
+                               "GBps": round(mb * 1e3 / us.value, 0),
+                               "TFLOPs": round(2 * M * N * K / us.value / 1e6, 1)}
         del ws
         torch.cuda.empty_cache()
 print(json.dumps(out))
