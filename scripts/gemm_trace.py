@@ -10,6 +10,8 @@ from paper_2404_18322_b200 import device as dev  # noqa: E402
 
 ctx = dev.Context(0)
 shapes = [(4096, 4096, 64), (4096, 4096, 16), (12288, 4096, 64), (22016, 4096, 64), (4096, 11008, 64)]
+if os.environ.get("BE_TRACE_SHAPES"):  # e.g. "12288x4096x256,22016x4096x256"
+    shapes = [tuple(int(v) for v in sh.split("x")) for sh in os.environ["BE_TRACE_SHAPES"].split(",")]
 for N, K, M in shapes:
     w = dev.pack_weight(ctx, (torch.rand(N, K, device="cuda", dtype=torch.bfloat16) - 0.5) * 0.05)
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
