@@ -343,13 +343,12 @@ __device__ __forceinline__ void qkv_chunk_rr(const EpiParams& E, int f, int t0, 
 // the warp reduces in a fixed order (bit-reproducible).
 // All loads are issued before any reduction (one L2 round trip): a token's groups are read as
 // float4s, lane l taking float4s l and l + 32 (ss_groups <= 256, i.e. d_model <= 8192).
-template <int BN>
+template <int BN, int kEpiWarps>
 __device__ __forceinline__ void tile_rstd(const EpiParams& E, int n0, int q, float* rs) {
   const int lane = threadIdx.x & 31;
   const int G = E.ss_groups;
   const int G4 = G >> 2;
   const float inv_d = 1.0f / (float)(G * 32);
-  constexpr int kEpiWarps = epi_warps<BN>();
   constexpr int J = (BN + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
   // wide tiles (BN > 64) in rounds of 16 tokens: all 64 at once would exceed the register file
   constexpr int JC = J < 16 ? J : 16;
@@ -402,7 +401,7 @@ struct SkRange {
 // flight share a few token tiles and all weight tiles stay L2-resident; the per-CTA iteration
 // range [it_begin, it_end) is then virtual (its own tiles back to back).
 template <int BN, int STAGES, int CTAS, int MODE, bool RR>
-__global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
+__global__ void __launch_bounds__(64 + 32 * epi_warps<BN, RR>(), CTAS)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ wpk,
                    const __grid_constant__ CUtensorMap map_x, int K, int m_tiles, int n_tiles,
                    int rr_gm, EpiParams E) {
@@ -468,7 +467,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], epi_warps<BN>());
+      mbar_init(&tempty[a], epi_warps<BN, RR>());
     }
     mbar_init(fixbar, 1);
     fence_barrier_init();
@@ -594,7 +593,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
   } else {
     // ---------------- epilogue warps 2 .. 1 + epi_warps<BN>()
     pdl_wait();
-    constexpr int kEpiWarps = epi_warps<BN>();
+    constexpr int kEpiWarps = epi_warps<BN, RR>();
     constexpr int kEpiThreads = 32 * kEpiWarps;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int ew = warp - 2;  // epilogue warp 0..kEpiWarps-1
@@ -647,7 +646,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<BN>(), CTAS)
           for (int k = threadIdx.x - 64; k < BN; k += kEpiThreads)
             rs[k] = n0 + k < E.ntok ? __ldg(E.rs_in + n0 + k) : 0.f;
         } else {
-          tile_rstd<BN>(E, n0, ew, rs);
+          tile_rstd<BN, kEpiWarps>(E, n0, ew, rs);
         }
         named_bar_sync(2, kEpiThreads);
       }
@@ -898,7 +897,7 @@ static cudaError_t launch_bn_rr(const GemmLaunch& L, cudaStream_t stream) {
   const int n_tiles = (L.epi.ntok + BN - 1) / BN;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(L.grid, 1, 1);
-  cfg.blockDim = dim3(64 + 32 * epi_warps<BN>(), 1, 1);
+  cfg.blockDim = dim3(64 + 32 * epi_warps<BN, RR>(), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

@@ -80,12 +80,16 @@ struct EpiParams {
   LoraTable lora_b;
 };
 
-// epilogue warps per CTA: two per TMEM lane quarter (4 -> 8 warps: decode step +4-5%). Four per
-// quarter measured -1% .. +2% on the decode step across boxes (and spills in the LoRA modes),
-// slower on prefill: kept at two.
-template <int BN>
+#ifndef BE_GEMM_WIDE_EPI16
+#define BE_GEMM_WIDE_EPI16 1  // stream-K launches of 128/256-token tiles: four warps per quarter
+#endif
+// epilogue warps per CTA: two per TMEM lane quarter (4 -> 8 warps: decode step +4-5%); four per
+// quarter for stream-K launches of 128/256-token tiles (C5's 256-row decode: the owners' 128
+// columns per thread were the launch tail; +1.4% C5), not for the 16-64-token decode tiles (-1%
+// .. +2% across boxes, spills in the LoRA modes) nor for the round-robin prefill (slower).
+template <int BN, bool RR = false>
 __host__ __device__ constexpr int epi_warps() {
-  return 8;
+  return BE_GEMM_WIDE_EPI16 && BN >= 128 && !RR ? 16 : 8;
 }
 constexpr int kBM = 128;
 constexpr int kBK = 64;
